@@ -1,0 +1,156 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (needs /root/reference):
+
+    python tests/golden/make_golden.py
+
+It imports `qcfuse` from /root/reference/pkg/src read-only, runs the reference's
+own fused path (`FusionEngine.run("QCFuse", …)`, `assemble_context`,
+`probe_query`, `score_critical`, `recompute_selected`) on seeded synthetic
+inputs, and writes small `.npz` fixtures next to this script. Nothing under
+/root/reference is copied; the reference's own known-answer file
+`tests/data/golden_logits_ab.json` is re-serialised as data.
+"""
+
+from __future__ import annotations
+
+import json
+import shutil
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg")
+HERE = Path(__file__).resolve().parent
+
+
+def _import_reference():
+    sys.path.insert(0, str(REF / "src"))
+    import qcfuse.fusion as fusion  # noqa: E402
+    import qcfuse.model as model  # noqa: E402
+    import qcfuse.store as store  # noqa: E402
+    return model, store, fusion
+
+
+def _case(model, store_mod, fusion, cfg_kwargs, chunk_sizes, n_query, ratio,
+          anchor_ratio, chunk_seed0, query_seed, max_new, full_rows: bool):
+    cfg = model.ModelConfig(**cfg_kwargs)
+    w = model.init_weights(cfg)
+    tmp = Path(tempfile.mkdtemp(prefix="qcf-golden-"))
+    try:
+        st = store_mod.ChunkStore(tmp / "store", cfg)
+        eng = fusion.FusionEngine(w, st)
+        chunk_tokens, cids = [], []
+        for i, n in enumerate(chunk_sizes):
+            toks = np.random.default_rng(chunk_seed0 + i).integers(0, 256, n)
+            chunk_tokens.append(toks.astype(np.int64))
+            cids.append(st.precompute(w, [int(t) for t in toks], anchor_ratio, f"c{i}").chunk_id)
+        query = np.random.default_rng(query_seed).integers(0, 256, n_query).astype(np.int64)
+        qlist = [int(t) for t in query]
+
+        fused = eng.assemble_context(cids)
+        probe = eng.probe_query(qlist, fused, fusion.PROBE_ANCHORS)
+        scores = eng.score_critical(probe, fused)
+        sel = fusion.select_topn(scores, ratio)
+        upd, _ = eng.recompute_selected(fused, sel)
+        res = eng.run("QCFuse", ratio, cids, qlist, max_new=max_new)
+        assert np.array_equal(res.selection.indices, sel.indices)
+        full = eng.oracle_run(fused.token_ids, qlist, max_new=max_new)
+
+        c = cfg.critical_layer
+        s64 = np.sort(scores.astype(np.float64))[::-1]
+        n = sel.indices.size
+        gap = float((s64[n - 1] - s64[n]) / s64[n - 1]) if 0 < n < s64.size else float("nan")
+        out = {
+            "cfg": json.dumps(cfg.to_dict()),
+            "ratio": ratio, "anchor_ratio": anchor_ratio,
+            "query": query,
+            "first_logits": res.first_logits.astype(np.float32),
+            "full_logits": full["first_logits"].astype(np.float32),
+            "answer": np.asarray(res.answer_tokens, np.int64),
+            "full_answer": np.asarray(full["answer_tokens"], np.int64),
+            "offsets": np.asarray(fused.offsets, np.int64),
+            "q_c": probe.queries[c - 1].astype(np.float32),
+            "prefix_positions": probe.prefix_positions.astype(np.int64),
+            "scores": scores.astype(np.float32),
+            "selection": sel.indices.astype(np.int64),
+            "cutoff_rel_gap": gap,
+        }
+        for i, toks in enumerate(chunk_tokens):
+            rec = st.get_record(cids[i])
+            out[f"chunk{i}_tokens"] = toks
+            out[f"chunk{i}_anchors"] = rec.anchor_indices.astype(np.int64)
+            out[f"chunk{i}_norms"] = rec.key_norms.astype(np.float32)
+        L = cfg.n_layers
+        sample = np.unique(np.clip(np.array([0, 1, 2, fused.n_ctx // 3, fused.n_ctx // 2,
+                                             fused.n_ctx - 1, fused.n_ctx]), 0, fused.n_ctx))
+        out["sample_rows"] = sample
+        for li in range(L):
+            fk, fv = fused.layer_kv[li].keys, fused.layer_kv[li].values
+            uk, uv = upd.layer_kv[li].keys, upd.layer_kv[li].values
+            if full_rows:
+                out[f"fused_k{li}"], out[f"fused_v{li}"] = fk, fv
+                out[f"upd_k{li}"], out[f"upd_v{li}"] = uk, uv
+            else:
+                out[f"fused_k{li}"] = fk[sample]
+                out[f"fused_v{li}"] = fv[sample]
+                srow = sel.indices[:: max(1, sel.indices.size // 8)][:8]
+                out[f"upd_rows{li}"] = srow
+                out[f"upd_k{li}"] = uk[srow]
+                out[f"upd_v{li}"] = uv[srow]
+            out[f"fused_ksum{li}"] = np.float64(fk.astype(np.float64).sum())
+            out[f"fused_vsum{li}"] = np.float64(fv.astype(np.float64).sum())
+            out[f"upd_ksum{li}"] = np.float64(uk.astype(np.float64).sum())
+            out[f"upd_vsum{li}"] = np.float64(uv.astype(np.float64).sum())
+        return out
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def main():
+    model, store_mod, fusion = _import_reference()
+
+    # (1) the reference's own frozen logits fixture, re-serialised as data
+    src = json.loads((REF / "tests/data/golden_logits_ab.json").read_text())
+    (HERE / "ref_golden_logits_ab.json").write_text(json.dumps(src, indent=1))
+
+    # (2) the reference conftest "small" config (L4 H2 d32 dh16 dff64 seed 1234)
+    small = dict(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+    for k, (sizes, nq, r, ar) in enumerate([((20, 24), 6, 0.3, 0.25),
+                                             ((16, 18, 12), 4, 0.5, 0.05),
+                                             ((9,), 1, 0.2, 0.3)]):
+        d = _case(model, store_mod, fusion, small, sizes, nq, r, ar, 100 + 10 * k, 500 + k,
+                  max_new=8, full_rows=True)
+        np.savez_compressed(HERE / f"small_case{k}.npz", **d)
+
+    # (3) BASELINE config 1: L4 H4 D64 d256 F1024, 4x128 chunks, q16, r .15
+    tiny = dict(n_layers=4, n_heads=4, d_model=256, d_head=64, d_ff=1024, seed=1234)
+    for k in range(6):
+        d = _case(model, store_mod, fusion, tiny, (128, 128, 128, 128), 16, 0.15, 0.05,
+                  0, 10_000 + k, max_new=8 if k == 0 else 1, full_rows=False)
+        np.savez_compressed(HERE / f"tiny_case{k}.npz", **d)
+        print(f"tiny case {k}: N={d['selection'].size} cutoff rel gap {d['cutoff_rel_gap']:.3e}")
+
+    # (4) splitmix64 + init vectors for a Llama-width slice (first draws of each tensor)
+    cfg = model.ModelConfig(n_layers=32, n_heads=32, d_model=4096, d_head=128, d_ff=14336,
+                            seed=1234)
+    shapes = [(cfg.vocab_size, cfg.d_model)]
+    for _ in range(cfg.n_layers):
+        shapes += [(4096, 4096)] * 4 + [(4096, 14336), (14336, 4096)]
+    starts, off = [], 0
+    for r, c in shapes:
+        starts.append(off)
+        off += r * c
+    steps = np.concatenate([np.arange(s, s + 16, dtype=np.uint64) for s in starts[:13]]
+                           + [np.arange(off - 16, off, dtype=np.uint64)])
+    u = model.uniform_from_u64(model.splitmix64_at(cfg.seed, steps))
+    vals = (model.WEIGHT_LOW + u * (model.WEIGHT_HIGH - model.WEIGHT_LOW)).astype(np.float32)
+    np.savez_compressed(HERE / "init_llama_probe.npz", steps=steps, values=vals,
+                        total=np.uint64(off))
+    print("wrote fixtures to", HERE)
+
+
+if __name__ == "__main__":
+    main()
