@@ -1,0 +1,158 @@
+/*
+ * qcfuse_b200 — C ABI of the B200-native QCFuse fused-prefill kernels.
+ *
+ * Every entry point takes device pointers, plain sizes and a CUDA stream, never
+ * allocates, never synchronises, and returns an int status (0 = QCF_OK,
+ * negative = error; qcf_last_error() holds the message for the calling thread).
+ * No torch types cross this boundary. The reference package is pure Python, so
+ * its "FFI" is Python calling these through ctypes; each
+ * function names the reference symbol (file:line under
+ * /root/reference/pkg/src/qcfuse/) whose arithmetic it replaces.
+ *
+ * Layouts (row-major, token-major like the reference's LayerKV and .qcfk):
+ *   KV table / chunk KV : [rows][Hkv][D]   one tensor per layer (layer stride given)
+ *   activations x       : [M][d]           float32 residual stream
+ *   weights (GEMM B)    : [N][K]           K-major (the reference's [d_in][d_out]
+ *                                           transposed once at load)
+ *   positions / rows    : int32
+ * dtype codes: QCF_F32 (parity mode) or QCF_BF16 (speed mode).
+ */
+#ifndef QCFUSE_B200_H
+#define QCFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* qcf_stream_t;
+
+enum qcf_status {
+  QCF_OK = 0,
+  QCF_EINVAL = -1,       /* bad argument            -> ValueError */
+  QCF_ESHAPE = -2,       /* inconsistent shapes     -> ValueError */
+  QCF_ECUDA = -3,        /* CUDA launch/runtime     -> RuntimeError */
+  QCF_EUNSUPPORTED = -4, /* shape/dtype not built   -> NotImplementedError */
+  QCF_EWORKSPACE = -5    /* workspace too small     -> ValueError */
+};
+
+enum qcf_dtype { QCF_F32 = 0, QCF_BF16 = 1 };
+
+enum qcf_epilogue {
+  QCF_EPI_STORE = 0,     /* C = acc                (C in out_dtype)          */
+  QCF_EPI_RELU = 1,      /* C = max(acc, 0)        (C in out_dtype)          */
+  QCF_EPI_ADD_F32 = 2    /* C(f32) += acc          (residual stream update)  */
+};
+
+/* ---- library ------------------------------------------------------------ */
+const char* qcf_version(void);
+const char* qcf_last_error(void);
+/* 1 when the sm_100a tcgen05 GEMM is usable on the current device. */
+int qcf_tc_available(void);
+
+/* ---- deterministic init: model.py:35-46 (splitmix64_at), 67-69, 225-257 ----
+ * Writes draws [start, start + rows*cols) of the splitmix64 stream keyed by
+ * `seed`, each mapped to float32(-0.05 + 0.1*u53), as a rows x cols row-major
+ * matrix; with transpose=1 the matrix is written as out[c*ld_out + r] (K-major
+ * GEMM operand). out_dtype f32 or bf16 (bf16 = round-to-nearest of the f32). */
+int qcf_init_uniform(uint64_t seed, uint64_t start, int64_t rows, int64_t cols,
+                     int transpose, int out_dtype, void* out, int64_t ld_out,
+                     qcf_stream_t stream);
+
+/* ---- fused-context assembly: fusion.py:234-263 + model.py:271-292 ---------- */
+typedef struct {
+  const void* k;          /* chunk K, layer 0 row 0 ([L][n_tok][Hkv][D])       */
+  const void* v;          /* chunk V                                          */
+  int64_t layer_stride;   /* elements between consecutive layers              */
+  int32_t n_tok;          /* chunk length S_c                                 */
+  int32_t offset;         /* fused row of the chunk's first token (off_c >= 1)*/
+} qcf_chunk_desc;
+
+/* fused_k[l][off_c + i] = R(off_c) . chunk_k[l][i]   (re-rotation composes)
+ * fused_v[l][off_c + i] = chunk_v[l][i]                (bit copy)
+ * fused_*[l][0]         = bos_*[l]                     (BOS row, position 0)
+ * `chunks` is a DEVICE array of n_chunks descriptors. cos/sin tables are float64
+ * [n_pos][D/2] built on the host exactly as model.py:264-280 builds the angles. */
+int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                 const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                 int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                 const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                 int dtype, qcf_stream_t stream);
+
+/* dst[l][i] = src[l][rows[i]] for K and V (anchor prefix gather, fusion.py:281-303) */
+int qcf_gather_rows(const void* src_k, const void* src_v, int64_t src_layer_stride,
+                    const int32_t* rows, int64_t n_rows, void* dst_k, void* dst_v,
+                    int64_t dst_layer_stride, int n_layers, int64_t row_elems,
+                    int dtype, qcf_stream_t stream);
+
+/* ---- per-row ops: model.py:305-308 (LN), fusion.py:464 (embedding gather) -- */
+/* x[i] = emb[tokens[rows ? rows[i] - row_base : i]]  (float32 residual stream) */
+int qcf_embed(const int32_t* tokens, const int32_t* rows, int32_t row_base, int64_t m,
+              const float* emb, int d, float* x, qcf_stream_t stream);
+/* out[i] = (x[i]-mean)/sqrt(var+eps)*g + b ; out in out_dtype */
+int qcf_layernorm(const float* x, int64_t m, int d, const float* g, const float* b,
+                  float eps, void* out, int out_dtype, qcf_stream_t stream);
+/* logits[r] = LN_f(x[rows[r]]) @ emb^T  (model.py:384-385, fusion.py:540) */
+int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d,
+                const float* g, const float* b, float eps, const float* emb,
+                int vocab, float* logits, qcf_stream_t stream);
+/* norms[i] = mean_h ||k[i,h,:]||_2   (store.py:339-340) */
+int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dtype,
+                  qcf_stream_t stream);
+
+/* ---- projections: model.py:361-363, 375, 341-342 ---------------------------
+ * C[M,N] (op)= A[M,K] . B[N,K]^T, A/B in `dtype` (bf16 -> tcgen05 tensor cores,
+ * f32 -> FFMA parity kernel), fp32 accumulation, epilogue per qcf_epilogue. */
+int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
+             void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
+             int out_dtype, qcf_stream_t stream);
+/* Same contract, forced onto the SIMT path (cross-check of the tensor-core path). */
+int qcf_gemm_simt(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
+                  void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
+                  int out_dtype, qcf_stream_t stream);
+
+/* ---- RoPE at absolute positions + KV scatter: fusion.py:471-478 ------------
+ * qkv: float32 [M][(H + 2*Hkv)*D] (Q | K | V). q_out[i] = R(pos[i]).Q[i]
+ * (dtype); k_tab[dst_rows[i]] = R(pos[i]).K[i]; v_tab[dst_rows[i]] = V[i]. */
+int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
+                         const int32_t* pos, const int32_t* dst_rows,
+                         const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                         void* q_out, void* k_tab, void* v_tab, int dtype,
+                         qcf_stream_t stream);
+
+/* ---- location-aware attention: fusion.py:194-208 -> model.py:326-338 -------
+ * out[i,h] = sum_{j<=kmax[i]} softmax_j(q[i,h].k[j,h/(H/Hkv)] / float(sqrt(D))) v[j]
+ * q/out [M][H][D], k/v table [n_keys][Hkv][D]; kmax inclusive, < n_keys. */
+int qcf_attention(int dtype, const void* q, const void* k, const void* v,
+                  const int32_t* kmax, int64_t m, int h, int hkv, int d,
+                  int64_t n_keys, void* out, qcf_stream_t stream);
+
+/* ---- critical-layer scoring: fusion.py:313-326 + 566-569 ------------------
+ * scores[n] = mean_{h,t} softmax_n((q[t,h].k[n,h]) * scale), t over all nq rows
+ * (agg_last=0) or the last row (agg_last=1). precise=1 accumulates in float64.
+ * workspace >= qcf_score_workspace(...) bytes. */
+size_t qcf_score_workspace(int64_t n_ctx, int nq, int h);
+int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, int h,
+              int hkv, int d, double scale, int agg_last, int precise, float* scores,
+              void* workspace, size_t ws_bytes, qcf_stream_t stream);
+
+/* ---- Top-N selection: fusion.py:141-158 (stable argsort, ties -> lower index)
+ * idx_out[0..n_sel) = ascending (1-based + base) positions of the n_sel largest
+ * scores (scores must be >= +0 or NaN-free). n_sel is computed by the host as
+ * ceil(ratio*n) in double. workspace >= qcf_topn_workspace(n). */
+size_t qcf_topn_workspace(int64_t n);
+int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
+             int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream);
+
+/* Small device helpers used by the request graph. */
+/* out[i] = a[i] + add (int32) */
+int qcf_iota_add(const int32_t* a, int64_t n, int32_t add, int32_t* out, qcf_stream_t stream);
+/* out[i] = start + i */
+int qcf_iota(int64_t n, int32_t start, int32_t* out, qcf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCFUSE_B200_H */

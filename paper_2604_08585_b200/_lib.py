@@ -1,0 +1,99 @@
+"""ctypes binding of `libqcfuse_b200.so` (the C ABI declared in
+`include/qcfuse_b200.h`).
+
+This is the reference-side FFI a maintainer would add: the reference package is
+pure Python (`/root/reference/pkg/src/qcfuse`), so its kernels are bound with
+ctypes. Status codes map onto the exceptions the reference raises
+(`fusion.py:151,206,238,...` ValueError; NotImplementedError for shapes not
+built; RuntimeError for CUDA failures). There is no fallback: if the library is
+missing, importing the engine fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("QCFUSE_B200_LIB", _HERE / "libqcfuse_b200.so"))
+
+QCF_F32, QCF_BF16 = 0, 1
+EPI_STORE, EPI_RELU, EPI_ADD_F32 = 0, 1, 2
+
+QCF_OK, QCF_EINVAL, QCF_ESHAPE, QCF_ECUDA, QCF_EUNSUPPORTED, QCF_EWORKSPACE = 0, -1, -2, -3, -4, -5
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_F = ctypes.c_float
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+
+class ChunkDesc(ctypes.Structure):
+    """Mirror of `qcf_chunk_desc` (include/qcfuse_b200.h)."""
+    _fields_ = [("k", _P), ("v", _P), ("layer_stride", _I64), ("n_tok", _I32), ("offset", _I32)]
+
+
+# name -> (restype, argtypes); every symbol include/qcfuse_b200.h declares
+SIGNATURES: dict[str, tuple] = {
+    "qcf_version": (ctypes.c_char_p, []),
+    "qcf_last_error": (ctypes.c_char_p, []),
+    "qcf_tc_available": (_I, []),
+    "qcf_init_uniform": (_I, [_U64, _U64, _I64, _I64, _I, _I, _P, _I64, _P]),
+    "qcf_assemble": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _P, _I64, _I, _P]),
+    "qcf_gather_rows": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _I, _I64, _I, _P]),
+    "qcf_embed": (_I, [_P, _P, _I32, _I64, _P, _I, _P, _P]),
+    "qcf_layernorm": (_I, [_P, _I64, _I, _P, _P, _F, _P, _I, _P]),
+    "qcf_lm_head": (_I, [_P, _P, _I64, _I, _P, _P, _F, _P, _I, _P, _P]),
+    "qcf_key_norms": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
+    "qcf_gemm": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
+    "qcf_gemm_simt": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
+    "qcf_rope_qkv_scatter": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _P]),
+    "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
+    "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
+    "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
+    "qcf_topn_workspace": (_SZ, [_I64]),
+    "qcf_topn": (_I, [_P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
+    "qcf_iota_add": (_I, [_P, _I64, _I32, _P, _P]),
+    "qcf_iota": (_I, [_I64, _I32, _P, _P]),
+}
+
+
+class QCFError(RuntimeError):
+    pass
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} not found: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()' or `make`)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int, what: str = "") -> None:
+    if status == QCF_OK:
+        return
+    msg = (lib.qcf_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status in (QCF_EINVAL, QCF_ESHAPE, QCF_EWORKSPACE):
+        raise ValueError(text)
+    if status == QCF_EUNSUPPORTED:
+        raise NotImplementedError(text)
+    raise QCFError(text)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib, name)(*args), name)

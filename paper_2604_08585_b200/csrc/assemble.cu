@@ -1,0 +1,159 @@
+// K1: fused-context assembly with RoPE re-alignment (fusion.py:234-263,
+// model.py:271-292). HBM-bound: every chunk K/V element is read once and the
+// fused table written once, with 16-byte vector accesses; the chunk offset
+// rotation uses a float64 cos/sin table built on the host exactly as the
+// reference builds its angles (model.py:278-281).
+#include "common.cuh"
+
+namespace qcf {
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { static constexpr int N = 4; };
+template <> struct Vec16<__nv_bfloat16> { static constexpr int N = 8; };
+
+__device__ __forceinline__ int find_chunk(const qcf_chunk_desc* ch, int n_chunks, int row) {
+  int lo = 0, hi = n_chunks - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (ch[mid].offset <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ void rotate_vec(const T* src, T* dst, int j0, const double* ctab,
+                                           const double* stab);
+
+template <>
+__device__ __forceinline__ void rotate_vec<float>(const float* src, float* dst, int j0,
+                                                  const double* ctab, const double* stab) {
+  float4 x = *reinterpret_cast<const float4*>(src);
+  float4 y;
+  rotate_pair_exact(x.x, x.y, ctab[j0], stab[j0], y.x, y.y);
+  rotate_pair_exact(x.z, x.w, ctab[j0 + 1], stab[j0 + 1], y.z, y.w);
+  *reinterpret_cast<float4*>(dst) = y;
+}
+
+template <>
+__device__ __forceinline__ void rotate_vec<__nv_bfloat16>(const __nv_bfloat16* src, __nv_bfloat16* dst,
+                                                          int j0, const double* ctab, const double* stab) {
+  uint4 raw = *reinterpret_cast<const uint4*>(src);
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&raw);
+  uint4 outr;
+  __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(&outr);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    float2 f = __bfloat1622float2(p[t]);
+    float oe, oo;
+    rotate_pair_fast(f.x, f.y, (float)ctab[j0 + t], (float)stab[j0 + t], oe, oo);
+    q[t] = __floats2bfloat162_rn(oe, oo);
+  }
+  *reinterpret_cast<uint4*>(dst) = outr;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) assemble_kernel(
+    const qcf_chunk_desc* __restrict__ chunks, int n_chunks, int n_rows /* 1 + n_ctx */,
+    const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
+    T* __restrict__ fv, int64_t fstride, int row_elems, int d,
+    const double* __restrict__ ctab, const double* __restrict__ stab) {
+  constexpr int V = Vec16<T>::N;
+  const int layer = blockIdx.y;
+  const int vpr = row_elems / V;
+  const int64_t total = (int64_t)n_rows * vpr;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / vpr);
+    const int e = (int)(idx - (int64_t)row * vpr) * V;  // element within the row
+    T* dk = fk + layer * fstride + (int64_t)row * row_elems + e;
+    T* dv = fv + layer * fstride + (int64_t)row * row_elems + e;
+    if (row == 0) {
+      *reinterpret_cast<uint4*>(dk) = *reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems + e);
+      *reinterpret_cast<uint4*>(dv) = *reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems + e);
+      continue;
+    }
+    const qcf_chunk_desc c = chunks[find_chunk(chunks, n_chunks, row)];
+    const int64_t src_off = layer * c.layer_stride + (int64_t)(row - c.offset) * row_elems + e;
+    const T* sk = reinterpret_cast<const T*>(c.k) + src_off;
+    const T* sv = reinterpret_cast<const T*>(c.v) + src_off;
+    *reinterpret_cast<uint4*>(dv) = __ldg(reinterpret_cast<const uint4*>(sv));
+    const int j0 = (e % d) >> 1;
+    rotate_vec<T>(sk, dk, j0, ctab + (int64_t)c.offset * (d / 2), stab + (int64_t)c.offset * (d / 2));
+  }
+}
+
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ sk, const T* __restrict__ sv, int64_t sstride,
+                                   const int32_t* __restrict__ rows, int64_t n_rows,
+                                   T* __restrict__ dk, T* __restrict__ dv, int64_t dstride,
+                                   int64_t row_elems) {
+  constexpr int V = Vec16<T>::N;
+  const int layer = blockIdx.y;
+  const int64_t vpr = row_elems / V;
+  const int64_t total = n_rows * vpr;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / vpr, e = (idx - i * vpr) * V;
+    const int64_t src = layer * sstride + (int64_t)rows[i] * row_elems + e;
+    const int64_t dst = layer * dstride + i * row_elems + e;
+    *reinterpret_cast<uint4*>(dk + dst) = __ldg(reinterpret_cast<const uint4*>(sk + src));
+    *reinterpret_cast<uint4*>(dv + dst) = __ldg(reinterpret_cast<const uint4*>(sv + src));
+  }
+}
+
+}  // namespace qcf
+
+extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                            const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                            int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                            const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                            int dtype, qcf_stream_t stream) {
+  QCF_REQUIRE(chunks && bos_k && bos_v && fused_k && fused_v && cos_tbl && sin_tbl, QCF_EINVAL,
+              "qcf_assemble: null pointer");
+  QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1, QCF_EINVAL,
+              "qcf_assemble: bad sizes");
+  QCF_REQUIRE(d % 8 == 0, QCF_EUNSUPPORTED, "qcf_assemble: d_head must be a multiple of 8");
+  QCF_REQUIRE(n_ctx < n_pos, QCF_ESHAPE, "qcf_assemble: RoPE table too short (%lld <= %d)",
+              (long long)n_pos, n_ctx);
+  const int row_elems = hkv * d;
+  QCF_REQUIRE(fused_layer_stride >= (int64_t)(n_ctx + 1) * row_elems, QCF_ESHAPE,
+              "qcf_assemble: fused layer stride too small");
+  auto s = qcf::as_stream(stream);
+  const int vec = dtype == QCF_F32 ? 4 : 8;
+  const int64_t per_layer = (int64_t)(n_ctx + 1) * (row_elems / vec);
+  int gx = (int)std::min<int64_t>((per_layer + 255) / 256, 65535 * 4);
+  dim3 grid(gx, n_layers);
+  if (dtype == QCF_F32)
+    qcf::assemble_kernel<float><<<grid, 256, 0, s>>>(chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
+        (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
+  else if (dtype == QCF_BF16)
+    qcf::assemble_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(chunks, n_chunks, n_ctx + 1,
+        (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
+        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
+  else
+    QCF_REQUIRE(false, QCF_EINVAL, "qcf_assemble: bad dtype");
+  QCF_LAUNCH_CHECK("qcf_assemble");
+  return QCF_OK;
+}
+
+extern "C" int qcf_gather_rows(const void* src_k, const void* src_v, int64_t src_layer_stride,
+                               const int32_t* rows, int64_t n_rows, void* dst_k, void* dst_v,
+                               int64_t dst_layer_stride, int n_layers, int64_t row_elems,
+                               int dtype, qcf_stream_t stream) {
+  QCF_REQUIRE(src_k && src_v && rows && dst_k && dst_v, QCF_EINVAL, "qcf_gather_rows: null pointer");
+  QCF_REQUIRE(row_elems % 8 == 0, QCF_EUNSUPPORTED, "qcf_gather_rows: row must be 16B multiple");
+  if (n_rows == 0 || n_layers == 0) return QCF_OK;
+  auto s = qcf::as_stream(stream);
+  const int vec = dtype == QCF_F32 ? 4 : 8;
+  int gx = (int)std::min<int64_t>((n_rows * (row_elems / vec) + 255) / 256, 65535);
+  dim3 grid(gx, n_layers);
+  if (dtype == QCF_F32)
+    qcf::gather_rows_kernel<float><<<grid, 256, 0, s>>>((const float*)src_k, (const float*)src_v,
+        src_layer_stride, rows, n_rows, (float*)dst_k, (float*)dst_v, dst_layer_stride, row_elems);
+  else
+    qcf::gather_rows_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)src_k,
+        (const __nv_bfloat16*)src_v, src_layer_stride, rows, n_rows, (__nv_bfloat16*)dst_k,
+        (__nv_bfloat16*)dst_v, dst_layer_stride, row_elems);
+  QCF_LAUNCH_CHECK("qcf_gather_rows");
+  return QCF_OK;
+}

@@ -1,0 +1,56 @@
+// Dispatch of the public GEMM / attention entry points onto the sm_100a
+// tensor-core kernels (bf16) or the FFMA parity kernels (f32).
+#include "attention.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace qcf {
+
+static int g_tc_state = -1;  // -1 unknown, 0 no, 1 yes
+
+static bool tc_ok() {
+  if (g_tc_state < 0) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    g_tc_state = (major == 10 && minor == 0) ? 1 : 0;
+  }
+  return g_tc_state == 1;
+}
+
+}  // namespace qcf
+
+extern "C" int qcf_tc_available(void) { return qcf::tc_ok() ? 1 : 0; }
+
+extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c,
+                        int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype,
+                        qcf_stream_t stream) {
+  int st = qcf::gemm_check_args(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype);
+  if (st != QCF_OK) return st;
+  if (m == 0 || n == 0) return QCF_OK;
+  auto s = qcf::as_stream(stream);
+  if (dtype == QCF_BF16) {
+    QCF_REQUIRE(qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm: bf16 path needs an sm_100 (B200) device");
+    st = qcf::gemm_tc_launch(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
+    if (st != QCF_EUNSUPPORTED) return st;
+    // shapes outside the tcgen05 kernel's alignment contract (K % 8 != 0, tiny
+    // toy widths) run on the SIMT kernel; still on the GPU, never on the host
+  }
+  return qcf::gemm_simt_launch(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
+}
+
+extern "C" int qcf_attention(int dtype, const void* q, const void* k, const void* v,
+                             const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
+                             void* out, qcf_stream_t stream) {
+  QCF_REQUIRE(q && k && v && kmax && out, QCF_EINVAL, "qcf_attention: null pointer");
+  QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && n_keys > 0, QCF_EINVAL, "qcf_attention: bad shape");
+  QCF_REQUIRE(dtype == QCF_F32 || dtype == QCF_BF16, QCF_EINVAL, "qcf_attention: bad dtype");
+  if (m == 0) return QCF_OK;
+  auto s = qcf::as_stream(stream);
+  if (dtype == QCF_BF16 && qcf::tc_ok()) {
+    int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s);
+    if (st != QCF_EUNSUPPORTED) return st;
+  }
+  return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, s);
+}

@@ -1,0 +1,139 @@
+// K4: critical-layer query->context scoring (fusion.py:313-326, _softmax_last
+// fusion.py:566-569): per (head, query row) a softmax over the n_ctx context
+// keys of (Q_c . K) * scale, then the mean over (head, row) per key. Three
+// passes: logits into the workspace, per-row max/sum, column mean. `precise`
+// runs the contraction and softmax in float64 (the fp32 parity scoring mode,
+// whose float32-rounded output orders exactly like the reference's scores).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace qcf {
+
+constexpr int SC_TILE = 64;
+
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(256) score_logits_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                           int64_t n_ctx, int nq, int t0, int h,
+                                                           int hkv, int d, Acc scale,
+                                                           Acc* __restrict__ S) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Acc* Qs = reinterpret_cast<Acc*>(smraw);          // [nt][d]
+  const int nt = nq - t0;
+  Acc* Ks = Qs + nt * d;                             // [SC_TILE][d+1]
+  const int head = blockIdx.y, kvh = head / (h / hkv);
+  const int64_t n0 = (int64_t)blockIdx.x * SC_TILE;
+  for (int e = threadIdx.x; e < nt * d; e += blockDim.x) {
+    int t = e / d, c = e % d;
+    Qs[e] = (Acc)to_f<T>(q[((int64_t)(t0 + t) * h + head) * d + c]);
+  }
+  for (int e = threadIdx.x; e < SC_TILE * d; e += blockDim.x) {
+    int j = e / d, c = e % d;
+    int64_t n = n0 + j;
+    Ks[j * (d + 1) + c] = n < n_ctx ? (Acc)to_f<T>(k[(n * hkv + kvh) * d + c]) : (Acc)0;
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < nt * SC_TILE; p += blockDim.x) {
+    const int t = p / SC_TILE, j = p % SC_TILE;
+    const int64_t n = n0 + j;
+    if (n >= n_ctx) continue;
+    Acc acc = 0;
+    for (int c = 0; c < d; ++c) acc += Qs[t * d + c] * Ks[j * (d + 1) + c];
+    S[((int64_t)head * nt + t) * n_ctx + n] = acc * scale;
+  }
+}
+
+template <typename Acc>
+__global__ void score_rowstats_kernel(const Acc* __restrict__ S, int64_t n_ctx, Acc* __restrict__ rmax,
+                                      Acc* __restrict__ rsum) {
+  __shared__ Acc red[32];
+  const int64_t r = blockIdx.x;
+  const Acc* s = S + r * n_ctx;
+  Acc mx = -INFINITY;
+  for (int64_t n = threadIdx.x; n < n_ctx; n += blockDim.x) mx = s[n] > mx ? s[n] : mx;
+  for (int o = 16; o > 0; o >>= 1) { Acc t = __shfl_xor_sync(0xffffffffu, mx, o); mx = t > mx ? t : mx; }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : (Acc)-INFINITY;
+    for (int o = 16; o > 0; o >>= 1) { Acc t = __shfl_xor_sync(0xffffffffu, mx, o); mx = t > mx ? t : mx; }
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  Acc sum = 0;
+  for (int64_t n = threadIdx.x; n < n_ctx; n += blockDim.x) sum += exp(s[n] - mx);
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Acc t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    rmax[r] = mx;
+    rsum[r] = t;
+  }
+}
+
+template <typename Acc>
+__global__ void score_colmean_kernel(const Acc* __restrict__ S, int64_t n_ctx, int rows,
+                                     const Acc* __restrict__ rmax, const Acc* __restrict__ rsum,
+                                     float* __restrict__ scores) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= n_ctx) return;
+  Acc acc = 0;
+  for (int r = 0; r < rows; ++r) acc += exp(S[(int64_t)r * n_ctx + n] - rmax[r]) / rsum[r];
+  scores[n] = (float)(acc / (Acc)rows);
+}
+
+template <typename T, typename Acc>
+static int score_impl(const void* q, const void* k, int64_t n_ctx, int nq, int h, int hkv, int d,
+                      double scale, int agg_last, float* scores, void* ws, cudaStream_t s) {
+  const int t0 = agg_last ? nq - 1 : 0;
+  const int nt = nq - t0;
+  const int rows = h * nt;
+  Acc* S = reinterpret_cast<Acc*>(ws);
+  Acc* rmax = S + (int64_t)rows * n_ctx;
+  Acc* rsum = rmax + rows;
+  const size_t smem = sizeof(Acc) * ((size_t)nt * d + (size_t)SC_TILE * (d + 1));
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(score_logits_kernel<T, Acc>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "qcf_score attr");
+  }
+  QCF_REQUIRE(smem <= 220 * 1024, QCF_EUNSUPPORTED, "qcf_score: query too long for one tile");
+  dim3 g1(ceil_div(n_ctx, SC_TILE), h);
+  score_logits_kernel<T, Acc><<<g1, 256, smem, s>>>((const T*)q, (const T*)k, n_ctx, nq, t0, h, hkv,
+                                                    d, (Acc)scale, S);
+  QCF_LAUNCH_CHECK("qcf_score logits");
+  score_rowstats_kernel<Acc><<<rows, 256, 0, s>>>(S, n_ctx, rmax, rsum);
+  QCF_LAUNCH_CHECK("qcf_score rowstats");
+  score_colmean_kernel<Acc><<<ceil_div(n_ctx, 256), 256, 0, s>>>(S, n_ctx, rows, rmax, rsum, scores);
+  QCF_LAUNCH_CHECK("qcf_score colmean");
+  return QCF_OK;
+}
+
+}  // namespace qcf
+
+extern "C" size_t qcf_score_workspace(int64_t n_ctx, int nq, int h) {
+  const size_t rows = (size_t)h * nq;
+  return sizeof(double) * (rows * (size_t)n_ctx + 2 * rows) + 256;
+}
+
+extern "C" int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, int h,
+                         int hkv, int d, double scale, int agg_last, int precise, float* scores,
+                         void* workspace, size_t ws_bytes, qcf_stream_t stream) {
+  QCF_REQUIRE(q && k && scores && workspace, QCF_EINVAL, "qcf_score: null pointer");
+  QCF_REQUIRE(n_ctx > 0 && nq > 0 && h > 0 && hkv > 0 && h % hkv == 0 && d > 0, QCF_EINVAL,
+              "qcf_score: bad sizes");
+  QCF_REQUIRE(ws_bytes >= qcf_score_workspace(n_ctx, nq, h), QCF_EWORKSPACE,
+              "qcf_score: workspace too small");
+  auto s = qcf::as_stream(stream);
+  if (dtype == QCF_F32)
+    return precise ? qcf::score_impl<float, double>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s)
+                   : qcf::score_impl<float, float>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s);
+  if (dtype == QCF_BF16)
+    return precise ? qcf::score_impl<__nv_bfloat16, double>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s)
+                   : qcf::score_impl<__nv_bfloat16, float>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s);
+  QCF_REQUIRE(false, QCF_EINVAL, "qcf_score: bad dtype");
+}

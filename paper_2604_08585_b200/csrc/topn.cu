@@ -1,0 +1,109 @@
+// K5: Top-N token selection (fusion.py:141-158). The reference sorts
+// -float64(score) with a stable argsort, keeps the first N and returns them
+// ascending + 1. Equivalent single-CTA formulation: an 8-bit-digit radix
+// select finds the N-th largest key T (keys are the order-preserving uint32
+// image of the float32 scores), then an index-ordered block scan keeps every
+// key > T plus the first N - count(> T) keys == T (ties -> lower index) and
+// compacts them in ascending order. Bit-exact by construction.
+#include "common.cuh"
+
+namespace qcf {
+
+constexpr int TN_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t order_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// inclusive block scan of one int per thread (1024 threads)
+__device__ __forceinline__ int block_scan_incl(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) warp_tot[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    warp_tot[lane] = t;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  const int add = w > 0 ? warp_tot[w - 1] : 0;
+  total = warp_tot[31];
+  __syncthreads();
+  return v + add;
+}
+
+__global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restrict__ scores, int64_t n,
+                                                          int64_t n_sel, int32_t base,
+                                                          int32_t* __restrict__ out) {
+  __shared__ int hist[256];
+  __shared__ int warp_tot[32];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_need;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_prefix = 0; s_need = (int)n_sel; }
+  // ---- radix select of the n_sel-th largest key, 4 digits of 8 bits (MSB first)
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    const uint32_t hi_mask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      uint32_t key = order_key(scores[i]);
+      if ((key & hi_mask) == (prefix & hi_mask)) atomicAdd(&hist[(key >> shift) & 0xff], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int need = s_need, b = 255;
+      for (; b > 0; --b) {
+        if (hist[b] >= need) break;
+        need -= hist[b];
+      }
+      s_prefix = prefix | ((uint32_t)b << shift);
+      s_need = need;  // how many keys equal to the final threshold must be taken
+    }
+    __syncthreads();
+  }
+  const uint32_t T = s_prefix;
+  const int need_eq = s_need;
+  // ---- ordered compaction: key > T always, key == T for the first need_eq (index order)
+  int eq_before = 0, sel_before = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int64_t i = c0 + tid;
+    uint32_t key = i < n ? order_key(scores[i]) : 0u;
+    const int is_eq = (i < n && key == T) ? 1 : 0;
+    int eq_total;
+    const int eq_incl = block_scan_incl(is_eq, warp_tot, eq_total);
+    const int take = (i < n) && (key > T || (is_eq && eq_before + eq_incl <= need_eq)) ? 1 : 0;
+    int sel_total;
+    const int sel_incl = block_scan_incl(take, warp_tot, sel_total);
+    if (take) out[sel_before + sel_incl - 1] = (int32_t)i + base;
+    eq_before += eq_total;
+    sel_before += sel_total;
+  }
+}
+
+}  // namespace qcf
+
+extern "C" size_t qcf_topn_workspace(int64_t n) { (void)n; return 0; }
+
+extern "C" int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
+                        int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream) {
+  (void)workspace; (void)ws_bytes;
+  QCF_REQUIRE(scores && (idx_out || n_sel == 0), QCF_EINVAL, "qcf_topn: null pointer");
+  QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
+  QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
+  if (n_sel == 0) return QCF_OK;
+  qcf::topn_kernel<<<1, qcf::TN_THREADS, 0, qcf::as_stream(stream)>>>(scores, n, n_sel, base, idx_out);
+  QCF_LAUNCH_CHECK("qcf_topn");
+  return QCF_OK;
+}

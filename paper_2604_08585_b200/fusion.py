@@ -1,0 +1,814 @@
+"""B200-native QCFuse fusion engine behind the reference's `FusionEngine` API
+(fusion.py:211-563).
+
+Hot path (`FusionEngine.fuse` / `run("QCFuse", …)`), all on one CUDA stream,
+no host synchronisation between kernels:
+
+  K1 qcf_assemble          fused table = [BOS | R(off_c)·K_c …], V copied     fusion.py:234-263
+  K2 qcf_gather_rows       probe past = [BOS | anchor rows] for layers < c     fusion.py:281-303
+  K3 layer stack (q rows)  LN→QKV→RoPE→attn→Wo→LN→FFN for layers 1..c-1, then
+                           layer c's LN→Wq→RoPE = Q_c                          fusion.py:305-311
+  K4 qcf_score             softmax over context keys, mean over (h,t)         fusion.py:313-326
+  K5 qcf_topn              stable Top-N, ties → lower index, ascending        fusion.py:148-158
+  K6 layer stack (N+q rows) selected rows re-embedded, K/V scattered into the
+                           fused table in place, location-aware attention;
+                           the query rows ride in the same pass              fusion.py:446-490, 536-540
+     qcf_lm_head           LN_f + tied lm-head on the last query row         fusion.py:540
+
+The reference-shaped objects (`FusedContext.layer_kv`, `QueryProbe.queries`,
+`SelectionResult.indices`, `RunResult.first_logits` …) materialise host numpy
+lazily, only when a caller reads them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ChunkDesc, call
+from .model import (BOS_ID, EOS_ID, ModelWeights, byte_tokens, cuda_stream, render_tokens)
+from .pipeline import CostModel, ScheduleTrace, layer_times, policy_schedule, schedule_events
+from .runtime import Executor
+from .store import ChunkStore, HostLayerKV
+
+POLICIES = ("FullCompute", "FullReuse", "Random", "EPIC", "CacheBlend",
+            "KVShare", "QCLast", "QCAll", "QCFuse")
+PROBE_ANCHORS = "anchors"
+PROBE_FULL = "full"
+PROBE_NONE = "none"
+
+_EXECUTORS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _executor_for(weights: ModelWeights) -> Executor:
+    ex = _EXECUTORS.get(weights)
+    if ex is None:
+        ex = Executor(weights)
+        _EXECUTORS[weights] = ex
+    return ex
+
+
+def _i32(a, device) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.int32)), device=device)
+
+
+# ---------------------------------------------------------------------------
+# result types (fusion.py:62-138)
+# ---------------------------------------------------------------------------
+
+class _LazyLayers:
+    """Sequence of HostLayerKV over a device table, copied per layer on access."""
+
+    def __init__(self, k: torch.Tensor, v: torch.Tensor, n_rows: int):
+        self._k, self._v, self._n = k, v, n_rows
+        self._cache: dict[int, HostLayerKV] = {}
+
+    def __len__(self):
+        return self._k.shape[0]
+
+    def __getitem__(self, li):
+        if isinstance(li, slice):
+            return [self[i] for i in range(len(self))[li]]
+        if li < 0:
+            li += len(self)
+        if li not in self._cache:
+            self._cache[li] = HostLayerKV(self._k[li, :self._n].float().cpu().numpy(),
+                                          self._v[li, :self._n].float().cpu().numpy(), 0)
+        return self._cache[li]
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
+@dataclass
+class FusedContext:
+    chunk_ids: list[str]
+    token_ids: np.ndarray
+    offsets: list[int]
+    n_ctx: int
+    chunk_index: np.ndarray
+    k: torch.Tensor            # [L][cap][Hkv][D] device table (rows 0..n_ctx valid)
+    v: torch.Tensor
+    _layers: _LazyLayers | None = field(default=None, repr=False)
+
+    @property
+    def layer_kv(self) -> _LazyLayers:
+        if self._layers is None:
+            self._layers = _LazyLayers(self.k, self.v, self.n_ctx + 1)
+        return self._layers
+
+    def key_positions(self) -> np.ndarray:
+        return np.arange(0, self.n_ctx + 1, dtype=np.int64)
+
+    def copy_kv(self) -> list[HostLayerKV]:
+        return [kv.copy() for kv in self.layer_kv]
+
+    def clone(self, extra_rows: int = 0) -> "FusedContext":
+        L, cap, Hkv, D = self.k.shape
+        rows = max(cap, self.n_ctx + 1 + extra_rows)
+        k = torch.empty((L, rows, Hkv, D), dtype=self.k.dtype, device=self.k.device)
+        v = torch.empty_like(k)
+        k[:, :self.n_ctx + 1].copy_(self.k[:, :self.n_ctx + 1])
+        v[:, :self.n_ctx + 1].copy_(self.v[:, :self.n_ctx + 1])
+        return FusedContext(list(self.chunk_ids), self.token_ids, list(self.offsets), self.n_ctx,
+                            self.chunk_index, k, v)
+
+
+@dataclass
+class QueryProbe:
+    query_tokens: np.ndarray
+    positions: np.ndarray
+    q_store: torch.Tensor              # [layers_run][q][H][D] rotated queries
+    prefix_positions: np.ndarray
+    _crit_tab: tuple | None = field(default=None, repr=False)   # (k, v, n_prefix) at layer c
+    _crit_layer: int = 0
+    _queries: list | None = field(default=None, repr=False)
+
+    @property
+    def queries(self) -> list[np.ndarray]:
+        if self._queries is None:
+            self._queries = [self.q_store[i].float().cpu().numpy() for i in range(self.q_store.shape[0])]
+        return self._queries
+
+    @property
+    def critical_attention(self) -> np.ndarray:
+        """[H, q, n_prefix] probe attention over the prefix at the critical layer
+        (fusion.py:308-311). Diagnostic field; computed on demand on the device."""
+        tk, tv, n_pre = self._crit_tab
+        q = self.q_store[self._crit_layer - 1].float()            # [q, H, D]
+        nq, H, D = q.shape
+        keys = tk[: n_pre + nq].float()                            # [n, Hkv, D]
+        rep = H // keys.shape[1]
+        keys = keys.repeat_interleave(rep, dim=1)
+        s = torch.einsum("mhd,nhd->hmn", q, keys) / math.sqrt(D)
+        mask = torch.ones(nq, n_pre + nq, dtype=torch.bool, device=q.device)
+        mask[:, n_pre:] = torch.tril(torch.ones(nq, nq, dtype=torch.bool, device=q.device))
+        s = s.masked_fill(~mask[None], float("-inf"))
+        return torch.softmax(s, dim=-1)[:, :, :n_pre].cpu().numpy()
+
+
+@dataclass
+class SelectionResult:
+    policy: str
+    ratio: float
+    indices: np.ndarray
+    scores: np.ndarray
+
+    @property
+    def n_selected(self) -> int:
+        return int(self.indices.size)
+
+
+@dataclass
+class RecomputeTrace:
+    updated_indices: np.ndarray
+    fetch_seconds: list[float]
+    compute_seconds: list[float]
+    events: list[dict] = field(default_factory=list)
+
+
+@dataclass
+class OracleComparison:
+    logit_div_max: float
+    logit_kl: float
+    token_match: float
+    overlap: float
+
+
+@dataclass
+class RunResult:
+    policy: str
+    ratio: float
+    answer_tokens: list[int]
+    answer_text: str
+    first_logits: np.ndarray
+    selection: SelectionResult
+    trace: RecomputeTrace
+    schedule: ScheduleTrace
+    ttft_sim: float
+    comparison: OracleComparison | None = None
+    timings_ms: dict = field(default_factory=dict)
+
+
+@dataclass
+class RunOptions:
+    max_new: int = 32
+    query_agg: str = "mean"
+    selection_seed: int = 0
+    epic_per_chunk: bool = False
+    qcall_layer_average: bool = False
+    score_precise: bool = True      # float64 scoring (the fp32 parity scoring mode)
+
+
+# ---------------------------------------------------------------------------
+# module-level ops (fusion.py:141-208)
+# ---------------------------------------------------------------------------
+
+def n_select(ratio: float, n_ctx: int) -> int:
+    """N = ceil(ratio * n_ctx) in Python double (fusion.py:155)."""
+    if not (0.0 <= ratio <= 1.0):
+        raise ValueError("ratio must be in [0, 1]")
+    return math.ceil(ratio * n_ctx)
+
+
+def topn_device(scores: torch.Tensor, n: int, base: int = 1, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+    """Ascending (base-offset) indices of the n largest scores, ties → lower
+    index, via the `qcf_topn` kernel."""
+    m = scores.numel()
+    out = out if out is not None else torch.empty(max(n, 1), dtype=torch.int32, device=scores.device)
+    call("qcf_topn", scores.data_ptr(), m, n, base, out.data_ptr(), None, 0, cuda_stream(stream))
+    return out[:n]
+
+
+def top_n_positions(scores, n: int) -> np.ndarray:
+    """fusion.py:141-145 on the device."""
+    s = torch.as_tensor(np.asarray(scores, dtype=np.float32), device="cuda")
+    return topn_device(s, int(n)).cpu().numpy().astype(np.int64)
+
+
+def select_topn(scores, ratio: float, policy: str = "QCFuse") -> SelectionResult:
+    """fusion.py:148-158: N = ceil(ratio·n_ctx), ties toward the lower index."""
+    if not (0.0 <= ratio <= 1.0):
+        raise ValueError("ratio must be in [0, 1]")
+    s = np.asarray(scores, dtype=np.float64).astype(np.float32)
+    n = n_select(ratio, s.size)
+    idx = topn_device(torch.as_tensor(s, device="cuda"), n).cpu().numpy().astype(np.int64)
+    return SelectionResult(policy, ratio, idx, s)
+
+
+def epic_select(n_ctx: int, ratio: float, chunk_spans=None) -> SelectionResult:
+    """Static prefix selection (fusion.py:161-177); host-side index list."""
+    if not (0.0 <= ratio <= 1.0):
+        raise ValueError("ratio must be in [0, 1]")
+    if chunk_spans is None:
+        idx = np.arange(1, math.ceil(ratio * n_ctx) + 1, dtype=np.int64)
+    else:
+        picks = []
+        for start, length in chunk_spans:
+            picks.extend(range(start, start + math.ceil(ratio * length)))
+        idx = np.asarray(sorted(picks), dtype=np.int64)
+    return SelectionResult("EPIC", ratio, idx, np.zeros(n_ctx, np.float32))
+
+
+def _splitmix_next_below(state: int, n: int) -> tuple[int, int]:
+    m = (1 << 64) - 1
+    state = (state + 0x9E3779B97F4A7C15) & m
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return state, (z ^ (z >> 31)) % n
+
+
+def random_select(seed: int, n_ctx: int, ratio: float) -> SelectionResult:
+    """Seeded Fisher-Yates over 1..n_ctx (fusion.py:180-191)."""
+    if not (0.0 <= ratio <= 1.0):
+        raise ValueError("ratio must be in [0, 1]")
+    n = math.ceil(ratio * n_ctx)
+    arr = list(range(1, n_ctx + 1))
+    st = seed & ((1 << 64) - 1)
+    for i in range(n_ctx - 1, 0, -1):
+        st, j = _splitmix_next_below(st, i + 1)
+        arr[i], arr[j] = arr[j], arr[i]
+    return SelectionResult("Random", ratio, np.asarray(sorted(arr[:n]), dtype=np.int64),
+                           np.zeros(n_ctx, np.float32))
+
+
+def sparse_attention(q, positions, keys, values, visible) -> np.ndarray:
+    """Attention of scattered rows over a KV table (fusion.py:194-208), on the
+    device. The location-aware kernel covers prefix-visibility masks (row i
+    sees keys 0..kmax[i], the only masks the fused path produces)."""
+    q = np.asarray(q, np.float32)
+    keys = np.asarray(keys, np.float32)
+    values = np.asarray(values, np.float32)
+    visible = np.asarray(visible, bool)
+    if visible.shape != (q.shape[0], keys.shape[0]):
+        raise ValueError("visibility mask shape mismatch")
+    if not visible.any(axis=1).all():
+        raise ValueError("every query row needs at least one visible key")
+    kmax = visible.shape[1] - 1 - np.argmax(visible[:, ::-1], axis=1)
+    prefix = np.arange(visible.shape[1])[None, :] <= kmax[:, None]
+    if not np.array_equal(prefix, visible):
+        raise NotImplementedError("sparse_attention: only prefix (causal-by-position) masks are "
+                                  "built on the device")
+    m, H, D = q.shape
+    dev = torch.device("cuda")
+    tq = torch.as_tensor(q, device=dev)
+    tk = torch.as_tensor(keys, device=dev)
+    tv = torch.as_tensor(values, device=dev)
+    out = torch.empty_like(tq)
+    call("qcf_attention", _lib.QCF_F32, tq.data_ptr(), tk.data_ptr(), tv.data_ptr(),
+         _i32(kmax, dev).data_ptr(), m, H, keys.shape[1], D, keys.shape[0], out.data_ptr(),
+         cuda_stream())
+    return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# request plan + device buffers of the fused fast path
+# ---------------------------------------------------------------------------
+
+@dataclass
+class _Plan:
+    chunk_ids: list[str]
+    records: list
+    offsets: list[int]
+    n_ctx: int
+    q: int
+    n_sel: int
+    anchor_rows: np.ndarray      # [1 + A] fused rows of the probe prefix
+    policy: str
+
+
+class _Bufs:
+    """Device buffers for one request shape (fixed addresses → graph replay)."""
+
+    def __init__(self, eng: "FusionEngine", n_ctx: int, q: int, n_sel: int, n_anchor_rows: int,
+                 n_chunks: int, extra_rows: int = 0):
+        cfg, dev = eng.config, eng.device
+        L, H, Hkv, D = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.d_head
+        dt = eng.weights.torch_dtype
+        c = cfg.critical_layer
+        self.rows = 1 + n_ctx + q + extra_rows
+        self.fk = torch.empty((L, self.rows, Hkv, D), dtype=dt, device=dev)
+        self.fv = torch.empty_like(self.fk)
+        self.desc = torch.empty(n_chunks * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
+        self.tok = torch.empty(self.rows, dtype=torch.int32, device=dev)
+        self.anchor_rows = torch.empty(max(n_anchor_rows, 1), dtype=torch.int32, device=dev)
+        self.n_pre = n_anchor_rows
+        self.pk = torch.empty((c, n_anchor_rows + q, Hkv, D), dtype=dt, device=dev)
+        self.pv = torch.empty_like(self.pk)
+        ar = torch.arange(q, dtype=torch.int32, device=dev)
+        self.p_pos = ar + (n_ctx + 1)                 # probe positions n_ctx+1..
+        self.p_dst = ar + n_anchor_rows               # probe rows in its compact table
+        self.qc = torch.empty((1, q, H, D), dtype=dt, device=dev)
+        self.scores = torch.empty(n_ctx, dtype=torch.float32, device=dev)
+        self.score_ws = torch.empty(int(_lib.lib.qcf_score_workspace(n_ctx, q, H)), dtype=torch.uint8,
+                                    device=dev)
+        self.rc_pos = torch.empty(n_sel + q, dtype=torch.int32, device=dev)
+        self.rc_pos[n_sel:] = ar + (n_ctx + 1)
+        self.last_row = torch.tensor([n_sel + q - 1], dtype=torch.int32, device=dev)
+        self.logits = torch.empty((1, cfg.vocab_size), dtype=torch.float32, device=dev)
+        self.sc_probe = eng.ex.scratch(q, key=("probe", id(self)))
+        self.sc_rc = eng.ex.scratch(n_sel + q, key=("rc", id(self)))
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+
+class FusionEngine:
+    """B200 engine with the reference's FusionEngine surface (fusion.py:211-563)."""
+
+    def __init__(self, weights: ModelWeights, store: ChunkStore, cost: CostModel | None = None,
+                 options: RunOptions | None = None):
+        if store.dtype != weights.dtype:
+            raise ValueError("store pool dtype must match the weights dtype")
+        self.weights = weights
+        self.config = weights.config
+        self.store = store
+        self.cost = cost or CostModel(tier=store.tier)
+        self.options = options or RunOptions()
+        self.device = weights.device
+        self.ex = _executor_for(weights)
+        # BOS row computed once at position 0 (fusion.py:226-227)
+        bos = torch.tensor([BOS_ID], dtype=torch.int32, device=self.device)
+        bk, bv, _ = self.ex.forward_full(bos, 0)
+        self._bos_k, self._bos_v = bk[:, 0].contiguous(), bv[:, 0].contiguous()
+        self._bufs: dict[tuple, _Bufs] = {}
+        self._oracle_cache: dict = {}
+
+    # ------------------------------------------------------------------
+    # planning helpers
+    # ------------------------------------------------------------------
+    def _records(self, chunk_ids):
+        if not chunk_ids:
+            raise ValueError("chunk list must be non-empty")
+        recs = [self.store.get_record(cid) for cid in chunk_ids]
+        offs, pos = [], 1
+        for r in recs:
+            offs.append(pos)
+            pos += r.n_tokens
+        L = self.config.n_layers
+        for r in recs:   # fetch accounting of assemble_context (store.py:402-403)
+            nb = 2 * r.n_tokens * self.config.n_kv_heads * self.config.d_head * 4
+            self.store.manifest.layers_fetched += L
+            self.store.manifest.bytes_fetched += L * nb
+        return recs, offs, pos - 1
+
+    def _desc_bytes(self, recs, offs) -> torch.Tensor:
+        arr = (ChunkDesc * len(recs))()
+        for i, (r, o) in enumerate(zip(recs, offs)):
+            arr[i].k = r.k.data_ptr()
+            arr[i].v = r.v.data_ptr()
+            arr[i].layer_stride = r.k.stride(0)
+            arr[i].n_tok = r.n_tokens
+            arr[i].offset = o
+        return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
+
+    def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None):
+        cfg = self.config
+        self.ex.rope.ensure(n_ctx + 2)
+        call("qcf_assemble", desc_dev.data_ptr(), len(recs), n_ctx, self._bos_k.data_ptr(),
+             self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(), fk.stride(0), cfg.n_layers,
+             cfg.n_kv_heads, cfg.d_head, self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(),
+             self.ex.rope.n_pos, self.weights.qcf_dtype, cuda_stream(stream))
+
+    @staticmethod
+    def _anchor_rows(recs, offs, mode, n_ctx) -> np.ndarray:
+        if mode == PROBE_FULL:
+            return np.arange(0, n_ctx + 1, dtype=np.int64)
+        rows = [np.zeros(1, np.int64)]
+        if mode == PROBE_ANCHORS:
+            for r, o in zip(recs, offs):
+                if r.anchor_indices.size:
+                    rows.append(o + r.anchor_indices)
+        elif mode != PROBE_NONE:
+            raise ValueError(f"unknown probe mode: {mode}")
+        return np.concatenate(rows)
+
+    # ------------------------------------------------------------------
+    # context assembly (fusion.py:234-263)
+    # ------------------------------------------------------------------
+    def assemble_context(self, chunk_ids: list[str], extra_rows: int = 0) -> FusedContext:
+        recs, offs, n_ctx = self._records(chunk_ids)
+        cfg = self.config
+        fk = torch.empty((cfg.n_layers, 1 + n_ctx + extra_rows, cfg.n_kv_heads, cfg.d_head),
+                         dtype=self.weights.torch_dtype, device=self.device)
+        fv = torch.empty_like(fk)
+        desc = self._desc_bytes(recs, offs).to(self.device)
+        self._assemble_into(recs, offs, n_ctx, fk, fv, desc)
+        token_ids = np.concatenate([r.token_ids for r in recs])
+        chunk_index = np.concatenate([np.full(r.n_tokens, i, np.int64) for i, r in enumerate(recs)])
+        return FusedContext(list(chunk_ids), token_ids, offs, n_ctx, chunk_index, fk, fv)
+
+    # ------------------------------------------------------------------
+    # probing and scoring (fusion.py:269-329)
+    # ------------------------------------------------------------------
+    def probe_query(self, query_tokens, fused: FusedContext, mode: str = PROBE_ANCHORS,
+                    layers: int | None = None) -> QueryProbe:
+        toks = np.asarray(query_tokens, dtype=np.int64)
+        if toks.size == 0:
+            raise ValueError("query must be non-empty")
+        cfg = self.config
+        recs = [self.store.get_record(cid) for cid in fused.chunk_ids]
+        rows = self._anchor_rows(recs, fused.offsets, mode, fused.n_ctx)
+        n_layers = cfg.n_layers if layers is None else layers
+        q = toks.size
+        n_pre = rows.size
+        dev = self.device
+        dt = self.weights.torch_dtype
+        pk = torch.empty((n_layers, n_pre + q, cfg.n_kv_heads, cfg.d_head), dtype=dt, device=dev)
+        pv = torch.empty_like(pk)
+        s = cuda_stream()
+        call("qcf_gather_rows", fused.k.data_ptr(), fused.v.data_ptr(), fused.k.stride(0),
+             _i32(rows, dev).data_ptr(), n_pre, pk.data_ptr(), pv.data_ptr(), pk.stride(0), n_layers,
+             cfg.n_kv_heads * cfg.d_head, self.weights.qcf_dtype, s)
+        ar = torch.arange(q, dtype=torch.int32, device=dev)
+        pos = ar + (fused.n_ctx + 1)
+        dst = ar + n_pre
+        self.ex.rope.ensure(fused.n_ctx + q + 2)
+        sc = self.ex.scratch(q, key="probe_api")
+        self.ex.embed(sc, q, _i32(toks, dev))
+        q_store = torch.empty((n_layers, q, cfg.n_heads, cfg.d_head), dtype=dt, device=dev)
+        self.ex.stack(sc, q, pos, dst, dst, pk, pv, layers=range(n_layers), q_store=q_store)
+        positions = np.arange(1 + fused.n_ctx, 1 + fused.n_ctx + q, dtype=np.int64)
+        c = cfg.critical_layer
+        crit = (pk[c - 1], pv[c - 1], n_pre) if n_layers >= c else None
+        return QueryProbe(toks, positions, q_store, fused.key_positions()[rows] if mode != PROBE_FULL
+                          else fused.key_positions(), crit, c)
+
+    def _score_dev(self, q_c: torch.Tensor, k_ctx: torch.Tensor, n_ctx: int, out: torch.Tensor,
+                   ws: torch.Tensor, stream=None) -> None:
+        cfg = self.config
+        call("qcf_score", self.weights.qcf_dtype, q_c.data_ptr(), k_ctx.data_ptr(), n_ctx,
+             q_c.shape[0], cfg.n_heads, cfg.n_kv_heads, cfg.d_head, 1.0 / math.sqrt(cfg.d_head),
+             1 if self.options.query_agg == "last" else 0, 1 if self.options.score_precise else 0,
+             out.data_ptr(), ws.data_ptr(), ws.numel(), cuda_stream(stream))
+
+    def score_against_keys(self, probe: QueryProbe, fused: FusedContext, layer: int) -> np.ndarray:
+        if self.options.query_agg not in ("mean", "last"):
+            raise ValueError(f"unknown query_agg: {self.options.query_agg}")
+        q_c = probe.q_store[layer - 1]
+        if q_c.shape[1] != self.config.n_heads or q_c.shape[2] != fused.k.shape[3]:
+            raise ValueError("probe and fused context disagree on head shape")
+        out = torch.empty(fused.n_ctx, dtype=torch.float32, device=self.device)
+        ws = torch.empty(int(_lib.lib.qcf_score_workspace(fused.n_ctx, q_c.shape[0], self.config.n_heads)),
+                         dtype=torch.uint8, device=self.device)
+        self._score_dev(q_c, fused.k[layer - 1, 1:], fused.n_ctx, out, ws)
+        return out.cpu().numpy()
+
+    def score_critical(self, probe: QueryProbe, fused: FusedContext) -> np.ndarray:
+        return self.score_against_keys(probe, fused, self.config.critical_layer)
+
+    def oracle_importance(self, context_tokens, query_tokens) -> np.ndarray:
+        """Critical-layer importance from a full GPU forward over
+        [BOS | context | query] (fusion.py:331-346)."""
+        ctx = np.asarray(context_tokens, np.int64)
+        qt = np.asarray(query_tokens, np.int64)
+        toks = _i32(np.concatenate([[BOS_ID], ctx, qt]), self.device)
+        c = self.config.critical_layer
+        m = toks.numel()
+        cfg = self.config
+        q_store = torch.empty((cfg.n_layers, m, cfg.n_heads, cfg.d_head), dtype=self.weights.torch_dtype,
+                              device=self.device)
+        tk, tv = self.ex.new_table(m)
+        ar = torch.arange(m, dtype=torch.int32, device=self.device)
+        self.ex.rope.ensure(m + 1)
+        sc = self.ex.scratch(m, key="oracle")
+        self.ex.embed(sc, m, toks)
+        self.ex.stack(sc, m, ar, ar, ar, tk, tv, layers=range(c), q_store=q_store)
+        out = torch.empty(ctx.size, dtype=torch.float32, device=self.device)
+        ws = torch.empty(int(_lib.lib.qcf_score_workspace(ctx.size, qt.size, cfg.n_heads)),
+                         dtype=torch.uint8, device=self.device)
+        self._score_dev(q_store[c - 1, 1 + ctx.size:].contiguous(), tk[c - 1, 1:1 + ctx.size],
+                        ctx.size, out, ws)
+        return out.cpu().numpy()
+
+    # ------------------------------------------------------------------
+    # selection policies (fusion.py:352-440)
+    # ------------------------------------------------------------------
+    def qcfuse_select(self, query_tokens, fused: FusedContext, ratio: float) -> SelectionResult:
+        probe = self.probe_query(query_tokens, fused, PROBE_ANCHORS, layers=self.config.critical_layer)
+        return select_topn(self.score_critical(probe, fused), ratio, "QCFuse")
+
+    def qclast_select(self, query_tokens, fused, ratio) -> SelectionResult:
+        probe = self.probe_query(query_tokens, fused, PROBE_NONE)
+        return select_topn(self.score_against_keys(probe, fused, self.config.n_layers), ratio, "QCLast")
+
+    def qcall_select(self, query_tokens, fused, ratio) -> SelectionResult:
+        probe = self.probe_query(query_tokens, fused, PROBE_FULL)
+        if self.options.qcall_layer_average:
+            scores = np.mean([self.score_against_keys(probe, fused, li)
+                              for li in range(1, self.config.n_layers + 1)], axis=0)
+        else:
+            scores = self.score_critical(probe, fused)
+        return select_topn(scores, ratio, "QCAll")
+
+    def select(self, policy: str, ratio: float, fused: FusedContext, query_tokens) -> SelectionResult:
+        if policy not in POLICIES:
+            raise ValueError(f"unknown policy: {policy}")
+        n = fused.n_ctx
+        if policy == "FullCompute":
+            return SelectionResult(policy, 1.0, np.arange(1, n + 1, dtype=np.int64), np.zeros(n, np.float32))
+        if policy == "FullReuse":
+            return SelectionResult(policy, 0.0, np.zeros(0, np.int64), np.zeros(n, np.float32))
+        if policy == "Random":
+            return random_select(self.options.selection_seed, n, ratio)
+        if policy == "EPIC":
+            spans = None
+            if self.options.epic_per_chunk:
+                spans = [(off, (fused.offsets + [n + 1])[i + 1] - off) for i, off in enumerate(fused.offsets)]
+            return epic_select(n, ratio, spans)
+        if policy == "QCLast":
+            return self.qclast_select(query_tokens, fused, ratio)
+        if policy == "QCAll":
+            return self.qcall_select(query_tokens, fused, ratio)
+        if policy in ("CacheBlend", "KVShare"):
+            raise NotImplementedError(f"{policy} is a comparison baseline outside the fused hot path "
+                                      "(SURVEY §8f rank 4)")
+        return self.qcfuse_select(query_tokens, fused, ratio)
+
+    # ------------------------------------------------------------------
+    # recomputation (fusion.py:446-490)
+    # ------------------------------------------------------------------
+    def recompute_selected(self, fused: FusedContext, selection: SelectionResult):
+        cfg = self.config
+        sel = np.asarray(selection.indices, dtype=np.int64)
+        if sel.size and (sel.min() < 1 or sel.max() > fused.n_ctx):
+            raise ValueError("selection indices out of context range")
+        new = fused.clone()
+        fetch, compute = layer_times(sel.size, fused.n_ctx, cfg, self.cost)
+        if sel.size:
+            dev = self.device
+            pos = _i32(sel, dev)
+            tok = _i32(np.concatenate([[BOS_ID], fused.token_ids]), dev)
+            sc = self.ex.scratch(sel.size, key="recompute_api")
+            self.ex.embed(sc, sel.size, tok, rows=pos)
+            self.ex.rope.ensure(fused.n_ctx + 2)
+            self.ex.stack(sc, sel.size, pos, pos, pos, new.k, new.v)
+            fetch_s, compute_s = [fetch] * cfg.n_layers, [compute] * cfg.n_layers
+        else:
+            fetch_s, compute_s = [fetch] * cfg.n_layers, [0.0] * cfg.n_layers
+        return new, RecomputeTrace(sel, fetch_s, compute_s)
+
+    # ------------------------------------------------------------------
+    # the fused fast path
+    # ------------------------------------------------------------------
+    def _plan(self, policy, ratio, chunk_ids, query_tokens) -> _Plan:
+        recs, offs, n_ctx = self._records(chunk_ids)
+        q = len(query_tokens)
+        if policy == "QCFuse":
+            n_sel = n_select(ratio, n_ctx)
+            rows = self._anchor_rows(recs, offs, PROBE_ANCHORS, n_ctx)
+        elif policy == "FullCompute":
+            n_sel, rows = n_ctx, np.zeros(1, np.int64)
+        elif policy == "FullReuse":
+            n_sel, rows = 0, np.zeros(1, np.int64)
+        else:
+            raise ValueError(f"fast path covers QCFuse/FullCompute/FullReuse, not {policy}")
+        return _Plan(list(chunk_ids), recs, offs, n_ctx, q, n_sel, rows, policy)
+
+    def _buffers(self, plan: _Plan, extra_rows: int = 0) -> _Bufs:
+        key = (tuple(r.n_tokens for r in plan.records), plan.q, plan.n_sel, plan.anchor_rows.size,
+               plan.policy, extra_rows)
+        b = self._bufs.get(key)
+        if b is None:
+            b = _Bufs(self, plan.n_ctx, plan.q, plan.n_sel, plan.anchor_rows.size, len(plan.records),
+                      extra_rows)
+            self._bufs[key] = b
+        return b
+
+    def _stage(self, plan: _Plan, b: _Bufs, query_tokens, stream=None) -> dict:
+        """Host → device copies of the request's inputs (chunk descriptors,
+        token table, probe rows). Returns the byte counts."""
+        desc = self._desc_bytes(plan.records, plan.offsets)
+        tok = np.concatenate([[BOS_ID], *[r.token_ids for r in plan.records],
+                              np.asarray(query_tokens, np.int64)]).astype(np.int32)
+        rows = plan.anchor_rows.astype(np.int32)
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            b.desc.copy_(desc.pin_memory(), non_blocking=True)
+            b.tok[:tok.size].copy_(torch.from_numpy(tok).pin_memory(), non_blocking=True)
+            b.anchor_rows[:rows.size].copy_(torch.from_numpy(rows).pin_memory(), non_blocking=True)
+        return {"h2d": desc.numel() + tok.nbytes + rows.nbytes}
+
+    def _launch(self, plan: _Plan, b: _Bufs, stream=None) -> None:
+        """Every kernel of one fused prefill, in order (see module docstring)."""
+        cfg, ex = self.config, self.ex
+        c, q, n_ctx, n_sel = cfg.critical_layer, plan.q, plan.n_ctx, plan.n_sel
+        s = cuda_stream(stream)
+        self._assemble_into(plan.records, plan.offsets, n_ctx, b.fk, b.fv, b.desc, stream)
+        if plan.policy == "QCFuse" and n_sel > 0:
+            call("qcf_gather_rows", b.fk.data_ptr(), b.fv.data_ptr(), b.fk.stride(0),
+                 b.anchor_rows.data_ptr(), b.n_pre, b.pk.data_ptr(), b.pv.data_ptr(), b.pk.stride(0),
+                 c, cfg.n_kv_heads * cfg.d_head, self.weights.qcf_dtype, s)
+            ex.embed(b.sc_probe, q, b.tok, rows=b.p_pos, stream=stream)
+            for li in range(c - 1):
+                ex.layer(li, b.sc_probe, q, b.p_pos, b.p_dst, b.p_dst, b.pk[li], b.pv[li], stream=stream)
+            ex.layer(c - 1, b.sc_probe, q, b.p_pos, b.p_dst, b.p_dst, b.pk[c - 1], b.pv[c - 1],
+                     q_only=True, q_out=b.qc[0], stream=stream)
+            self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream)
+            call("qcf_topn", b.scores.data_ptr(), n_ctx, n_sel, 1, b.rc_pos.data_ptr(), None, 0, s)
+        elif plan.policy == "FullCompute":
+            call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr(), s)
+        m = n_sel + q
+        ex.embed(b.sc_rc, m, b.tok, rows=b.rc_pos, stream=stream)
+        ex.stack(b.sc_rc, m, b.rc_pos, b.rc_pos, b.rc_pos, b.fk, b.fv, stream=stream)
+        ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
+
+    def prefill(self, policy: str, ratio: float, chunk_ids, query_tokens, use_graph: bool = True,
+                extra_rows: int = 0, stream=None):
+        """Device-side fused prefill up to first-token logits. Returns
+        (plan, buffers); logits in b.logits[0], selection in b.rc_pos[:n_sel]."""
+        plan = self._plan(policy, ratio, chunk_ids, query_tokens)
+        b = self._buffers(plan, extra_rows)
+        self._stage(plan, b, query_tokens, stream)
+        self.ex.rope.ensure(b.rows + 2)
+        if not use_graph:
+            self._launch(plan, b, stream)
+            return plan, b
+        if b.graph is None:
+            s = stream or torch.cuda.current_stream()
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(s)
+            with torch.cuda.stream(side):
+                self._launch(plan, b, side)       # warm-up (lazy attributes, workspaces)
+            s.wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._launch(plan, b, side)
+            s.wait_stream(side)
+            b.graph = g
+        b.graph.replay()
+        return plan, b
+
+    def fuse(self, query, chunk_ids, ratio: float = 0.15):
+        """North-star entry: fuse(query, chunks) → (first-token logits [V] f32
+        numpy, ascending selected positions). QCFuse policy."""
+        qt = byte_tokens(query) if isinstance(query, (str, bytes)) else list(query)
+        if not qt:
+            raise ValueError("query must be non-empty")
+        plan, b = self.prefill("QCFuse", ratio, chunk_ids, qt)
+        return b.logits[0].cpu().numpy(), b.rc_pos[:plan.n_sel].cpu().numpy().astype(np.int64)
+
+    # ------------------------------------------------------------------
+    # decode (model.py:433-465) over the fused table
+    # ------------------------------------------------------------------
+    def _decode(self, fk, fv, next_pos: int, first_logits: np.ndarray, max_new: int) -> list[int]:
+        if max_new < 1:
+            raise ValueError("max_new must be >= 1")
+        out, logits = [], first_logits
+        dev = self.device
+        tok = torch.empty(1, dtype=torch.int32, device=dev)
+        pos = torch.empty(1, dtype=torch.int32, device=dev)
+        zero = torch.zeros(1, dtype=torch.int32, device=dev)
+        lg = torch.empty((1, self.config.vocab_size), dtype=torch.float32, device=dev)
+        sc = self.ex.scratch(1, key="decode")
+        for step in range(max_new):
+            t = int(np.argmax(logits))
+            out.append(t)
+            if t == EOS_ID or step == max_new - 1:
+                break
+            tok.fill_(t)
+            pos.fill_(next_pos)
+            self.ex.rope.ensure(next_pos + 2)
+            self.ex.embed(sc, 1, tok)
+            self.ex.stack(sc, 1, pos, pos, pos, fk, fv)
+            self.ex.lm_head(sc, zero, lg)
+            logits = lg[0].cpu().numpy()
+            next_pos += 1
+        return out
+
+    # ------------------------------------------------------------------
+    # end to end (fusion.py:496-563)
+    # ------------------------------------------------------------------
+    def oracle_run(self, context_tokens, query_tokens, max_new: int | None = None) -> dict:
+        """Full-computation reference on the GPU (fusion.py:496-517): a full
+        prefill over [BOS | context | query], greedy decode, importance."""
+        max_new = max_new or self.options.max_new
+        key = (np.asarray(context_tokens, np.int64).tobytes(), np.asarray(query_tokens, np.int64).tobytes(),
+               max_new)
+        if key in self._oracle_cache:
+            return self._oracle_cache[key]
+        ctx = np.asarray(context_tokens, np.int64)
+        qt = np.asarray(query_tokens, np.int64)
+        toks = np.concatenate([[BOS_ID], ctx, qt])
+        m = toks.size
+        tk, tv = self.ex.new_table(m + max_new)
+        _, _, sc = self.ex.forward_full(_i32(toks, self.device), 0, tab=(tk, tv))
+        lg = torch.empty((1, self.config.vocab_size), dtype=torch.float32, device=self.device)
+        self.ex.lm_head(sc, torch.tensor([m - 1], dtype=torch.int32, device=self.device), lg)
+        first = lg[0].cpu().numpy()
+        answer = self._decode(tk, tv, m, first, max_new)
+        res = {"first_logits": first, "answer_tokens": answer,
+               "importance": self.oracle_importance(ctx, qt)}
+        self._oracle_cache[key] = res
+        return res
+
+    def run(self, policy: str, ratio: float, chunk_ids: list[str], query,
+            compare_oracle: bool = False, max_new: int | None = None) -> RunResult:
+        if policy not in POLICIES:
+            raise ValueError(f"unknown policy: {policy}")
+        if not (0.0 <= ratio <= 1.0):
+            raise ValueError("ratio must be in [0, 1]")
+        max_new = max_new or self.options.max_new
+        qt = byte_tokens(query) if isinstance(query, (str, bytes)) else list(query)
+        if not qt:
+            raise ValueError("query must be non-empty")
+        if not chunk_ids:
+            raise ValueError("chunk list must be non-empty")
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if policy in ("QCFuse", "FullCompute", "FullReuse") and self.options.query_agg == "mean":
+            ev0.record()
+            plan, b = self.prefill(policy, ratio, chunk_ids, qt, use_graph=False, extra_rows=max_new)
+            ev1.record()
+            n_ctx = plan.n_ctx
+            sel_idx = b.rc_pos[:plan.n_sel].cpu().numpy().astype(np.int64)
+            scores = (b.scores.cpu().numpy() if policy == "QCFuse" and plan.n_sel
+                      else np.zeros(n_ctx, np.float32))
+            selection = SelectionResult(policy, 1.0 if policy == "FullCompute" else
+                                        (0.0 if policy == "FullReuse" else ratio), sel_idx, scores)
+            first = b.logits[0].cpu().numpy()
+            fk, fv = b.fk, b.fv
+            token_ids = np.concatenate([r.token_ids for r in plan.records])
+        else:
+            ev0.record()
+            fused = self.assemble_context(chunk_ids, extra_rows=len(qt) + max_new)
+            selection = self.select(policy, ratio, fused, qt)
+            upd, _ = self.recompute_selected(fused, selection)
+            n_ctx = fused.n_ctx
+            fk, fv = upd.k, upd.v
+            m = len(qt)
+            pos = torch.arange(m, dtype=torch.int32, device=self.device) + (n_ctx + 1)
+            sc = self.ex.scratch(m, key="query_api")
+            self.ex.embed(sc, m, _i32(qt, self.device))
+            self.ex.stack(sc, m, pos, pos, pos, fk, fv)
+            lg = torch.empty((1, self.config.vocab_size), dtype=torch.float32, device=self.device)
+            self.ex.lm_head(sc, torch.tensor([m - 1], dtype=torch.int32, device=self.device), lg)
+            ev1.record()
+            first = lg[0].cpu().numpy()
+            sel_idx = selection.indices
+            token_ids = fused.token_ids
+        torch.cuda.synchronize()
+        ttft_ms = ev0.elapsed_time(ev1)
+        answer = self._decode(fk, fv, n_ctx + 1 + len(qt), first, max_new)
+        fetch, compute = layer_times(sel_idx.size, n_ctx, self.config, self.cost)
+        trace = RecomputeTrace(sel_idx, [fetch] * self.config.n_layers,
+                               [compute if sel_idx.size else 0.0] * self.config.n_layers)
+        schedule = policy_schedule(policy, sel_idx.size, n_ctx, len(qt), self.config, self.cost)
+        trace.events = schedule_events(schedule)
+        comparison = None
+        if compare_oracle:
+            from . import metrics
+            oracle = self.oracle_run(token_ids, qt, max_new)
+            div, kl = metrics.logit_divergence(oracle["first_logits"], first)
+            match = metrics.token_match_rate(oracle["answer_tokens"], answer, max_new)
+            top = top_n_positions(oracle["importance"], sel_idx.size)
+            comparison = OracleComparison(div, kl, match, metrics.selection_overlap(sel_idx, top))
+        return RunResult(policy, selection.ratio, answer, render_tokens(answer), first, selection,
+                         trace, schedule, schedule.ttft + self.cost.decode_gamma, comparison,
+                         {"ttft_device_ms": ttft_ms})

@@ -1,0 +1,248 @@
+"""Model configuration and device-resident weights.
+
+Mirrors the reference's `ModelConfig` (model.py:74-118, same fields, defaults,
+validation and `to_dict`, so store fingerprints agree) and generates the
+reference's splitmix64 weights ON THE GPU with `qcf_init_uniform`
+(model.py:225-257), bit-identical to the reference's float32 draws; bf16 mode
+rounds those float32 values to nearest bf16.
+
+Device layout (chosen for the tcgen05 GEMM, both operands K-major):
+  emb            f32  [V][d]            (embedding gather + tied lm-head)
+  wqkv           dt   [(H+2Hkv)·D][d]   = [Wq | Wk | Wv]ᵀ
+  wo             dt   [d][d]            = Woᵀ
+  w1             dt   [F][d]            = W1ᵀ
+  w2             dt   [d][F]            = W2ᵀ
+  ln*_g / ln*_b  f32  [d]
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import QCF_BF16, QCF_F32, call
+
+BOS_ID = 256
+EOS_ID = 257
+PAD_ID = 258
+VOCAB_SIZE = 259
+
+DTYPES = {"f32": (QCF_F32, torch.float32), "bf16": (QCF_BF16, torch.bfloat16)}
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """model.py:74-118."""
+    n_layers: int = 4
+    n_heads: int = 2
+    d_model: int = 32
+    d_head: int = 16
+    d_ff: int = 64
+    vocab_size: int = VOCAB_SIZE
+    rope_theta: float = 10000.0
+    ln_eps: float = 1e-5
+    seed: int = 1234
+    critical_layer: int | None = None  # 1-based; defaults to ceil(n_layers / 2)
+
+    def __post_init__(self):
+        if self.critical_layer is None:
+            object.__setattr__(self, "critical_layer", math.ceil(self.n_layers / 2))
+        self.validate()
+
+    def validate(self) -> None:
+        if self.d_model != self.n_heads * self.d_head:
+            raise ValueError("d_model must equal n_heads * d_head")
+        if self.n_layers < 4:
+            raise ValueError("n_layers must be >= 4")
+        if not (1 < self.critical_layer < self.n_layers):
+            raise ValueError("critical_layer must satisfy 1 < critical_layer < n_layers")
+        if self.vocab_size != VOCAB_SIZE:
+            raise ValueError(f"vocab_size must be {VOCAB_SIZE} (256 bytes + BOS/EOS/PAD)")
+        if self.d_head % 2 != 0:
+            raise ValueError("d_head must be even for rotary pairs")
+        if self.rope_theta <= 0 or self.ln_eps <= 0:
+            raise ValueError("rope_theta and ln_eps must be positive")
+
+    @property
+    def n_kv_heads(self) -> int:
+        return self.n_heads
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff",
+                                              "vocab_size", "rope_theta", "ln_eps", "seed",
+                                              "critical_layer")}
+
+    def layer_params(self) -> int:
+        d, f = self.d_model, self.d_ff
+        return 4 * d * d + 2 * d * f
+
+
+def tokenize(text) -> list[int]:
+    """BOS + bytes (model.py:181-185)."""
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    return [BOS_ID] + list(data)
+
+
+def byte_tokens(text) -> list[int]:
+    """Bytes, no BOS (model.py:188-191)."""
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    return list(data)
+
+
+def render_tokens(token_ids) -> str:
+    """Printable rendering (model.py:194-222)."""
+    out, buf = [], bytearray()
+
+    def flush():
+        if buf:
+            out.append(buf.decode("utf-8", errors="backslashreplace"))
+            buf.clear()
+
+    for t in token_ids:
+        t = int(t)
+        if t < 256:
+            if 32 <= t < 127 or t in (9, 10):
+                buf.append(t)
+            else:
+                flush()
+                out.append(f"\\x{t:02x}")
+        else:
+            flush()
+            out.append({BOS_ID: "<bos>", EOS_ID: "<eos>", PAD_ID: "<pad>"}[t])
+    flush()
+    return "".join(out)
+
+
+def cuda_stream(stream: torch.cuda.Stream | None = None):
+    s = stream or torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class DeviceLayer:
+    wqkv: torch.Tensor
+    wo: torch.Tensor
+    w1: torch.Tensor
+    w2: torch.Tensor
+    ln1_g: torch.Tensor
+    ln1_b: torch.Tensor
+    ln2_g: torch.Tensor
+    ln2_b: torch.Tensor
+
+
+@dataclass(eq=False)
+class ModelWeights:
+    """Device-resident weights (the reference's ModelWeights, model.py:136-141)."""
+    config: ModelConfig
+    dtype: str
+    emb: torch.Tensor
+    layers: list[DeviceLayer]
+    ln_f_gain: torch.Tensor
+    ln_f_bias: torch.Tensor
+    device: torch.device = field(default_factory=lambda: torch.device("cuda"))
+
+    @property
+    def qcf_dtype(self) -> int:
+        return DTYPES[self.dtype][0]
+
+    @property
+    def torch_dtype(self) -> torch.dtype:
+        return DTYPES[self.dtype][1]
+
+    @property
+    def token_embedding(self) -> np.ndarray:
+        return self.emb.cpu().numpy()
+
+    @classmethod
+    def from_host(cls, config: ModelConfig, token_embedding, layers, dtype="bf16",
+                  device="cuda") -> "ModelWeights":
+        """From host arrays in the reference layout: layers is a sequence of
+        objects with wq wk wv wo w1 w2 ([d_in][d_out]) and ln gains/biases."""
+        dev = torch.device(device)
+        tdt = DTYPES[dtype][1]
+
+        def t(a, dt=tdt):
+            return torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+
+        dl = []
+        for lw in layers:
+            wqkv = np.concatenate([lw.wq, lw.wk, lw.wv], axis=1).T
+            dl.append(DeviceLayer(t(wqkv), t(lw.wo.T), t(lw.w1.T), t(lw.w2.T),
+                                  t(_get(lw, "ln1_gain", "ln1_g"), torch.float32),
+                                  t(_get(lw, "ln1_bias", "ln1_b"), torch.float32),
+                                  t(_get(lw, "ln2_gain", "ln2_g"), torch.float32),
+                                  t(_get(lw, "ln2_bias", "ln2_b"), torch.float32)))
+        d = config.d_model
+        ones = torch.ones(d, dtype=torch.float32, device=dev)
+        return cls(config, dtype, t(token_embedding, torch.float32), dl, ones, torch.zeros_like(ones), dev)
+
+
+def _get(obj, *names):
+    for n in names:
+        if hasattr(obj, n):
+            return getattr(obj, n)
+    raise AttributeError(names[0])
+
+
+def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
+                 layers: int | None = None) -> ModelWeights:
+    """GPU restatement of init_weights (model.py:225-257): stream order
+    embedding, then per layer wq wk wv wo w1 w2, each row-major."""
+    config.validate()
+    dev = torch.device(device)
+    qdt, tdt = DTYPES[dtype]
+    d, f, V = config.d_model, config.d_ff, config.vocab_size
+    s = cuda_stream()
+    seed = config.seed & ((1 << 64) - 1)
+    emb = torch.empty(V, d, dtype=torch.float32, device=dev)
+    call("qcf_init_uniform", seed, 0, V, d, 0, QCF_F32, emb.data_ptr(), d, s)
+    off = V * d
+    n_build = config.n_layers if layers is None else layers
+    dl = []
+    for _ in range(n_build):
+        wqkv = torch.empty(3 * d, d, dtype=tdt, device=dev)
+        wo = torch.empty(d, d, dtype=tdt, device=dev)
+        w1 = torch.empty(f, d, dtype=tdt, device=dev)
+        w2 = torch.empty(d, f, dtype=tdt, device=dev)
+        esz = wqkv.element_size()
+        for j in range(3):  # wq, wk, wv -> rows [j*d, (j+1)*d) of wqkv
+            call("qcf_init_uniform", seed, off, d, d, 1, qdt, wqkv.data_ptr() + j * d * d * esz, d, s)
+            off += d * d
+        call("qcf_init_uniform", seed, off, d, d, 1, qdt, wo.data_ptr(), d, s)
+        off += d * d
+        call("qcf_init_uniform", seed, off, d, f, 1, qdt, w1.data_ptr(), d, s)
+        off += d * f
+        call("qcf_init_uniform", seed, off, f, d, 1, qdt, w2.data_ptr(), f, s)
+        off += f * d
+        ones = torch.ones(d, dtype=torch.float32, device=dev)
+        zeros = torch.zeros(d, dtype=torch.float32, device=dev)
+        dl.append(DeviceLayer(wqkv, wo, w1, w2, ones, zeros, ones.clone(), zeros.clone()))
+    ones = torch.ones(d, dtype=torch.float32, device=dev)
+    return ModelWeights(config, dtype, emb, dl, ones, torch.zeros_like(ones), dev)
+
+
+class RopeTable:
+    """float64 cos/sin [n_pos][D/2] on the device, built with numpy exactly as
+    the reference builds its angles (model.py:264-280): angle = pos · θ^(−2j/D)
+    in float64, np.cos / np.sin. Grows on demand; positions index rows."""
+
+    def __init__(self, d_head: int, theta: float, device, n_pos: int = 8192):
+        self.d_head, self.theta, self.device = d_head, theta, torch.device(device)
+        self.n_pos = 0
+        self.cos = self.sin = None
+        self.ensure(n_pos)
+
+    def ensure(self, n_pos: int) -> None:
+        if n_pos <= self.n_pos:
+            return
+        n = max(n_pos, 2 * self.n_pos)
+        j = np.arange(self.d_head // 2, dtype=np.float64)
+        inv = self.theta ** (-2.0 * j / self.d_head)
+        ang = np.arange(n, dtype=np.float64)[:, None] * inv[None, :]
+        self.cos = torch.as_tensor(np.cos(ang)).to(self.device)
+        self.sin = torch.as_tensor(np.sin(ang)).to(self.device)
+        self.n_pos = n

@@ -1,0 +1,138 @@
+"""The decoder layer stack as a sequence of C-ABI kernel launches.
+
+One executor serves every hot-path forward of the reference:
+  * selective recompute + query rows (fusion.py:446-490 fused with 536-540),
+  * the anchor probe (fusion.py:269-311 → model.py:403-424),
+  * chunk precompute / full prefill (model.py:391-400), decode steps (433-465).
+Each is "M rows at positions `pos`, writing their fresh K/V into table rows
+`dst`, attending to table rows 0..kmax[i]" (model.py:345-388 with the mask of
+fusion.py:467). Launches only — no host synchronisation — so a whole request
+can be captured into a CUDA graph.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import EPI_ADD_F32, EPI_RELU, EPI_STORE, QCF_F32, call
+from .model import ModelWeights, RopeTable, cuda_stream
+
+
+@dataclass
+class Scratch:
+    """Per-M activations (fixed addresses once allocated; graph friendly)."""
+    cap: int
+    x: torch.Tensor      # f32 [cap, d] residual stream
+    a: torch.Tensor      # dt  [cap, d] LN output (GEMM A operand)
+    qkv: torch.Tensor    # f32 [cap, (H+2Hkv)D]
+    q: torch.Tensor      # dt  [cap, H, D] rotated queries
+    o: torch.Tensor      # dt  [cap, H*D] attention output
+    hid: torch.Tensor    # dt  [cap, F]   relu(W1 x)
+
+
+class Executor:
+    def __init__(self, weights: ModelWeights, rope: RopeTable | None = None):
+        self.w = weights
+        self.cfg = weights.config
+        self.rope = rope or RopeTable(self.cfg.d_head, self.cfg.rope_theta, weights.device)
+        self._scratch: dict[int, Scratch] = {}
+
+    # ------------------------------------------------------------------
+    def scratch(self, m: int, key=None) -> Scratch:
+        """Scratch with capacity >= m; `key` separates independent users (graphs)."""
+        k = key if key is not None else "default"
+        s = self._scratch.get(k)
+        if s is None or s.cap < m:
+            cfg, dev, dt = self.cfg, self.w.device, self.w.torch_dtype
+            cap = max(m, 16)
+            H, Hkv, D = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
+            s = Scratch(cap,
+                        torch.empty(cap, cfg.d_model, dtype=torch.float32, device=dev),
+                        torch.empty(cap, cfg.d_model, dtype=dt, device=dev),
+                        torch.empty(cap, (H + 2 * Hkv) * D, dtype=torch.float32, device=dev),
+                        torch.empty(cap, H, D, dtype=dt, device=dev),
+                        torch.empty(cap, H * D, dtype=dt, device=dev),
+                        torch.empty(cap, cfg.d_ff, dtype=dt, device=dev))
+            self._scratch[k] = s
+        return s
+
+    # ------------------------------------------------------------------
+    def embed(self, sc: Scratch, m: int, tokens: torch.Tensor, rows: torch.Tensor | None = None,
+              row_base: int = 0, stream=None) -> None:
+        call("qcf_embed", tokens.data_ptr(), rows.data_ptr() if rows is not None else None,
+             row_base, m, self.w.emb.data_ptr(), self.cfg.d_model, sc.x.data_ptr(),
+             cuda_stream(stream))
+
+    def layer(self, li: int, sc: Scratch, m: int, pos: torch.Tensor, dst: torch.Tensor,
+              kmax: torch.Tensor, tab_k: torch.Tensor, tab_v: torch.Tensor,
+              q_only: bool = False, q_out: torch.Tensor | None = None, stream=None) -> None:
+        """One decoder layer (model.py:359-376) over m rows.
+
+        tab_k/tab_v: [n_rows, Hkv, D] views of THIS layer's table. With q_only
+        the layer stops after LN1 → QKV → RoPE (the probe's critical-layer Q)."""
+        cfg, w = self.cfg, self.w
+        lw = w.layers[li]
+        d, H, Hkv, D, F = cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.d_head, cfg.d_ff
+        dt = w.qcf_dtype
+        s = cuda_stream(stream)
+        nq = (H + 2 * Hkv) * D
+        call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln1_g.data_ptr(), lw.ln1_b.data_ptr(),
+             cfg.ln_eps, sc.a.data_ptr(), dt, s)
+        call("qcf_gemm", dt, sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, sc.qkv.data_ptr(), nq,
+             m, nq, d, EPI_STORE, QCF_F32, s)
+        qdst = q_out if q_out is not None else sc.q
+        call("qcf_rope_qkv_scatter", sc.qkv.data_ptr(), m, H, Hkv, D, pos.data_ptr(),
+             dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(), self.rope.n_pos,
+             qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
+        if q_only:
+            return
+        call("qcf_attention", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
+             kmax.data_ptr(), m, H, Hkv, D, tab_k.shape[0], sc.o.data_ptr(), s)
+        call("qcf_gemm", dt, sc.o.data_ptr(), H * D, lw.wo.data_ptr(), H * D, sc.x.data_ptr(), d,
+             m, d, H * D, EPI_ADD_F32, QCF_F32, s)
+        call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln2_g.data_ptr(), lw.ln2_b.data_ptr(),
+             cfg.ln_eps, sc.a.data_ptr(), dt, s)
+        call("qcf_gemm", dt, sc.a.data_ptr(), d, lw.w1.data_ptr(), d, sc.hid.data_ptr(), F,
+             m, F, d, EPI_RELU, dt, s)
+        call("qcf_gemm", dt, sc.hid.data_ptr(), F, lw.w2.data_ptr(), F, sc.x.data_ptr(), d,
+             m, d, F, EPI_ADD_F32, QCF_F32, s)
+
+    def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
+              layers: range | None = None, q_store: torch.Tensor | None = None, stream=None) -> None:
+        """Run layers over m rows. tab_k/tab_v: [L, n_rows, Hkv, D].
+        q_store (optional) [L, m, H, D] receives each layer's rotated Q."""
+        layers = range(self.cfg.n_layers) if layers is None else layers
+        for li in layers:
+            self.layer(li, sc, m, pos, dst, kmax, tab_k[li], tab_v[li],
+                       q_out=q_store[li] if q_store is not None else None, stream=stream)
+
+    def lm_head(self, sc: Scratch, rows: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+        """logits[r] = LN_f(x[rows[r]]) @ embᵀ (model.py:384-385)."""
+        cfg = self.cfg
+        call("qcf_lm_head", sc.x.data_ptr(), rows.data_ptr(), rows.numel(), cfg.d_model,
+             self.w.ln_f_gain.data_ptr(), self.w.ln_f_bias.data_ptr(), cfg.ln_eps,
+             self.w.emb.data_ptr(), cfg.vocab_size, out.data_ptr(), cuda_stream(stream))
+
+    # ------------------------------------------------------------------
+    def new_table(self, n_rows: int) -> tuple[torch.Tensor, torch.Tensor]:
+        cfg = self.cfg
+        shape = (cfg.n_layers, n_rows, cfg.n_kv_heads, cfg.d_head)
+        return (torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device),
+                torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device))
+
+    def forward_full(self, tokens: torch.Tensor, start: int = 0, tab=None, want_logits_rows=None,
+                     stream=None):
+        """Full causal forward of `tokens` at positions start.. (model.py:391-400).
+        Returns (table K, table V, x scratch). Table row i = token i."""
+        m = tokens.numel()
+        self.rope.ensure(start + m + 1)
+        dev = self.w.device
+        tk, tv = tab if tab is not None else self.new_table(m)
+        ar = torch.arange(m, dtype=torch.int32, device=dev)
+        pos = ar + start
+        sc = self.scratch(m, key=("full", m))
+        self.embed(sc, m, tokens, stream=stream)
+        self.stack(sc, m, pos, ar, ar, tk, tv, stream=stream)
+        return tk, tv, sc

@@ -152,5 +152,34 @@ def main():
     print("wrote fixtures to", HERE)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def extra_fixtures():
+    """Reference-written .qcfk chunk + manifest, random_select / epic_select
+    outputs, policy schedules (host-logic parity)."""
+    model, store_mod, fusion = _import_reference()
+    import qcfuse.pipeline as pipeline
+    cfg = model.ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+    w = model.init_weights(cfg)
+    root = HERE / "ref_store"
+    if root.exists():
+        shutil.rmtree(root)
+    st = store_mod.ChunkStore(root, cfg)
+    toks = [int(t) for t in np.random.default_rng(77).integers(0, 256, 19)]
+    rec = st.precompute(w, toks, 0.25, "ref-chunk")
+    out = {"chunk_id": rec.chunk_id, "anchors": rec.anchor_indices.tolist(),
+           "fingerprint": store_mod.config_fingerprint(cfg)}
+    rs = {}
+    for seed, n, r in [(0, 37, 0.3), (5, 100, 0.15), (9, 7, 1.0), (3, 50, 0.0)]:
+        rs[f"{seed}_{n}_{r}"] = fusion.random_select(seed, n, r).indices.tolist()
+    out["random_select"] = rs
+    out["epic"] = fusion.epic_select(40, 0.2, [(1, 15), (16, 25)]).indices.tolist()
+    sch = pipeline.policy_schedule("QCFuse", 51, 256, 16, model.ModelConfig(), pipeline.CostModel())
+    out["schedule_qcfuse"] = {"ttft": sch.ttft, "compute_end": sch.compute_end, "pre": sch.pre_phase}
+    (HERE / "host_logic.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "extra":
+    extra_fixtures()

@@ -1,0 +1,245 @@
+"""Kernel-level parity on the B200 through the C ABI.
+
+Floating-point kernels are checked against a plain PyTorch fp32 reference of
+the same op (tolerances stated per test); integer/ordering kernels (Top-N,
+init, gather, V copy) are checked bit-exact."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+torch.backends.cuda.matmul.allow_tf32 = False
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2604_08585_b200 import _lib
+    return _lib
+
+
+def S():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def p(t):
+    return t.data_ptr() if t is not None else None
+
+
+# ---------------------------------------------------------------- init
+def test_init_uniform_bit_exact_vs_oracle(L):
+    from oracle import qcfuse_oracle as O
+    rows, cols, start = 37, 53, 123456789
+    ref = O.draw_uniform_f32(1234, start, rows * cols).reshape(rows, cols)
+    out = torch.empty(rows, cols, dtype=torch.float32, device="cuda")
+    L.call("qcf_init_uniform", 1234, start, rows, cols, 0, L.QCF_F32, p(out), cols, S())
+    assert np.array_equal(out.cpu().numpy(), ref)
+    outt = torch.empty(cols, rows, dtype=torch.float32, device="cuda")
+    L.call("qcf_init_uniform", 1234, start, rows, cols, 1, L.QCF_F32, p(outt), rows, S())
+    assert np.array_equal(outt.cpu().numpy(), ref.T)
+    outb = torch.empty(cols, rows, dtype=torch.bfloat16, device="cuda")
+    L.call("qcf_init_uniform", 1234, start, rows, cols, 1, L.QCF_BF16, p(outb), rows, S())
+    assert torch.equal(outb.cpu(), torch.as_tensor(ref.T).to(torch.bfloat16))
+
+
+def test_init_weights_matches_oracle_small():
+    import paper_2604_08585_b200 as Q
+    from oracle import qcfuse_oracle as O
+    cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+    w = Q.init_weights(cfg, dtype="f32")
+    ow = O.init_weights(O.Config(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234))
+    assert np.array_equal(w.emb.cpu().numpy(), ow.emb)
+    for dl, ol in zip(w.layers, ow.layers):
+        wqkv = np.concatenate([ol.wq, ol.wk, ol.wv], axis=1).T
+        assert np.array_equal(dl.wqkv.cpu().numpy(), wqkv)
+        assert np.array_equal(dl.wo.cpu().numpy(), ol.wo.T)
+        assert np.array_equal(dl.w1.cpu().numpy(), ol.w1.T)
+        assert np.array_equal(dl.w2.cpu().numpy(), ol.w2.T)
+
+
+def test_init_llama_width_draws_match_golden(golden_dir):
+    import paper_2604_08585_b200 as Q
+    z = np.load(golden_dir / "init_llama_probe.npz")
+    cfg = Q.ModelConfig(n_layers=32, n_heads=32, d_model=4096, d_head=128, d_ff=14336, seed=1234)
+    w = Q.init_weights(cfg, dtype="f32", layers=1)  # embedding + layer 1 (the first 13 tensors' heads)
+    # draw s of tensor j lands at a known element; check embedding + wq/wk/wv/wo/w1/w2 of layer 1
+    d, f, V = 4096, 14336, 259
+    emb = w.emb.cpu().numpy().ravel()
+    assert np.array_equal(emb[:16], z["values"][:16])
+    l0 = w.layers[0]
+    wq = l0.wqkv[:d].T.contiguous().cpu().numpy().ravel()
+    assert np.array_equal(wq[:16], z["values"][16:32])
+    w2 = l0.w2.T.contiguous().cpu().numpy().ravel()
+    assert np.array_equal(w2[:16], z["values"][96:112])
+
+
+# ---------------------------------------------------------------- GEMM
+GEMM_SHAPES = [(1, 259, 64), (33, 96, 32), (128, 256, 256), (800, 1024, 512), (300, 384, 4096),
+               (32, 12288, 4096)]
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_vs_torch_fp32(L, m, n, k, dtype, epi):
+    torch.manual_seed(m * 7 + n + k)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    qdt = L.QCF_F32 if dtype == "f32" else L.QCF_BF16
+    a = (torch.randn(m, k, device="cuda") * 0.5).to(tdt)
+    b = (torch.randn(n, k, device="cuda") * 0.05).to(tdt)
+    ref = a.float() @ b.float().T
+    out_dt = L.QCF_F32 if epi == 2 or dtype == "f32" else L.QCF_BF16
+    c0 = torch.randn(m, n, device="cuda") if epi == 2 else None
+    c = c0.clone() if epi == 2 else torch.empty(m, n, device="cuda",
+                                                 dtype=torch.float32 if out_dt == L.QCF_F32 else torch.bfloat16)
+    L.call("qcf_gemm", qdt, p(a), k, p(b), k, p(c), n, m, n, k, epi, out_dt, S())
+    if epi == 1:
+        ref = torch.relu(ref)
+    if epi == 2:
+        ref = c0 + ref
+    scale = ref.abs().max().item()
+    tol = 2e-6 * math.sqrt(k) * max(scale, 1.0)          # fp32 accumulation-order noise
+    if out_dt == L.QCF_BF16:
+        tol += scale * 2 ** -8                            # one bf16 rounding of the output
+    err = (c.float() - ref).abs().max().item()
+    assert err < tol, (err, tol)
+
+
+@pytest.mark.parametrize("m,n,k", [(800, 12288, 4096), (129, 4096, 14336), (5, 512, 128)])
+def test_gemm_tensor_core_matches_simt(L, m, n, k):
+    torch.manual_seed(0)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    c1 = torch.empty(m, n, device="cuda")
+    c2 = torch.empty(m, n, device="cuda")
+    L.call("qcf_gemm", L.QCF_BF16, p(a), k, p(b), k, p(c1), n, m, n, k, 0, L.QCF_F32, S())
+    L.call("qcf_gemm_simt", L.QCF_BF16, p(a), k, p(b), k, p(c2), n, m, n, k, 0, L.QCF_F32, S())
+    assert (c1 - c2).abs().max().item() < 1e-3 * math.sqrt(k / 128)
+
+
+# ---------------------------------------------------------------- attention
+def torch_attention(q, k, v, kmax):
+    m, H, D = q.shape
+    n, Hkv, _ = k.shape
+    rep = H // Hkv
+    kk = k.float().repeat_interleave(rep, dim=1)
+    vv = v.float().repeat_interleave(rep, dim=1)
+    s = torch.einsum("mhd,nhd->hmn", q.float(), kk) / math.sqrt(D)
+    mask = torch.arange(n, device=q.device)[None, :] <= kmax[:, None]
+    s = s.masked_fill(~mask[None], float("-inf"))
+    w = torch.softmax(s, dim=-1)
+    return torch.einsum("hmn,nhd->mhd", w, vv)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("m,n,H,D", [(7, 40, 2, 16), (77, 513, 4, 64), (200, 1100, 8, 128),
+                                     (32, 291, 32, 128), (1, 5, 2, 8)])
+def test_attention_location_aware(L, dtype, m, n, H, D):
+    torch.manual_seed(m + n)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    qdt = L.QCF_F32 if dtype == "f32" else L.QCF_BF16
+    q = torch.randn(m, H, D, device="cuda").to(tdt)
+    k = torch.randn(n, H, D, device="cuda").to(tdt)
+    v = torch.randn(n, H, D, device="cuda").to(tdt)
+    kmax = torch.sort(torch.randint(0, n, (m,), device="cuda")).values.int()
+    out = torch.empty_like(q)
+    L.call("qcf_attention", qdt, p(q), p(k), p(v), p(kmax), m, H, H, D, n, p(out), S())
+    ref = torch_attention(q, k, v, kmax.long())
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    assert (out.float() - ref).abs().max().item() < tol
+
+
+# ---------------------------------------------------------------- Top-N
+@pytest.mark.parametrize("n,frac,levels", [(5120, 0.15, None), (512, 0.15, None), (1000, 0.3, 4),
+                                           (37, 1.0, None), (64, 0.0, None), (32768, 0.15, 16),
+                                           (1, 1.0, None), (300, 0.5, 1)])
+def test_topn_bit_exact(L, n, frac, levels):
+    rng = np.random.default_rng(n)
+    if levels:
+        s = rng.choice(np.linspace(0, 1, levels), size=n).astype(np.float32)   # heavy ties
+    else:
+        s = rng.random(n).astype(np.float32)
+    k = math.ceil(frac * n)
+    ref = np.sort(np.argsort(-s.astype(np.float64), kind="stable")[:k]) + 1
+    ts = torch.as_tensor(s, device="cuda")
+    out = torch.full((max(k, 1),), -7, dtype=torch.int32, device="cuda")
+    L.call("qcf_topn", p(ts), n, k, 1, p(out), None, 0, S())
+    assert np.array_equal(out[:k].cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------- scoring
+@pytest.mark.parametrize("agg", ["mean", "last"])
+def test_score_vs_oracle_and_topn_on_reference_inputs(L, golden_dir, agg):
+    """Kernel-level selection parity: the reference's own Q_c and the oracle's
+    fused K_c (assembly is bit-exact) through qcf_score + qcf_topn reproduce the
+    reference's selected index set exactly (zero tolerance)."""
+    from oracle import qcfuse_oracle as O
+    from tests.gpu_util import oracle_cfg_from_golden
+    for name in ["tiny_case0", "tiny_case1", "tiny_case2", "tiny_case3", "tiny_case4", "tiny_case5",
+                 "small_case0", "small_case1"]:
+        z = np.load(golden_dir / f"{name}.npz")
+        oc = oracle_cfg_from_golden(z)
+        ow = O.init_weights(oc)
+        nc = len([f for f in z.files if f.startswith("chunk") and f.endswith("_tokens")])
+        chunks = [O.precompute_chunk(ow, z[f"chunk{i}_tokens"], float(z["anchor_ratio"])) for i in range(nc)]
+        fused = O.assemble(ow, chunks)
+        c = oc.critical_layer
+        kc = fused.keys[c - 1][1:]
+        qc = z["q_c"]
+        ref_scores = O.score_against_keys(qc, kc, oc.d_head, agg)
+        tq = torch.as_tensor(qc, device="cuda")
+        tk = torch.as_tensor(kc, device="cuda")
+        n_ctx = kc.shape[0]
+        scores = torch.empty(n_ctx, device="cuda")
+        ws = torch.empty(int(L.lib.qcf_score_workspace(n_ctx, qc.shape[0], oc.n_heads)), dtype=torch.uint8,
+                         device="cuda")
+        L.call("qcf_score", L.QCF_F32, p(tq), p(tk), n_ctx, qc.shape[0], oc.n_heads, oc.n_heads, oc.d_head,
+               1.0 / math.sqrt(oc.d_head), 1 if agg == "last" else 0, 1, p(scores), p(ws), ws.numel(), S())
+        got = scores.cpu().numpy()
+        assert np.abs(got - ref_scores).max() <= 2e-7 * ref_scores.max() * 8
+        if agg == "mean":
+            assert np.abs(got - z["scores"]).max() <= 1e-6
+            n_sel = math.ceil(float(z["ratio"]) * n_ctx)
+            idx = torch.empty(n_sel, dtype=torch.int32, device="cuda")
+            L.call("qcf_topn", p(scores), n_ctx, n_sel, 1, p(idx), None, 0, S())
+            assert np.array_equal(idx.cpu().numpy(), z["selection"]), name
+
+
+# ---------------------------------------------------------------- assembly / rope
+def test_assemble_bit_exact_vs_oracle(golden_dir, tmp_path):
+    from tests.gpu_util import golden_setup
+    z, oc, ow, chunks, w, store, ids, eng = golden_setup(golden_dir, "small_case1", "f32", tmp_path)
+    from oracle import qcfuse_oracle as O
+    ref = O.assemble(ow, chunks)
+    fused = eng.assemble_context(ids)
+    assert fused.offsets == ref.offsets
+    for li in range(oc.n_layers):
+        # BOS row from the GPU forward; chunk rows: float64 re-rotation is bit-exact
+        assert np.array_equal(fused.layer_kv[li].keys[1:], ref.keys[li][1:])
+        assert np.array_equal(fused.layer_kv[li].values[1:], ref.values[li][1:])
+        assert np.abs(fused.layer_kv[li].keys[0] - ref.keys[li][0]).max() < 1e-6
+
+
+def test_rope_scatter_exact_rotation(L):
+    from oracle import qcfuse_oracle as O
+    import paper_2604_08585_b200 as Q
+    rng = np.random.default_rng(3)
+    m, H, D = 9, 2, 16
+    qkv = rng.normal(size=(m, 3 * H * D)).astype(np.float32)
+    pos = np.array([1, 5, 17, 300, 4096, 4097, 5000, 6, 7], np.int32)
+    rope = Q.model.RopeTable(D, 10000.0, "cuda", 8192)
+    tq = torch.as_tensor(qkv, device="cuda")
+    qo = torch.empty(m, H, D, device="cuda")
+    kt = torch.zeros(8, H, D, device="cuda")
+    vt = torch.zeros(8, H, D, device="cuda")
+    dst = torch.as_tensor(np.arange(m, dtype=np.int32) % 8, device="cuda")
+    dst = torch.as_tensor(np.array([0, 1, 2, 3, 4, 5, 6, 7, 7], np.int32)[:m], device="cuda")
+    tp = torch.as_tensor(pos, device="cuda")
+    L.call("qcf_rope_qkv_scatter", p(tq), m, H, H, D, p(tp), p(dst), p(rope.cos), p(rope.sin), rope.n_pos,
+           p(qo), p(kt), p(vt), L.QCF_F32, S())
+    ref_q = O.rope(qkv[:, :H * D].reshape(m, H, D), pos, 10000.0)
+    assert np.array_equal(qo.cpu().numpy(), ref_q)
+    ref_k = O.rope(qkv[:, H * D:2 * H * D].reshape(m, H, D), pos, 10000.0)
+    assert np.array_equal(kt.cpu().numpy()[:7], ref_k[:7])

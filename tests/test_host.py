@@ -1,0 +1,185 @@
+"""CPU tests (no GPU): the C-ABI library loads and exports every declared
+symbol; the host-side logic (store format, manifest, selection helpers, cost
+model, request sharding) matches the reference's behaviour."""
+
+import json
+import re
+import shutil
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "qcfuse_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(qcf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2604_08585_b200 import _lib
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(_lib.lib, s), s
+        assert s in _lib.SIGNATURES, f"{s} declared in the header but not bound"
+    assert set(_lib.SIGNATURES) == set(syms)
+    assert _lib.lib.qcf_version().startswith(b"qcfuse_b200")
+
+
+def test_library_is_sm100a():
+    import subprocess
+    so = ROOT / "paper_2604_08585_b200" / "libqcfuse_b200.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_errors_map_to_reference_exceptions():
+    from paper_2604_08585_b200 import _lib
+    with pytest.raises(ValueError):
+        _lib.call("qcf_topn", None, 10, 3, 1, None, None, 0, None)
+    with pytest.raises(ValueError):
+        _lib.call("qcf_gemm", 0, None, 1, None, 1, None, 1, 1, 1, 1, 0, 0, None)
+
+
+def test_qcfk_reads_reference_written_file(tmp_path, golden_dir):
+    from paper_2604_08585_b200.model import ModelConfig
+    from paper_2604_08585_b200.store import (config_fingerprint, read_qcfk, write_qcfk, chunk_hash,
+                                              Manifest)
+    host = json.loads((golden_dir / "host_logic.json").read_text())
+    cfg = ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+    assert config_fingerprint(cfg) == host["fingerprint"]
+    src = golden_dir / "ref_store"
+    man = Manifest.loads((src / "manifest.txt").read_text())
+    assert man.fingerprint == host["fingerprint"]
+    rel = man.chunks[host["chunk_id"]][0]
+    toks, k, v, norms, anchors, name = read_qcfk(src / rel, host["fingerprint"])
+    assert chunk_hash(toks) == host["chunk_id"]
+    assert anchors.tolist() == host["anchors"] and name == "ref-chunk"
+    assert k.shape == (4, 19, 2, 16)
+    # byte-identical rewrite (format parity, store.py:134-155)
+    out = tmp_path / "x.qcfk"
+    write_qcfk(out, host["fingerprint"], toks, k, v, norms, anchors, name)
+    assert out.read_bytes() == (src / rel).read_bytes()
+
+
+def test_qcfk_corruption_and_fingerprint(tmp_path, golden_dir):
+    from paper_2604_08585_b200.store import FingerprintMismatch, StoreError, read_qcfk
+    host = json.loads((golden_dir / "host_logic.json").read_text())
+    src = next((golden_dir / "ref_store").rglob("*.qcfk"))
+    raw = src.read_bytes()
+    bad = tmp_path / "bad.qcfk"
+    bad.write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(StoreError):
+        read_qcfk(bad, None)
+    bad.write_bytes(raw[:-3])
+    with pytest.raises(StoreError):
+        read_qcfk(bad, None)
+    with pytest.raises(FingerprintMismatch):
+        read_qcfk(src, "00" * 32)
+
+
+def test_store_opens_reference_store_and_rejects_other_config(tmp_path, golden_dir):
+    from paper_2604_08585_b200.model import ModelConfig
+    from paper_2604_08585_b200.store import ChunkStore, FingerprintMismatch
+    root = tmp_path / "s"
+    shutil.copytree(golden_dir / "ref_store", root)
+    cfg = ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+    st = ChunkStore(root, cfg, dtype="f32", device="cpu")
+    host = json.loads((golden_dir / "host_logic.json").read_text())
+    assert host["chunk_id"] in st
+    rec = st.get_record(host["chunk_id"])          # device="cpu" here: pool on host for the test
+    assert rec.n_tokens == 19 and rec.anchor_indices.tolist() == host["anchors"]
+    with pytest.raises(KeyError):
+        st.get_record("ab" * 32)
+    with pytest.raises(FingerprintMismatch):
+        ChunkStore(root, ModelConfig(seed=99), device="cpu")
+
+
+def test_extract_anchors_rules():
+    from paper_2604_08585_b200.store import extract_anchors
+    assert extract_anchors([3.0, 1.0, 2.0], 1 / 3).tolist() == [0]
+    assert extract_anchors([1.0, 1.0], 0.5).tolist() == [0]
+    assert extract_anchors([0.5, 2.0, 1.0], 1.0).tolist() == [0, 1, 2]
+    with pytest.raises(ValueError):
+        extract_anchors([], 0.5)
+
+
+def test_random_and_epic_select_match_reference(golden_dir):
+    from paper_2604_08585_b200.fusion import epic_select, random_select, n_select
+    host = json.loads((golden_dir / "host_logic.json").read_text())
+    for key, idx in host["random_select"].items():
+        seed, n, r = key.split("_")
+        assert random_select(int(seed), int(n), float(r)).indices.tolist() == idx
+    assert epic_select(40, 0.2, [(1, 15), (16, 25)]).indices.tolist() == host["epic"]
+    assert n_select(0.07, 100) == 8          # ceil in double (fusion.py:155)
+    with pytest.raises(ValueError):
+        n_select(1.5, 10)
+
+
+def test_cost_model_schedule_matches_reference(golden_dir):
+    from paper_2604_08585_b200.model import ModelConfig
+    from paper_2604_08585_b200.pipeline import CostModel, policy_schedule, schedule_pipelined
+    host = json.loads((golden_dir / "host_logic.json").read_text())["schedule_qcfuse"]
+    sch = policy_schedule("QCFuse", 51, 256, 16, ModelConfig(), CostModel())
+    assert sch.ttft == host["ttft"] and sch.compute_end == host["compute_end"]
+    assert schedule_pipelined([2, 2, 2], [3, 3, 3]).ttft == 11
+
+
+def test_model_config_mirrors_reference():
+    from paper_2604_08585_b200.model import ModelConfig, byte_tokens, tokenize
+    assert ModelConfig().critical_layer == 2
+    for bad in (dict(n_layers=3), dict(d_model=30), dict(critical_layer=1), dict(critical_layer=4),
+                dict(vocab_size=300)):
+        with pytest.raises(ValueError):
+            ModelConfig(**bad)
+    assert tokenize("Hi") == [256, 72, 105] and byte_tokens("Hi") == [72, 105]
+
+
+def test_shard_blocks_cover_everything():
+    from paper_2604_08585_b200.dist import shard
+    for n in (0, 1, 7, 64, 65):
+        for w in (1, 2, 3, 8):
+            got = [i for r in range(w) for i in shard(n, w, r)]
+            assert got == list(range(n))
+            sizes = [len(shard(n, w, r)) for r in range(w)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _gather_worker(rank, world, port, n_total, q):
+    import os
+    import torch.distributed as dist
+    from paper_2604_08585_b200.dist import gather_rows, max_over_ranks, shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = shard(n_total, world, rank)
+    local = torch.stack([torch.full((3,), float(i)) for i in mine]) if len(mine) else torch.zeros(0, 3)
+    full = gather_rows(local, n_total, world, rank)
+    t = max_over_ranks(float(rank + 1), "cpu")
+    if rank == 0:
+        q.put((full[:, 0].tolist(), t))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total", [5, 8])
+def test_gather_two_ranks_gloo(n_total):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, n_total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    rows, t = q.get()
+    assert rows == [float(i) for i in range(n_total)]
+    assert t == 2.0
