@@ -95,5 +95,46 @@ def check(status: int, what: str = "") -> None:
     raise QCFError(text)
 
 
+# kernels launched per successful call (for the bench's gpu_launches claim)
+KERNELS_PER_CALL = {"qcf_score": 3}
+_NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
+               "qcf_topn_workspace"}
+launch_count = 0
+
+
+class Profiler:
+    """Records a CUDA event pair around every C-ABI launch (eager, current
+    stream). Used by bench.py's instrumented pass; never active in graphs."""
+
+    def __init__(self):
+        import torch
+        self._torch = torch
+        self.records: list[tuple[str, tuple, object, object]] = []
+
+    def wrap(self, name, args, fn):
+        ev0 = self._torch.cuda.Event(enable_timing=True)
+        ev1 = self._torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        st = fn()
+        ev1.record()
+        self.records.append((name, args, ev0, ev1))
+        return st
+
+    def summary(self) -> list[tuple[str, tuple, float]]:
+        self._torch.cuda.synchronize()
+        return [(n, a, e0.elapsed_time(e1)) for n, a, e0, e1 in self.records]
+
+
+profiler: Profiler | None = None
+
+
 def call(name: str, *args) -> None:
-    check(getattr(lib, name)(*args), name)
+    global launch_count
+    fn = getattr(lib, name)
+    if profiler is not None and name not in _NON_KERNEL:
+        st = profiler.wrap(name, args, lambda: fn(*args))
+    else:
+        st = fn(*args)
+    check(st, name)
+    if name not in _NON_KERNEL:
+        launch_count += KERNELS_PER_CALL.get(name, 1)

@@ -1,9 +1,6 @@
-// Placeholder tensor-core entry points (replaced by gemm_tc.cu / attention_tc.cu).
+// Placeholder for the tensor-core attention entry point (see attention_tc.cu when built).
 #include "attention.cuh"
-#include "gemm.cuh"
 namespace qcf {
-int gemm_tc_launch(const void*, int64_t, const void*, int64_t, void*, int64_t, int64_t, int64_t,
-                   int64_t, int, int, cudaStream_t) { return QCF_EUNSUPPORTED; }
 int attention_tc_launch(const void*, const void*, const void*, const int32_t*, int64_t, int, int,
                         int, int64_t, void*, cudaStream_t) { return QCF_EUNSUPPORTED; }
 }
