@@ -1,0 +1,295 @@
+// Location-aware attention on the 5th-gen tensor cores (fusion.py:194-208 /
+// model.py:326-338 with the "key position <= row position" mask of
+// fusion.py:467): row i of a 128-row query tile sees table rows 0..kmax[i].
+//
+// One CTA = (128 query rows, one head). Warp roles:
+//   warp 0      TMA producer: Q tile once, then K/V tiles of 128 keys (2-stage ring)
+//   warp 1      MMA issuer:   S_j = Q.K_j^T into a double-buffered TMEM S, then
+//                             O += P_{j-1}.V_{j-1} (V read MN-major straight from
+//                             the token-major table: no transpose pass)
+//   warps 2..5  softmax:      one thread per query row; S row via tcgen05.ld,
+//                             per-row mask, exp2 with a lazily-updated reference
+//                             max (O in TMEM is rescaled only when the running
+//                             max grows by > 2^8), P -> SW128 smem, final O / l.
+// Query rows arrive sorted by position (selection is ascending), so a tile's
+// key range is [0, max kmax] and only its tail tiles are partially masked.
+#include <cuda.h>
+
+#include "attention.cuh"
+#include "sm100.cuh"
+
+namespace qcf {
+
+using namespace sm100;
+
+int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int box_rows);
+
+constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
+constexpr int AT_THREADS = 192;
+constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
+constexpr int AT_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q, K[2], V[2], P
+
+// MN-major SW128 descriptor (B = V: N = head dim contiguous, K = keys):
+// 8-key groups 1024 B apart (SBO), 64-column atoms 16 KB apart (LBO).
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(const void* smem_tile) {
+  const uint32_t a = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)(16384 >> 4) << 16;  // LBO: next 64-wide MN atom
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO: next 8-row K group
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+               const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
+               int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + AT_TILE_BYTES;          // [2]
+  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [2]
+  uint8_t* sP = smem + 5 * AT_TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * AT_TILE_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;    // [2]
+  uint64_t* kv_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* s_free = bars + 7;     // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  __shared__ int s_kend;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int qt = n_qt - 1 - blockIdx.x;  // longest tiles first
+  const int head = blockIdx.y;
+  const int kvh = head / (H / Hkv);
+  const int m0 = qt * AT_BM;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+    // key range of this tile: rows are sorted, but take the max to be safe
+    int mx = 0;
+    for (int i = m0; i < min(M, m0 + AT_BM); ++i) mx = max(mx, kmax[i]);
+    s_kend = min(mx + 1, n_keys);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      mbar_expect_tx(q_full, AT_TILE_BYTES);
+      tma_load_2d(sQ, &map_q, q_full, head * AT_D, m0);
+      tma_load_2d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * AT_TILE_BYTES);
+        uint8_t* k = sK + st * AT_TILE_BYTES;
+        uint8_t* v = sV + st * AT_TILE_BYTES;
+        tma_load_2d(k, &map_k, &kv_full[st], kvh * AT_D, j * AT_BN);
+        tma_load_2d(k + AT_TILE_BYTES / 2, &map_k, &kv_full[st], kvh * AT_D + 64, j * AT_BN);
+        tma_load_2d(v, &map_v, &kv_full[st], kvh * AT_D, j * AT_BN);
+        tma_load_2d(v + AT_TILE_BYTES / 2, &map_v, &kv_full[st], kvh * AT_D + 64, j * AT_BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A, K-major B
+      constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_pv = [&](int jj) {
+        const int st = jj & 1;
+        mbar_wait(p_full, jj & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk) {
+          const uint64_t a = umma_desc_k_sw128(sP + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+          const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
+          mma_bf16(tO, a, b, idesc_o, (jj | kk) != 0);
+        }
+        mma_commit(&kv_empty[st]);
+        mma_commit(pv_done);
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1, sb = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&s_free[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk) {
+          const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+          const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
+                             (uint64_t)((kk & 3) * 2);
+          mma_bf16(tS[sb], a, b, idesc_s, kk != 0);
+        }
+        mma_commit(&s_full[sb]);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_tiles - 1);
+    }
+  } else {  // ---------------- softmax / correction / epilogue (warps 2..5)
+    const int g = warp & 3;
+    const int r = g * 32 + lane;          // row within the tile == TMEM lane
+    const int row = m0 + r;
+    const int my_kmax = row < M ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      const int key0 = j * AT_BN;
+      // pass 1: masked tile max
+      float tmax = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < AT_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS[sb] + c * 32 + lane_off, v);
+        tmem_ld_wait();
+        const int lim = my_kmax - key0 - c * 32;  // columns <= lim are visible
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i <= lim) tmax = fmaxf(tmax, __uint_as_float(v[i]));
+      }
+      tmax *= scale_log2;
+      // the previous P.V must be done before P is overwritten or O rescaled
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_ref == -INFINITY) ? 0.f : exp2f(m_ref - tmax);
+        m_ref = tmax;
+        l *= alpha;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's O rows in TMEM
+#pragma unroll 1
+        for (int c = 0; c < AT_D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tO + c * 32 + lane_off, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+              "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tO + c * 32 + lane_off),
+              "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+              "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+              "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+              "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      // pass 2: P = exp2(s*scale - m_ref) -> bf16 into the SW128 K-major P tile
+      float psum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < AT_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS[sb] + c * 32 + lane_off, v);
+        tmem_ld_wait();
+        const int lim = my_kmax - key0 - c * 32;
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = (i <= lim) ? exp2f(__uint_as_float(v[i]) * scale_log2 - m_ref) : 0.f;
+          float p1 = (i + 1 <= lim) ? exp2f(__uint_as_float(v[i + 1]) * scale_log2 - m_ref) : 0.f;
+          psum += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        // columns c*32..c*32+31 = atom (c>>1), 16-byte chunks 4*(c&1)..+3
+        uint8_t* atom = sP + (c >> 1) * (AT_TILE_BYTES / 2) + r * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = ((c & 1) * 4 + q) ^ (r & 7);
+          *reinterpret_cast<uint4*>(atom + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      l += psum;
+      tc_fence_before();
+      mbar_arrive(&s_free[sb]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+      mbar_arrive(p_full);
+    }
+    // epilogue: O / l
+    mbar_wait(pv_done, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < AT_D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tO + c * 32 + lane_off, v);
+      tmem_ld_wait();
+      if (row < M) {
+        __nv_bfloat16* o = out + ((int64_t)row * H + head) * AT_D + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk;
+          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            p2[u] = __floats2bfloat162_rn(__uint_as_float(v[i + 2 * u]) * inv, __uint_as_float(v[i + 2 * u + 1]) * inv);
+          *reinterpret_cast<uint4*>(o + i) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
+                        int hkv, int d, int64_t n_keys, void* out, cudaStream_t s) {
+  if (d != AT_D || m > INT32_MAX || n_keys > INT32_MAX) return QCF_EUNSUPPORTED;
+  if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) return QCF_EUNSUPPORTED;
+  CUtensorMap mq, mk, mv;
+  int st = make_kmajor_map(&mq, q, m, (int64_t)h * d, (int64_t)h * d, AT_BM);
+  if (st == QCF_OK) st = make_kmajor_map(&mk, k, n_keys, (int64_t)hkv * d, (int64_t)hkv * d, AT_BN);
+  if (st == QCF_OK) st = make_kmajor_map(&mv, v, n_keys, (int64_t)hkv * d, (int64_t)hkv * d, AT_BN);
+  if (st != QCF_OK) return st;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
+    attr = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
+  dim3 grid((unsigned)((m + AT_BM - 1) / AT_BM), (unsigned)h);
+  attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, s>>>(mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
+                                                   (__nv_bfloat16*)out);
+  QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");
+  return QCF_OK;
+}
+
+}  // namespace qcf

@@ -32,20 +32,52 @@ __device__ __forceinline__ void row_stats(const float* __restrict__ xr, int d, i
   rstd_var = warp_sum(v) / d;
 }
 
+// One CTA (128 threads) per row; the row stays in registers between the mean
+// and variance passes (d <= 128 * LN_VPT), block reductions in fp32.
+constexpr int LN_THREADS = 128, LN_VPT = 64;
+
+__device__ __forceinline__ float block_sum_128(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float t = red[0] + red[1] + red[2] + red[3];
+  __syncthreads();
+  return t;
+}
+
 template <typename T>
-__global__ void layernorm_kernel(const float* __restrict__ x, int64_t m, int d,
-                                 const float* __restrict__ g, const float* __restrict__ b,
-                                 float eps, T* __restrict__ out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (row >= m) return;
+__global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __restrict__ x, int64_t m, int d,
+                                                               const float* __restrict__ g,
+                                                               const float* __restrict__ b, float eps,
+                                                               T* __restrict__ out) {
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
   const float* xr = x + row * d;
-  double mean, var;
-  row_stats(xr, d, lane, mean, var);
-  // numpy (model.py:306-308): mean/var are float32, then (x-mean)/sqrt(var+eps)*g+b in f32
-  const float fm = (float)mean, fs = sqrtf((float)var + eps);
+  float v[LN_VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int e = threadIdx.x + i * LN_THREADS;
+    v[i] = e < d ? xr[e] : 0.f;
+    s += v[i];
+  }
+  const float mean = block_sum_128(s, red) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int e = threadIdx.x + i * LN_THREADS;
+    const float t = v[i] - mean;
+    q += e < d ? t * t : 0.f;
+  }
+  const float var = block_sum_128(q, red) / d;
+  const float sd = sqrtf(var + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b  (model.py:308)
   T* orow = out + row * d;
-  for (int e = lane; e < d; e += 32) orow[e] = from_f<T>(((xr[e] - fm) / fs) * g[e] + b[e]);
+#pragma unroll
+  for (int i = 0; i < LN_VPT; ++i) {
+    const int e = threadIdx.x + i * LN_THREADS;
+    if (e < d) orow[e] = from_f<T>(((v[i] - mean) / sd) * g[e] + b[e]);
+  }
 }
 
 // One block per output row: LN_f into shared memory, then one warp per vocab id.
@@ -113,11 +145,14 @@ int qcf_layernorm(const float* x, int64_t m, int d, const float* g, const float*
   QCF_REQUIRE(x && g && b && out && d > 0 && m >= 0, QCF_EINVAL, "qcf_layernorm: bad args");
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
-  unsigned grid = (unsigned)((m + 7) / 8);
+  QCF_REQUIRE(d <= qcf::LN_THREADS * qcf::LN_VPT, QCF_EUNSUPPORTED, "qcf_layernorm: d_model > %d",
+              qcf::LN_THREADS * qcf::LN_VPT);
+  QCF_REQUIRE(m <= 0x7fffffff, QCF_EUNSUPPORTED, "qcf_layernorm: too many rows");
+  unsigned grid = (unsigned)m;
   if (out_dtype == QCF_F32)
-    qcf::layernorm_kernel<float><<<grid, 256, 0, s>>>(x, m, d, g, b, eps, (float*)out);
+    qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
   else if (out_dtype == QCF_BF16)
-    qcf::layernorm_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
+    qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
   else
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_layernorm: bad dtype");
   QCF_LAUNCH_CHECK("qcf_layernorm");

@@ -243,3 +243,23 @@ def test_rope_scatter_exact_rotation(L):
     assert np.array_equal(qo.cpu().numpy(), ref_q)
     ref_k = O.rope(qkv[:, H * D:2 * H * D].reshape(m, H, D), pos, 10000.0)
     assert np.array_equal(kt.cpu().numpy()[:7], ref_k[:7])
+
+
+@pytest.mark.parametrize("m,n,H,growth", [(800, 5153, 4, 0.0), (300, 2000, 2, 6.0), (33, 700, 3, 20.0)])
+def test_attention_tensor_core_long_and_rescale(L, m, n, H, growth):
+    """tcgen05 attention over many 128-key tiles; `growth` makes later keys
+    dominate so the lazily-updated softmax max must rescale O in TMEM."""
+    torch.manual_seed(n)
+    D = 128
+    q = torch.randn(m, H, D, device="cuda")
+    k = torch.randn(n, H, D, device="cuda")
+    if growth:
+        k = k * (1 + growth * torch.linspace(0, 1, n, device="cuda"))[:, None, None] / 4
+    v = torch.randn(n, H, D, device="cuda")
+    q, k, v = q.bfloat16(), k.bfloat16(), v.bfloat16()
+    pos = torch.sort(torch.randperm(n - 1, device="cuda")[:m] + 1).values.int()
+    out = torch.empty_like(q)
+    L.call("qcf_attention", L.QCF_BF16, p(q), p(k), p(v), p(pos), m, H, H, D, n, p(out), S())
+    ref = torch_attention(q, k, v, pos.long())
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2 * max(1.0, ref.abs().max().item()), err
