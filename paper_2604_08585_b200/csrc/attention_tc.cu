@@ -84,10 +84,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     mbar_init(p_full, 128);
     mbar_init(pv_done, 1);
     fence_barrier_init();
-    // key range of this tile: rows are sorted, but take the max to be safe
-    int mx = 0;
-    for (int i = m0; i < min(M, m0 + AT_BM); ++i) mx = max(mx, kmax[i]);
-    s_kend = min(mx + 1, n_keys);
+    s_kend = 0;
+  }
+  __syncthreads();
+  // key range of this tile = 1 + max kmax over its rows (parallel max; rows are
+  // normally sorted but the kernel does not rely on it)
+  if (threadIdx.x < AT_BM) {
+    int v = (m0 + (int)threadIdx.x < M) ? kmax[m0 + threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();

@@ -1,8 +1,8 @@
 // Row-wise ops of the decoder layer: embedding gather (fusion.py:464,
 // model.py:350), LayerNorm (model.py:305-308), the tied lm-head on the last
 // query row (model.py:384-385 / fusion.py:540), and chunk key norms
-// (store.py:339-340). One warp per row; statistics accumulate in float64 so the
-// float32 residual stream matches numpy's pairwise float32 sums to ~1 ulp.
+// (store.py:339-340). LayerNorm keeps a row in registers (one CTA per row) and
+// reduces in fp32; key norms accumulate in float64.
 #include "common.cuh"
 
 namespace qcf {
@@ -32,18 +32,34 @@ __device__ __forceinline__ void row_stats(const float* __restrict__ xr, int d, i
   rstd_var = warp_sum(v) / d;
 }
 
-// One CTA (128 threads) per row; the row stays in registers between the mean
-// and variance passes (d <= 128 * LN_VPT), block reductions in fp32.
-constexpr int LN_THREADS = 128, LN_VPT = 64;
+// One CTA (256 threads) per row. All loads (x, gain, bias) are issued up front
+// as float4 into registers, so the kernel pays ~2 memory round trips; fp32
+// block reductions for mean and (x-mean)^2.
+constexpr int LN_THREADS = 256, LN_V4 = 8;  // d <= 256 * 4 * 8 = 8192
 
-__device__ __forceinline__ float block_sum_128(float v, float* red) {
+__device__ __forceinline__ float block_sum_256(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
-  float t = red[0] + red[1] + red[2] + red[3];
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_THREADS / 32; ++i) t += red[i];
   __syncthreads();
   return t;
+}
+
+template <typename T>
+__device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  *reinterpret_cast<uint2*>(p) = u;
 }
 
 template <typename T>
@@ -51,57 +67,113 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
                                                                const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps,
                                                                T* __restrict__ out) {
-  __shared__ float red[4];
+  __shared__ float red[LN_THREADS / 32];
   const int64_t row = blockIdx.x;
-  const float* xr = x + row * d;
-  float v[LN_VPT];
+  const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  const int n4 = d >> 2;
+  float4 v[LN_V4], gv[LN_V4], bv[LN_V4];
+#pragma unroll
+  for (int i = 0; i < LN_V4; ++i) {
+    const int e = threadIdx.x + i * LN_THREADS;
+    const bool ok = e < n4;
+    v[i] = ok ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[i] = ok ? g4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    bv[i] = ok ? b4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int e = threadIdx.x + i * LN_THREADS;
-    v[i] = e < d ? xr[e] : 0.f;
-    s += v[i];
-  }
-  const float mean = block_sum_128(s, red) / d;
+  for (int i = 0; i < LN_V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mean = block_sum_256(s, red) / d;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
-    const int e = threadIdx.x + i * LN_THREADS;
-    const float t = v[i] - mean;
-    q += e < d ? t * t : 0.f;
+  for (int i = 0; i < LN_V4; ++i) {
+    if (threadIdx.x + i * LN_THREADS < n4) {
+      const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
+      q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+    }
   }
-  const float var = block_sum_128(q, red) / d;
+  const float var = block_sum_256(q, red) / d;
   const float sd = sqrtf(var + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b  (model.py:308)
   T* orow = out + row * d;
 #pragma unroll
-  for (int i = 0; i < LN_VPT; ++i) {
+  for (int i = 0; i < LN_V4; ++i) {
     const int e = threadIdx.x + i * LN_THREADS;
-    if (e < d) orow[e] = from_f<T>(((v[i] - mean) / sd) * g[e] + b[e]);
+    if (e < n4)
+      store4<T>(orow + 4 * e, ((v[i].x - mean) / sd) * gv[i].x + bv[i].x, ((v[i].y - mean) / sd) * gv[i].y + bv[i].y,
+                ((v[i].z - mean) / sd) * gv[i].z + bv[i].z, ((v[i].w - mean) / sd) * gv[i].w + bv[i].w);
   }
 }
 
-// One block per output row: LN_f into shared memory, then one warp per vocab id.
-__global__ void lm_head_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, int d,
-                               const float* __restrict__ g, const float* __restrict__ b, float eps,
-                               const float* __restrict__ emb, int vocab, float* __restrict__ logits) {
+// generic fallback (d % 4 != 0): one CTA per row, strided scalar loop
+template <typename T>
+__global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(const float* __restrict__ x, int64_t m, int d,
+                                                                      const float* __restrict__ g,
+                                                                      const float* __restrict__ b, float eps,
+                                                                      T* __restrict__ out) {
+  __shared__ float red[LN_THREADS / 32];
+  const float* xr = x + (int64_t)blockIdx.x * d;
+  float s = 0.f;
+  for (int e = threadIdx.x; e < d; e += LN_THREADS) s += xr[e];
+  const float mean = block_sum_256(s, red) / d;
+  float q = 0.f;
+  for (int e = threadIdx.x; e < d; e += LN_THREADS) { const float t = xr[e] - mean; q += t * t; }
+  const float sd = sqrtf(block_sum_256(q, red) / d + eps);
+  T* orow = out + (int64_t)blockIdx.x * d;
+  for (int e = threadIdx.x; e < d; e += LN_THREADS) orow[e] = from_f<T>(((xr[e] - mean) / sd) * g[e] + b[e]);
+}
+
+// lm-head: grid (vocab tiles of 32, rows). Every CTA recomputes LN_f of its
+// row into shared memory (d floats), then each of 8 warps dots 4 vocab rows.
+constexpr int LM_THREADS = 256, LM_VT = 32;
+
+__global__ void __launch_bounds__(LM_THREADS) lm_head_kernel(const float* __restrict__ x,
+                                                             const int32_t* __restrict__ rows, int d,
+                                                             const float* __restrict__ g,
+                                                             const float* __restrict__ b, float eps,
+                                                             const float* __restrict__ emb, int vocab,
+                                                             float* __restrict__ logits) {
   extern __shared__ float xs[];
-  __shared__ float stat[2];
-  const int r = blockIdx.x;
+  __shared__ float red[8];
+  const int r = blockIdx.y;
   const float* xr = x + (int64_t)(rows ? rows[r] : r) * d;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (warp == 0) {
-    double mean, var;
-    row_stats(xr, d, lane, mean, var);
-    if (lane == 0) { stat[0] = (float)mean; stat[1] = sqrtf((float)var + eps); }
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float s = 0.f;
+  for (int e = threadIdx.x; e < d; e += LM_THREADS) { const float v = xr[e]; xs[e] = v; s += v; }
+  s = warp_sum(s);
+  if (lane == 0) red[warp] = s;
   __syncthreads();
-  for (int e = threadIdx.x; e < d; e += blockDim.x) xs[e] = ((xr[e] - stat[0]) / stat[1]) * g[e] + b[e];
+  float mean = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mean += red[w];
+  mean /= d;
   __syncthreads();
-  for (int v = warp; v < vocab; v += nw) {
+  float q = 0.f;
+  for (int e = threadIdx.x; e < d; e += LM_THREADS) { const float t = xs[e] - mean; q += t * t; }
+  q = warp_sum(q);
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  float var = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) var += red[w];
+  const float sd = sqrtf(var / d + eps);
+  for (int e = threadIdx.x; e < d; e += LM_THREADS) xs[e] = ((xs[e] - mean) / sd) * g[e] + b[e];
+  __syncthreads();
+  for (int vv = warp; vv < LM_VT; vv += 8) {
+    const int v = blockIdx.x * LM_VT + vv;
+    if (v >= vocab) break;
     const float* er = emb + (int64_t)v * d;
-    float acc = 0.f;
-    for (int e = lane; e < d; e += 32) acc = fmaf(xs[e], er[e], acc);
-    acc = warp_sum(acc);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int e = lane;
+    for (; e + 96 < d; e += 128) {
+      a0 = fmaf(xs[e], er[e], a0);
+      a1 = fmaf(xs[e + 32], er[e + 32], a1);
+      a2 = fmaf(xs[e + 64], er[e + 64], a2);
+      a3 = fmaf(xs[e + 96], er[e + 96], a3);
+    }
+    for (; e < d; e += 32) a0 = fmaf(xs[e], er[e], a0);
+    const float acc = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
   }
 }
@@ -145,16 +217,20 @@ int qcf_layernorm(const float* x, int64_t m, int d, const float* g, const float*
   QCF_REQUIRE(x && g && b && out && d > 0 && m >= 0, QCF_EINVAL, "qcf_layernorm: bad args");
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
-  QCF_REQUIRE(d <= qcf::LN_THREADS * qcf::LN_VPT, QCF_EUNSUPPORTED, "qcf_layernorm: d_model > %d",
-              qcf::LN_THREADS * qcf::LN_VPT);
   QCF_REQUIRE(m <= 0x7fffffff, QCF_EUNSUPPORTED, "qcf_layernorm: too many rows");
-  unsigned grid = (unsigned)m;
-  if (out_dtype == QCF_F32)
-    qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
-  else if (out_dtype == QCF_BF16)
-    qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
-  else
+  const unsigned grid = (unsigned)m;
+  const bool vec = (d % 4 == 0) && d <= qcf::LN_THREADS * 4 * qcf::LN_V4 &&
+                   !(((uintptr_t)x | (uintptr_t)g | (uintptr_t)b | (uintptr_t)out) & 15) &&
+                   (out_dtype == QCF_F32 || d % 8 == 0);
+  if (out_dtype == QCF_F32) {
+    if (vec) qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
+    else qcf::layernorm_scalar_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
+  } else if (out_dtype == QCF_BF16) {
+    if (vec) qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
+    else qcf::layernorm_scalar_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
+  } else {
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_layernorm: bad dtype");
+  }
   QCF_LAUNCH_CHECK("qcf_layernorm");
   return QCF_OK;
 }
@@ -170,7 +246,8 @@ int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d, cons
     cudaError_t e = cudaFuncSetAttribute(qcf::lm_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return qcf::cuda_status(e, "qcf_lm_head attr");
   }
-  qcf::lm_head_kernel<<<(unsigned)n_rows, 512, smem, qcf::as_stream(stream)>>>(x, rows, d, g, b, eps, emb, vocab, logits);
+  dim3 grid((unsigned)((vocab + qcf::LM_VT - 1) / qcf::LM_VT), (unsigned)n_rows);
+  qcf::lm_head_kernel<<<grid, qcf::LM_THREADS, smem, qcf::as_stream(stream)>>>(x, rows, d, g, b, eps, emb, vocab, logits);
   QCF_LAUNCH_CHECK("qcf_lm_head");
   return QCF_OK;
 }

@@ -75,15 +75,28 @@ __global__ void score_rowstats_kernel(const Acc* __restrict__ S, int64_t n_ctx, 
   }
 }
 
+// column mean: CTA = 32 columns (lanes) x 8 warps splitting the (h,t) rows
 template <typename Acc>
-__global__ void score_colmean_kernel(const Acc* __restrict__ S, int64_t n_ctx, int rows,
-                                     const Acc* __restrict__ rmax, const Acc* __restrict__ rsum,
-                                     float* __restrict__ scores) {
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (n >= n_ctx) return;
+__global__ void __launch_bounds__(256) score_colmean_kernel(const Acc* __restrict__ S, int64_t n_ctx, int rows,
+                                                            const Acc* __restrict__ rmax,
+                                                            const Acc* __restrict__ rsum,
+                                                            float* __restrict__ scores) {
+  __shared__ Acc part[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = (int64_t)blockIdx.x * 32 + lane;
   Acc acc = 0;
-  for (int r = 0; r < rows; ++r) acc += exp(S[(int64_t)r * n_ctx + n] - rmax[r]) / rsum[r];
-  scores[n] = (float)(acc / (Acc)rows);
+  if (n < n_ctx) {
+#pragma unroll 4
+    for (int r = warp; r < rows; r += 8) acc += exp(S[(int64_t)r * n_ctx + n] - rmax[r]) / rsum[r];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && n < n_ctx) {
+    Acc t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    scores[n] = (float)(t / (Acc)rows);
+  }
 }
 
 template <typename T, typename Acc>
@@ -108,7 +121,7 @@ static int score_impl(const void* q, const void* k, int64_t n_ctx, int nq, int h
   QCF_LAUNCH_CHECK("qcf_score logits");
   score_rowstats_kernel<Acc><<<rows, 256, 0, s>>>(S, n_ctx, rmax, rsum);
   QCF_LAUNCH_CHECK("qcf_score rowstats");
-  score_colmean_kernel<Acc><<<ceil_div(n_ctx, 256), 256, 0, s>>>(S, n_ctx, rows, rmax, rsum, scores);
+  score_colmean_kernel<Acc><<<ceil_div(n_ctx, 32), 256, 0, s>>>(S, n_ctx, rows, rmax, rsum, scores);
   QCF_LAUNCH_CHECK("qcf_score colmean");
   return QCF_OK;
 }
