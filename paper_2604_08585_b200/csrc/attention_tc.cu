@@ -7,10 +7,12 @@
 //   warp 1      MMA issuer:   S_j = Q.K_j^T into a double-buffered TMEM S, then
 //                             O += P_{j-1}.V_{j-1} (V read MN-major straight from
 //                             the token-major table: no transpose pass)
-//   warps 2..5  softmax:      one thread per query row; S row via tcgen05.ld,
-//                             per-row mask, exp2 with a lazily-updated reference
-//                             max (O in TMEM is rescaled only when the running
-//                             max grows by > 2^8), P -> SW128 smem, final O / l.
+//   warps 2..17 softmax:      16 warps = 4 TMEM lane quarters (rows) x 4 column
+//                             groups of 32 keys; each thread owns 32 scores of one
+//                             row (one tcgen05.ld), row max combined through smem,
+//                             ex2 with a lazily-updated reference max (O in TMEM is
+//                             rescaled only when the running max grows by > 2^8),
+//                             P -> SW128 smem, final O / l per 32-column slice.
 // Query rows arrive sorted by position (selection is ascending), so a tile's
 // key range is [0, max kmax] and only its tail tiles are partially masked.
 #include <cuda.h>
@@ -25,7 +27,7 @@ using namespace sm100;
 int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int box_rows);
 
 constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
-constexpr int AT_THREADS = 192;
+constexpr int AT_THREADS = 576;  // 2 control warps + 16 softmax warps
 constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
 constexpr int AT_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q, K[2], V[2], P
 
@@ -40,6 +42,16 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(const void* smem_tile) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
@@ -61,6 +73,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   uint64_t* p_full = bars + 9;
   uint64_t* pv_done = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
   __shared__ int s_kend;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -69,6 +82,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   const int head = blockIdx.y;
   const int kvh = head / (H / Hkv);
   const int m0 = qt * AT_BM;
+  constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&map_q);
@@ -79,16 +93,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 128);
+      mbar_init(&s_free[s], N_SOFT);
     }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, N_SOFT);
     mbar_init(pv_done, 1);
     fence_barrier_init();
     s_kend = 0;
   }
   __syncthreads();
-  // key range of this tile = 1 + max kmax over its rows (parallel max; rows are
-  // normally sorted but the kernel does not rely on it)
+  // key range of this tile = 1 + max kmax over its rows (rows are normally
+  // sorted by position, but the kernel does not rely on it)
   if (threadIdx.x < AT_BM) {
     int v = (m0 + (int)threadIdx.x < M) ? kmax[m0 + threadIdx.x] : 0;
 #pragma unroll
@@ -101,8 +115,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
+  const uint32_t tS0 = tmem, tO = tmem + 256;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -150,38 +163,43 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
           const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
                              (uint64_t)((kk & 3) * 2);
-          mma_bf16(tS[sb], a, b, idesc_s, kk != 0);
+          mma_bf16(tS0 + sb * 128, a, b, idesc_s, kk != 0);
         }
         mma_commit(&s_full[sb]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_tiles - 1);
     }
-  } else {  // ---------------- softmax / correction / epilogue (warps 2..5)
-    const int g = warp & 3;
+  } else {  // ---------------- softmax / correction / epilogue (warps 2..17)
+    const int g = warp & 3;               // TMEM lane quarter -> rows 32g..32g+31
+    const int cg = (warp - 2) >> 2;       // column group: S keys / O dims 32cg..32cg+31
     const int r = g * 32 + lane;          // row within the tile == TMEM lane
     const int row = m0 + r;
     const int my_kmax = row < M ? kmax[row] : -1;
     const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const int bar_id = 1 + g;             // named barrier of the 4 warps sharing these rows
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      const int key0 = j * AT_BN;
-      // pass 1: masked tile max
-      float tmax = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < AT_BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS[sb] + c * 32 + lane_off, v);
-        tmem_ld_wait();
-        const int lim = my_kmax - key0 - c * 32;  // columns <= lim are visible
+      uint32_t v[32];
+      tmem_ld32(tS0 + sb * 128 + cg * 32 + lane_off, v);
+      tmem_ld_wait();
+      const int lim = my_kmax - j * AT_BN - cg * 32;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= 31);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      float pmax = -INFINITY;
+      if (all_vis) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i <= lim) tmax = fmaxf(tmax, __uint_as_float(v[i]));
+        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, __uint_as_float(v[i]));
+      } else if (!none_vis) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
       }
-      tmax *= scale_log2;
+      red[sb][cg][r] = pmax * scale_log2;
+      named_bar(bar_id, 128);
+      const float tmax = fmaxf(fmaxf(red[sb][0][r], red[sb][1][r]), fmaxf(red[sb][2][r], red[sb][3][r]));
       // the previous P.V must be done before P is overwritten or O rescaled
       if (j > 0) {
         mbar_wait(pv_done, (j - 1) & 1);
@@ -190,80 +208,79 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
       float alpha = 1.f;
       if (need) {
-        alpha = (m_ref == -INFINITY) ? 0.f : exp2f(m_ref - tmax);
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
         m_ref = tmax;
         l *= alpha;
       }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's O rows in TMEM
-#pragma unroll 1
-        for (int c = 0; c < AT_D / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld32(tO + c * 32 + lane_off, v);
-          tmem_ld_wait();
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's O slice in TMEM
+        uint32_t o[32];
+        tmem_ld32(tO + cg * 32 + lane_off, o);
+        tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-              "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tO + c * 32 + lane_off),
-              "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-              "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
-              "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
-              "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
-        }
+        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tO + cg * 32 + lane_off),
+            "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+            "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
+            "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
+            "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
-      // pass 2: P = exp2(s*scale - m_ref) -> bf16 into the SW128 K-major P tile
+      // P = exp2(s*scale - m_ref) -> bf16, columns 32cg..32cg+31 of the SW128 K-major P tile
+      uint32_t pk[16];
       float psum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < AT_BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS[sb] + c * 32 + lane_off, v);
-        tmem_ld_wait();
-        const int lim = my_kmax - key0 - c * 32;
-        uint32_t pk[16];
+      if (none_vis) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = 0u;
+      } else {
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float p0 = (i <= lim) ? exp2f(__uint_as_float(v[i]) * scale_log2 - m_ref) : 0.f;
-          float p1 = (i + 1 <= lim) ? exp2f(__uint_as_float(v[i + 1]) * scale_log2 - m_ref) : 0.f;
+          float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
+          float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
+          if (!all_vis) {
+            p0 = (i <= lim) ? p0 : 0.f;
+            p1 = (i + 1 <= lim) ? p1 : 0.f;
+          }
           psum += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        // columns c*32..c*32+31 = atom (c>>1), 16-byte chunks 4*(c&1)..+3
-        uint8_t* atom = sP + (c >> 1) * (AT_TILE_BYTES / 2) + r * 128;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = ((c & 1) * 4 + q) ^ (r & 7);
-          *reinterpret_cast<uint4*>(atom + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
       }
       l += psum;
+      uint8_t* atom = sP + (cg >> 1) * (AT_TILE_BYTES / 2) + r * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int chunk = ((cg & 1) * 4 + q) ^ (r & 7);
+        *reinterpret_cast<uint4*>(atom + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
       tc_fence_before();
       mbar_arrive(&s_free[sb]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       mbar_arrive(p_full);
     }
-    // epilogue: O / l
+    // epilogue: combine the 4 partial row sums, then O / l for this warp's 32 columns
+    named_bar(bar_id, 128);
+    red[0][cg][r] = l;
+    named_bar(bar_id, 128);
+    const float lt = (red[0][0][r] + red[0][1][r]) + (red[0][2][r] + red[0][3][r]);
     mbar_wait(pv_done, (n_tiles - 1) & 1);
     tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < AT_D / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tO + c * 32 + lane_off, v);
-      tmem_ld_wait();
-      if (row < M) {
-        __nv_bfloat16* o = out + ((int64_t)row * H + head) * AT_D + c * 32;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    uint32_t o[32];
+    tmem_ld32(tO + cg * 32 + lane_off, o);
+    tmem_ld_wait();
+    if (row < M) {
+      __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cg * 32;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 pk;
-          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk4;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            p2[u] = __floats2bfloat162_rn(__uint_as_float(v[i + 2 * u]) * inv, __uint_as_float(v[i + 2 * u + 1]) * inv);
-          *reinterpret_cast<uint4*>(o + i) = pk;
-        }
+        for (int u = 0; u < 4; ++u)
+          p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv, __uint_as_float(o[i + 2 * u + 1]) * inv);
+        *reinterpret_cast<uint4*>(dst + i) = pk4;
       }
     }
   }
