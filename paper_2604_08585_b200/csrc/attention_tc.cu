@@ -66,20 +66,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   uint8_t* sP = smem + 5 * AT_TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * AT_TILE_BYTES);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;    // [2]
-  uint64_t* kv_empty = bars + 3;   // [2]
+  uint64_t* k_full = bars + 1;     // [2]  K ring: freed as soon as S_j is computed
+  uint64_t* k_empty = bars + 3;    // [2]
   uint64_t* s_full = bars + 5;     // [2]
   uint64_t* s_free = bars + 7;     // [2]
   uint64_t* p_full = bars + 9;
   uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* v_full = bars + 11;    // [2]  V ring: freed when P_j.V_j is done
+  uint64_t* v_empty = bars + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
   __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
   __shared__ int s_kend;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (M + AT_BM - 1) / AT_BM;
-  const int qt = n_qt - 1 - blockIdx.x;  // longest tiles first
-  const int head = blockIdx.y;
+  const int qt = n_qt - 1 - blockIdx.y;  // longest tiles (largest positions) launch first
+  const int head = blockIdx.x;
   const int kvh = head / (H / Hkv);
   const int m0 = qt * AT_BM;
   constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
@@ -90,8 +92,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     tma_prefetch_desc(&map_v);
     mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&s_free[s], N_SOFT);
     }
@@ -122,16 +126,28 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       mbar_expect_tx(q_full, AT_TILE_BYTES);
       tma_load_2d(sQ, &map_q, q_full, head * AT_D, m0);
       tma_load_2d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0);
-      for (int j = 0; j < n_tiles; ++j) {
+      // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
+      // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
+      auto load_k = [&](int j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * AT_TILE_BYTES);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
         uint8_t* k = sK + st * AT_TILE_BYTES;
+        tma_load_2d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN);
+        tma_load_2d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN);
+      };
+      auto load_v = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
         uint8_t* v = sV + st * AT_TILE_BYTES;
-        tma_load_2d(k, &map_k, &kv_full[st], kvh * AT_D, j * AT_BN);
-        tma_load_2d(k + AT_TILE_BYTES / 2, &map_k, &kv_full[st], kvh * AT_D + 64, j * AT_BN);
-        tma_load_2d(v, &map_v, &kv_full[st], kvh * AT_D, j * AT_BN);
-        tma_load_2d(v + AT_TILE_BYTES / 2, &map_v, &kv_full[st], kvh * AT_D + 64, j * AT_BN);
+        tma_load_2d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN);
+        tma_load_2d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN);
+      };
+      load_k(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) load_k(j + 1);
+        load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -143,6 +159,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       auto issue_pv = [&](int jj) {
         const int st = jj & 1;
         mbar_wait(p_full, jj & 1);
+        mbar_wait(&v_full[st], (jj >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
@@ -150,12 +167,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
           mma_bf16(tO, a, b, idesc_o, (jj | kk) != 0);
         }
-        mma_commit(&kv_empty[st]);
+        mma_commit(&v_empty[st]);
         mma_commit(pv_done);
       };
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1, sb = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         mbar_wait(&s_free[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -166,6 +183,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           mma_bf16(tS0 + sb * 128, a, b, idesc_s, kk != 0);
         }
         mma_commit(&s_full[sb]);
+        mma_commit(&k_empty[st]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_tiles - 1);
@@ -249,11 +267,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         }
       }
       l += psum;
-      uint8_t* atom = sP + (cg >> 1) * (AT_TILE_BYTES / 2) + r * 128;
+      const uint32_t atom = smem_u32(sP + (cg >> 1) * (AT_TILE_BYTES / 2) + r * 128);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int chunk = ((cg & 1) * 4 + q) ^ (r & 7);
-        *reinterpret_cast<uint4*>(atom + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(atom + chunk * 16), "r"(pk[4 * q]),
+                     "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3]) : "memory");
       }
       tc_fence_before();
       mbar_arrive(&s_free[sb]);
@@ -308,7 +327,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
-  dim3 grid((unsigned)((m + AT_BM - 1) / AT_BM), (unsigned)h);
+  dim3 grid((unsigned)h, (unsigned)((m + AT_BM - 1) / AT_BM));
   attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, s>>>(mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
                                                    (__nv_bfloat16*)out);
   QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");
