@@ -107,7 +107,8 @@ def test_gemm_vs_torch_fp32(L, m, n, k, dtype, epi):
     assert err < tol, (err, tol)
 
 
-@pytest.mark.parametrize("m,n,k", [(800, 12288, 4096), (129, 4096, 14336), (5, 512, 128)])
+@pytest.mark.parametrize("m,n,k", [(800, 12288, 4096), (129, 4096, 14336), (5, 512, 128), (256, 12288, 256),
+                                   (513, 12288, 128), (1000, 4096, 14336), (600, 12288, 200), (5153, 14336, 256)])
 def test_gemm_tensor_core_matches_simt(L, m, n, k):
     torch.manual_seed(0)
     a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
