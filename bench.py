@@ -292,7 +292,7 @@ def main():
     gemm_shapes: dict[str, list] = {}
     for name, a, ms in recs:
         phases[name] = phases.get(name, 0.0) + ms
-        if name == "qcf_gemm":
+        if name in ("qcf_gemm", "qcf_gemm_ws"):
             m_, n_, k_ = a[7], a[8], a[9]
             gemm_flops += 2.0 * m_ * n_ * k_
             gemm_ms += ms

@@ -108,6 +108,14 @@ int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dt
 int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
              void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
              int out_dtype, qcf_stream_t stream);
+/* Same contract with a caller-owned workspace: skinny M (the probe's q rows)
+ * splits K across CTAs so the weights stream at HBM rate; partials are summed
+ * in a fixed order (deterministic). ws may be NULL when qcf_gemm_workspace()
+ * returns 0. */
+size_t qcf_gemm_workspace(int64_t m, int64_t n, int64_t k);
+int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
+                int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, void* ws, size_t ws_bytes,
+                qcf_stream_t stream);
 /* Same contract, forced onto the SIMT path (cross-check of the tensor-core path). */
 int qcf_gemm_simt(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
                   void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
@@ -121,6 +129,16 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
                          const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
                          void* q_out, void* k_tab, void* v_tab, int dtype,
                          qcf_stream_t stream);
+
+/* Fused QKV projection + RoPE + KV scatter (bf16, tcgen05): the projection
+ * a[M,K] . w[(H+2Hkv)D, K]^T never touches HBM in fp32; its epilogue rotates
+ * Q/K at pos[i] and writes q_out[i], k_tab[dst_rows[i]], v_tab[dst_rows[i]].
+ * Returns QCF_EUNSUPPORTED when d % 32 != 0 or m <= 32 (callers then use
+ * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478. */
+int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k,
+                      int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
+                      const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
+                      void* k_tab, void* v_tab, qcf_stream_t stream);
 
 /* ---- location-aware attention: fusion.py:194-208 -> model.py:326-338 -------
  * out[i,h] = sum_{j<=kmax[i]} softmax_j(q[i,h].k[j,h/(H/Hkv)] / float(sqrt(D))) v[j]

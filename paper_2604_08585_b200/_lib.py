@@ -52,7 +52,10 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_key_norms": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "qcf_gemm": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
     "qcf_gemm_simt": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
+    "qcf_gemm_workspace": (_SZ, [_I64, _I64, _I64]),
+    "qcf_gemm_ws": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P, _SZ, _P]),
     "qcf_rope_qkv_scatter": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _P]),
+    "qcf_gemm_qkv_rope": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
     "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
@@ -98,7 +101,7 @@ def check(status: int, what: str = "") -> None:
 # kernels launched per successful call (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {"qcf_score": 3}
 _NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
-               "qcf_topn_workspace"}
+               "qcf_topn_workspace", "qcf_gemm_workspace"}
 launch_count = 0
 
 

@@ -28,10 +28,65 @@ using namespace sm100;
 constexpr int TC_BM = 128, TC_BK = 64;
 constexpr int TC_THREADS = 192;
 
+constexpr int QCF_EPI_ROPE_QKV = 3;  // internal: RoPE + KV scatter epilogue of the QKV GEMM
+
+struct EpiArgs {
+  int kind, out_dtype;
+  const int32_t* pos;
+  const int32_t* dst;
+  const double* cos_tbl;
+  const double* sin_tbl;
+  void* q_out;
+  void* k_tab;
+  void* v_tab;
+  int h, hkv, d;
+};
 
 // fused epilogue for 32 consecutive columns of one output row
 __device__ __forceinline__ void epilogue_row32(void* __restrict__ C, int64_t ldc, int row, int col0, int N,
-                                               const uint32_t (&r)[32], int epi, int out_dtype) {
+                                               const uint32_t (&r)[32], const EpiArgs& ea) {
+  const int epi = ea.kind, out_dtype = ea.out_dtype;
+  if (epi == QCF_EPI_ROPE_QKV) {
+    // C columns = [Q | K | V] of `h`/`hkv` heads x d; rotate Q and K pairs at
+    // pos[row] (fusion.py:471-475), scatter K/V into table row dst[row] (477-478)
+    const int qd = ea.h * ea.d, kd = ea.hkv * ea.d;
+    int base;
+    __nv_bfloat16* out;
+    bool rot = true;
+    if (col0 < qd) {
+      base = col0;
+      out = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)row * qd + base;
+    } else {
+      const int64_t drow = ea.dst[row];
+      if (col0 < qd + kd) {
+        base = col0 - qd;
+        out = reinterpret_cast<__nv_bfloat16*>(ea.k_tab) + drow * kd + base;
+      } else {
+        base = col0 - qd - kd;
+        out = reinterpret_cast<__nv_bfloat16*>(ea.v_tab) + drow * kd + base;
+        rot = false;
+      }
+    }
+    const int half = ea.d >> 1;
+    const int64_t t0 = (int64_t)ea.pos[row] * half + ((base % ea.d) >> 1);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float e = __uint_as_float(r[2 * i]), o = __uint_as_float(r[2 * i + 1]);
+      if (rot) {
+        const float c = (float)ea.cos_tbl[t0 + i], sn = (float)ea.sin_tbl[t0 + i];
+        const float oe = e * c - o * sn, oo = e * sn + o * c;
+        e = oe;
+        o = oo;
+      }
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(e, o);
+      pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      reinterpret_cast<uint4*>(out)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    return;
+  }
   if (out_dtype == QCF_F32) {
     float* crow = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col0;
     if (col0 + 32 <= N) {
@@ -80,21 +135,30 @@ __device__ __forceinline__ void epilogue_row32(void* __restrict__ C, int64_t ldc
   }
 }
 
-template <int BN>
+// SKINNY (M <= 32): the A slab holds only 32 rows (4 KB) so the ring can be 16
+// deep; the MMA still reads 128 A rows, the extra 96 are stale smem feeding
+// output rows >= M that the epilogue never stores.
+// SKINNY also moves 4 swizzle atoms (K=256) per stage, amortising the per-stage
+// mbarrier round trips of the producer/MMA threads over 4x more weight bytes.
+template <int BN, bool SKINNY = false>
 struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int KATOMS = SKINNY ? 4 : 1;   // 64-element K atoms per stage
+  static constexpr int STAGES = SKINNY ? 4 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  static constexpr int A_ATOM = (SKINNY ? 32 : TC_BM) * TC_BK * 2;
+  static constexpr int B_ATOM = BN * TC_BK * 2;
+  static constexpr int A_BYTES = KATOMS * A_ATOM;
+  static constexpr int B_BYTES = KATOMS * B_ATOM;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN>
+template <int BN, bool SKINNY = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               void* __restrict__ C, int64_t ldc, int M, int N, int K, int epi, int out_dtype) {
-  using Cfg = TcCfg<BN>;
+               void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int splits,
+               int a_box_rows, float* __restrict__ partial) {
+  using Cfg = TcCfg<BN, SKINNY>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -108,8 +172,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (N + BN - 1) / BN;
-  const int n_work = m_tiles * n_tiles;
-  const int k_blocks = (K + TC_BK - 1) / TC_BK;
+  const int n_work = m_tiles * n_tiles * splits;
+  constexpr int KSTAGE = TC_BK * Cfg::KATOMS;                 // K elements per stage
+  const int k_blocks = (K + KSTAGE - 1) / KSTAGE;
+  const int kb_per = (k_blocks + splits - 1) / splits;
+  const uint32_t stage_tx = (uint32_t)Cfg::KATOMS * ((uint32_t)a_box_rows * TC_BK * 2 + Cfg::B_ATOM);
+  // work unit w -> (m tile fastest, then split, then n tile); split sp covers
+  // k blocks [sp*kb_per, min(k_blocks, (sp+1)*kb_per))
+  auto unit = [&](int w, int& mb, int& nb, int& kb0, int& kb1) {
+    mb = w % m_tiles;
+    const int r = w / m_tiles;
+    const int sp = r % splits;
+    nb = r / splits;
+    kb0 = sp * kb_per;
+    kb1 = min(k_blocks, kb0 + kb_per);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -128,14 +205,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     if (lane == 0) {  // ---------------- TMA producer
       uint32_t it = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int mb = w % m_tiles, nb = w / m_tiles;
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        int mb, nb, kb0, kb1;
+        unit(w, mb, nb, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
           const uint32_t ph = (it / Cfg::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + s * Cfg::A_BYTES, &map_a, &full[s], kb * TC_BK, mb * TC_BM);
-          tma_load_2d(sB + s * Cfg::B_BYTES, &map_b, &full[s], kb * TC_BK, nb * BN);
+          mbar_expect_tx(&full[s], stage_tx);
+#pragma unroll
+          for (int j = 0; j < Cfg::KATOMS; ++j) {
+            tma_load_2d(sA + s * Cfg::A_BYTES + j * Cfg::A_ATOM, &map_a, &full[s], kb * KSTAGE + j * TC_BK, mb * TC_BM);
+            tma_load_2d(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM, &map_b, &full[s], kb * KSTAGE + j * TC_BK, nb * BN);
+          }
         }
       }
     }
@@ -144,20 +225,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
       uint32_t it = 0, t = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+        int mb, nb, kb0, kb1;
+        unit(w, mb, nb, kb0, kb1);
         const int acc = t & 1;
         mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
           const uint32_t ph = (it / Cfg::STAGES) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t a0 = umma_desc_k_sw128(sA + s * Cfg::A_BYTES);
-          const uint64_t b0 = umma_desc_k_sw128(sB + s * Cfg::B_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk)  // +32 B per K=16 step inside the swizzle atom
-            mma_bf16(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          for (int j = 0; j < Cfg::KATOMS; ++j) {
+            const uint64_t a0 = umma_desc_k_sw128(sA + s * Cfg::A_BYTES + j * Cfg::A_ATOM);
+            const uint64_t b0 = umma_desc_k_sw128(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 16; ++kk)  // +32 B per K=16 step inside the swizzle atom
+              mma_bf16(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
+                       (kb > kb0 || j || kk) ? 1u : 0u);
+          }
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[acc]);
@@ -167,7 +254,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int g = warp & 3;  // TMEM lane quarter this warp may access
     uint32_t t = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
-      const int mb = w % m_tiles, nb = w / m_tiles;
+      int mb, nb, kb0, kb1;
+      unit(w, mb, nb, kb0, kb1);
+      const int sp = (w / m_tiles) % splits;
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -180,7 +269,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         tmem_ld_wait();
         const int col0 = nb * BN + cc * 32;
         if (!row_ok || col0 >= N) continue;
-        epilogue_row32(C, ldc, row, col0, N, r, epi, out_dtype);
+        if (splits > 1)  // raw fp32 partial; qcf reduce applies the epilogue in a fixed order
+          epilogue_row32(partial + (int64_t)sp * M * N, N, row, col0, N, r, EpiArgs{QCF_EPI_STORE, QCF_F32});
+        else
+          epilogue_row32(C, ldc, row, col0, N, r, ea);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -211,7 +303,7 @@ struct Tc2Cfg {
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                void* __restrict__ C, int64_t ldc, int M, int N, int K, int epi, int out_dtype) {
+                void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea) {
   using Cfg = Tc2Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -304,7 +396,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         tmem_ld_wait();
         const int col0 = nb * BN + cc * 32;
         if (!row_ok || col0 >= N) continue;
-        epilogue_row32(C, ldc, row, col0, N, r, epi, out_dtype);
+        epilogue_row32(C, ldc, row, col0, N, r, ea);
       }
       tc_fence_before();
       mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
@@ -315,6 +407,39 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// deterministic split-K reduction: C = epi(sum_s partial[s]) in split order
+__global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M, int N,
+                                     void* __restrict__ C, int64_t ldc, int epi, int out_dtype) {
+  const int64_t total4 = (int64_t)M * N / 4;
+  const int64_t mn = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 4 * i;
+    float4 acc = *reinterpret_cast<const float4*>(partial + e);
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 v = *reinterpret_cast<const float4*>(partial + sp * mn + e);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const int row = (int)(e / N), col = (int)(e - (int64_t)row * N);
+    if (out_dtype == QCF_F32) {
+      float4* c = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)row * ldc + col);
+      if (epi == QCF_EPI_ADD_F32) {
+        const float4 o = *c;
+        acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+      } else if (epi == QCF_EPI_RELU) {
+        acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+      }
+      *c = acc;
+    } else {
+      if (epi == QCF_EPI_RELU) {
+        acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+      }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
   }
 }
 
@@ -362,30 +487,39 @@ static int sm_count() {
   return n;
 }
 
-template <int BN>
+template <int BN, bool SKINNY = false>
 static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                     int64_t n, int64_t k, int epi, int out_dtype, cudaStream_t s) {
+                     int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, int splits = 1,
+                     int a_box_rows = TC_BM, float* partial = nullptr) {
+  const int epi = ea.kind, out_dtype = ea.out_dtype;
+  using Cfg = TcCfg<BN, SKINNY>;
   CUtensorMap mb;
   int st = make_kmajor_map(&mb, b, n, k, ldb, BN);
   if (st != QCF_OK) return st;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         TcCfg<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SKINNY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc attr");
     attr_set = true;
   }
-  const int64_t work = ((m + TC_BM - 1) / TC_BM) * ((n + BN - 1) / BN);
+  const int64_t work = ((m + TC_BM - 1) / TC_BM) * ((n + BN - 1) / BN) * splits;
   const int grid = (int)std::min<int64_t>(work, sm_count());
-  gemm_tc_kernel<BN><<<grid, TC_THREADS, TcCfg<BN>::SMEM, s>>>(ma, mb, c, ldc, (int)m, (int)n, (int)k, epi,
-                                                               out_dtype);
+  gemm_tc_kernel<BN, SKINNY><<<grid, TC_THREADS, Cfg::SMEM, s>>>(ma, mb, c, ldc, (int)m, (int)n, (int)k, ea,
+                                                                 splits, a_box_rows, partial);
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05)");
+  if (splits > 1) {
+    const int64_t total4 = m * n / 4;
+    const int rg = (int)std::min<int64_t>((total4 + 255) / 256, 4 * sm_count());
+    splitk_reduce_kernel<<<rg, 256, 0, s>>>(partial, splits, (int)m, (int)n, c, ldc, epi, out_dtype);
+    QCF_LAUNCH_CHECK("qcf_gemm(split-k reduce)");
+  }
   return QCF_OK;
 }
 
 template <int BN>
 static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                       int64_t n, int64_t k, int epi, int out_dtype, cudaStream_t s) {
+                       int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
   CUtensorMap mb;
   int st = make_kmajor_map(&mb, b, n, k, ldb, BN / 2);
   if (st != QCF_OK) return st;
@@ -410,8 +544,7 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, epi,
-                                     out_dtype);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 pair)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 pair)");
   return QCF_OK;
@@ -419,8 +552,56 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 
 static int g_pair_mode = -1;  // QCF_GEMM_PAIR env: 0 off, 1 on (default on)
 
+// Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
+// weights; A box trimmed to the live rows. Returns splits (1 = no workspace).
+static int skinny_splits(int64_t m, int64_t n, int64_t k) {
+  if (m > 32) return 1;
+  const int64_t tiles = (n + 63) / 64, kb = (k + 4 * TC_BK - 1) / (4 * TC_BK);
+  int sp = 1;
+  while (tiles * sp < 2 * sm_count() && kb / (sp * 2) >= 4 && sp < 16) sp *= 2;
+  return sp;
+}
+
+size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+  const int sp = skinny_splits(m, n, k);
+  return sp > 1 ? (size_t)sp * m * n * sizeof(float) : 0;
+}
+
+int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                   int64_t n, int64_t k, int epilogue, int out_dtype, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int sp = skinny_splits(m, n, k);
+  if (sp <= 1 || ws_bytes < gemm_workspace_bytes(m, n, k) || (n % 4) || ((uintptr_t)ws & 15)) return QCF_EUNSUPPORTED;
+  if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
+  if ((ldc % 4) || ((uintptr_t)c & 15)) return QCF_EUNSUPPORTED;
+  const int box = (int)((m + 15) / 16 * 16);
+  CUtensorMap ma;
+  int st = make_kmajor_map(&ma, a, m, k, lda, box);
+  if (st != QCF_OK) return st;
+  return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype}, s, sp, box, (float*)ws);
+}
+
+static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
+                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s);
+
 int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                    int64_t n, int64_t k, int epilogue, int out_dtype, cudaStream_t s) {
+  return gemm_tc_launch_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype}, s);
+}
+
+int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k, int h,
+                         int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
+                         const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s) {
+  if (d % 32 || m <= 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
+  if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab) & 15) return QCF_EUNSUPPORTED;
+  EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
+  const int64_t n = (int64_t)(h + 2 * hkv) * d;
+  void* dummy_c = q_out;  // C is not written by this epilogue
+  return gemm_tc_launch_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, s);
+}
+
+static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
+                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+  const int out_dtype = ea.out_dtype;
   // TMA: 16-byte aligned bases and row strides; vector epilogue alignment
   if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
   if (out_dtype == QCF_F32 && ((ldc % 4) || ((uintptr_t)c & 15))) return QCF_EUNSUPPORTED;
@@ -445,12 +626,12 @@ int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void*
     const int64_t t1 = mt * ((n + 255) / 256);
     const double e_one = 0.85 * (double)t1 / (double)(((t1 + sms - 1) / sms) * sms) * (double)m / (double)(mt * 128);
     if (units >= clusters / 2 && e_pair >= e_one)
-      return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
+      return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s);
   }
   // tile width: enough tiles to cover the SMs, widest tile otherwise
-  if (n >= 256 && mt * ((n + 255) / 256) >= sms) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
-  if (n >= 128 && mt * ((n + 127) / 128) >= sms) return launch_bn<128>(ma, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
-  return launch_bn<64>(ma, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
+  if (n >= 256 && mt * ((n + 255) / 256) >= sms) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, ea, s);
+  if (n >= 128 && mt * ((n + 127) / 128) >= sms) return launch_bn<128>(ma, b, ldb, c, ldc, m, n, k, ea, s);
+  return launch_bn<64>(ma, b, ldb, c, ldc, m, n, k, ea, s);
 }
 
 }  // namespace qcf

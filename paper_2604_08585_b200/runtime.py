@@ -16,6 +16,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import _lib
 from ._lib import EPI_ADD_F32, EPI_RELU, EPI_STORE, QCF_F32, call
 from .model import ModelWeights, RopeTable, cuda_stream
 
@@ -30,6 +31,7 @@ class Scratch:
     q: torch.Tensor      # dt  [cap, H, D] rotated queries
     o: torch.Tensor      # dt  [cap, H*D] attention output
     hid: torch.Tensor    # dt  [cap, F]   relu(W1 x)
+    ws: torch.Tensor     # u8  split-K workspace of the skinny-M GEMMs
 
 
 class Executor:
@@ -38,6 +40,9 @@ class Executor:
         self.cfg = weights.config
         self.rope = rope or RopeTable(self.cfg.d_head, self.cfg.rope_theta, weights.device)
         self._scratch: dict[int, Scratch] = {}
+        # fused QKV+RoPE epilogue: bf16 on a tcgen05 device, head dim a multiple of 32
+        self.fused_qkv = (weights.dtype == "bf16" and self.cfg.d_head % 32 == 0
+                          and torch.cuda.is_available() and bool(_lib.lib.qcf_tc_available()))
 
     # ------------------------------------------------------------------
     def scratch(self, m: int, key=None) -> Scratch:
@@ -48,13 +53,17 @@ class Executor:
             cfg, dev, dt = self.cfg, self.w.device, self.w.torch_dtype
             cap = max(m, 16)
             H, Hkv, D = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
+            d, F = cfg.d_model, cfg.d_ff
+            ws_bytes = max(int(_lib.lib.qcf_gemm_workspace(cap, n, k))
+                           for n, k in (((H + 2 * Hkv) * D, d), (d, H * D), (F, d), (d, F)))
             s = Scratch(cap,
                         torch.empty(cap, cfg.d_model, dtype=torch.float32, device=dev),
                         torch.empty(cap, cfg.d_model, dtype=dt, device=dev),
                         torch.empty(cap, (H + 2 * Hkv) * D, dtype=torch.float32, device=dev),
                         torch.empty(cap, H, D, dtype=dt, device=dev),
                         torch.empty(cap, H * D, dtype=dt, device=dev),
-                        torch.empty(cap, cfg.d_ff, dtype=dt, device=dev))
+                        torch.empty(cap, cfg.d_ff, dtype=dt, device=dev),
+                        torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev))
             self._scratch[k] = s
         return s
 
@@ -64,6 +73,11 @@ class Executor:
         call("qcf_embed", tokens.data_ptr(), rows.data_ptr() if rows is not None else None,
              row_base, m, self.w.emb.data_ptr(), self.cfg.d_model, sc.x.data_ptr(),
              cuda_stream(stream))
+
+    def gemm(self, sc: Scratch, a, lda, b, ldb, c, ldc, m, n, k, epi, out_dt, s) -> None:
+        """qcf_gemm_ws: tcgen05 (2-CTA / 1-CTA / split-K skinny) for bf16, FFMA for f32."""
+        call("qcf_gemm_ws", self.w.qcf_dtype, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), ldc,
+             m, n, k, epi, out_dt, sc.ws.data_ptr(), sc.ws.numel(), s)
 
     def layer(self, li: int, sc: Scratch, m: int, pos: torch.Tensor, dst: torch.Tensor,
               kmax: torch.Tensor, tab_k: torch.Tensor, tab_v: torch.Tensor,
@@ -80,24 +94,26 @@ class Executor:
         nq = (H + 2 * Hkv) * D
         call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln1_g.data_ptr(), lw.ln1_b.data_ptr(),
              cfg.ln_eps, sc.a.data_ptr(), dt, s)
-        call("qcf_gemm", dt, sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, sc.qkv.data_ptr(), nq,
-             m, nq, d, EPI_STORE, QCF_F32, s)
         qdst = q_out if q_out is not None else sc.q
-        call("qcf_rope_qkv_scatter", sc.qkv.data_ptr(), m, H, Hkv, D, pos.data_ptr(),
-             dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(), self.rope.n_pos,
-             qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
+        if self.fused_qkv and m > 32:
+            # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue
+            call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, m, d, H, Hkv, D,
+                 pos.data_ptr(), dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(),
+                 self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), s)
+        else:
+            self.gemm(sc, sc.a, d, lw.wqkv, d, sc.qkv, nq, m, nq, d, EPI_STORE, QCF_F32, s)
+            call("qcf_rope_qkv_scatter", sc.qkv.data_ptr(), m, H, Hkv, D, pos.data_ptr(),
+                 dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(), self.rope.n_pos,
+                 qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
         if q_only:
             return
         call("qcf_attention", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
              kmax.data_ptr(), m, H, Hkv, D, tab_k.shape[0], sc.o.data_ptr(), s)
-        call("qcf_gemm", dt, sc.o.data_ptr(), H * D, lw.wo.data_ptr(), H * D, sc.x.data_ptr(), d,
-             m, d, H * D, EPI_ADD_F32, QCF_F32, s)
+        self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.x, d, m, d, H * D, EPI_ADD_F32, QCF_F32, s)
         call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln2_g.data_ptr(), lw.ln2_b.data_ptr(),
              cfg.ln_eps, sc.a.data_ptr(), dt, s)
-        call("qcf_gemm", dt, sc.a.data_ptr(), d, lw.w1.data_ptr(), d, sc.hid.data_ptr(), F,
-             m, F, d, EPI_RELU, dt, s)
-        call("qcf_gemm", dt, sc.hid.data_ptr(), F, lw.w2.data_ptr(), F, sc.x.data_ptr(), d,
-             m, d, F, EPI_ADD_F32, QCF_F32, s)
+        self.gemm(sc, sc.a, d, lw.w1, d, sc.hid, F, m, F, d, EPI_RELU, dt, s)
+        self.gemm(sc, sc.hid, F, lw.w2, F, sc.x, d, m, d, F, EPI_ADD_F32, QCF_F32, s)
 
     def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
               layers: range | None = None, q_store: torch.Tensor | None = None, stream=None) -> None:

@@ -264,3 +264,56 @@ def test_attention_tensor_core_long_and_rescale(L, m, n, H, growth):
     ref = torch_attention(q, k, v, pos.long())
     err = (out.float() - ref).abs().max().item()
     assert err < 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("m,n,k,epi", [(32, 12288, 4096, 0), (32, 4096, 14336, 2), (32, 14336, 4096, 1),
+                                       (20, 4096, 4096, 2), (64, 1024, 2048, 0), (1, 4096, 4096, 0)])
+def test_gemm_skinny_splitk_deterministic(L, m, n, k, epi):
+    torch.manual_seed(m + n)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
+    c0 = torch.randn(m, n, device="cuda")
+    ws = torch.empty(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        c = c0.clone() if epi == 2 else torch.empty(m, n, device="cuda",
+                                                     dtype=torch.bfloat16 if epi == 1 else torch.float32)
+        L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c), n, m, n, k, epi, out_dt, p(ws), ws.numel(), S())
+        outs.append(c)
+    ref = a.float() @ b.float().T
+    if epi == 1:
+        ref = torch.relu(ref)
+    if epi == 2:
+        ref = c0 + ref
+    scale = ref.abs().max().item()
+    tol = 2e-6 * math.sqrt(k) * max(scale, 1.0) + (scale * 2 ** -8 if epi == 1 else 0)
+    assert (outs[0].float() - ref).abs().max().item() < tol
+    assert torch.equal(outs[0], outs[1])          # fixed-order split-K reduction
+
+
+@pytest.mark.parametrize("m,heads", [(800, 4), (33, 2), (5153, 2)])
+def test_fused_qkv_rope_matches_two_step(L, m, heads):
+    """qcf_gemm_qkv_rope == qcf_gemm (f32 QKV) + qcf_rope_qkv_scatter (bf16 table)."""
+    from paper_2604_08585_b200.model import RopeTable
+    torch.manual_seed(m)
+    D, K = 128, 512
+    N = 3 * heads * D
+    a = (torch.randn(m, K, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    pos = torch.sort(torch.randperm(6000, device="cuda")[:m]).values.int()
+    dst = torch.randperm(m + 7, device="cuda")[:m].int()
+    rope = RopeTable(D, 10000.0, "cuda", 8192)
+    q1 = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
+    k1 = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
+    v1 = torch.zeros_like(k1)
+    L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
+           rope.n_pos, p(q1), p(k1), p(v1), S())
+    qkv = torch.empty(m, N, device="cuda")
+    L.call("qcf_gemm", L.QCF_BF16, p(a), K, p(w), K, p(qkv), N, m, N, K, 0, L.QCF_F32, S())
+    q2, k2, v2 = torch.zeros_like(q1), torch.zeros_like(k1), torch.zeros_like(v1)
+    L.call("qcf_rope_qkv_scatter", p(qkv), m, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin), rope.n_pos,
+           p(q2), p(k2), p(v2), L.QCF_BF16, S())
+    for x, y in ((q1, q2), (k1, k2), (v1, v2)):
+        assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
+    assert torch.equal(v1, v2)
