@@ -94,6 +94,13 @@ int qcf_embed(const int32_t* tokens, const int32_t* rows, int32_t row_base, int6
 /* out[i] = (x[i]-mean)/sqrt(var+eps)*g + b ; out in out_dtype */
 int qcf_layernorm(const float* x, int64_t m, int d, const float* g, const float* b,
                   float eps, void* out, int out_dtype, qcf_stream_t stream);
+/* x += delta (residual update, written back), then out = LN(x). delta may be
+ * NULL (= qcf_layernorm). Fuses model.py:375-376's residual adds into the
+ * following LayerNorm so the projections store instead of read-modify-write. */
+int qcf_add_layernorm(float* x, const float* delta, int64_t m, int d, const float* g, const float* b,
+                      float eps, void* out, int out_dtype, qcf_stream_t stream);
+/* x[i] += delta[i] for n floats (n % 4 == 0, 16-byte aligned) */
+int qcf_add_rows(float* x, const float* delta, int64_t n, qcf_stream_t stream);
 /* logits[r] = LN_f(x[rows[r]]) @ emb^T  (model.py:384-385, fusion.py:540) */
 int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d,
                 const float* g, const float* b, float eps, const float* emb,

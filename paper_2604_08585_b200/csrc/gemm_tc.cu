@@ -140,6 +140,7 @@ __device__ __forceinline__ void epilogue_row32(void* __restrict__ C, int64_t ldc
 // output rows >= M that the epilogue never stores.
 // SKINNY also moves 4 swizzle atoms (K=256) per stage, amortising the per-stage
 // mbarrier round trips of the producer/MMA threads over 4x more weight bytes.
+
 template <int BN, bool SKINNY = false>
 struct TcCfg {
   static constexpr int KATOMS = SKINNY ? 4 : 1;   // 64-element K atoms per stage
@@ -258,10 +259,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       unit(w, mb, nb, kb0, kb1);
       const int sp = (w / m_tiles) % splits;
       const int acc = t & 1;
-      mbar_wait(&tfull[acc], (t >> 1) & 1);
-      tc_fence_after();
       const int row = mb * TC_BM + g * 32 + lane;
       const bool row_ok = row < M;
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
         uint32_t r[32];
@@ -385,10 +386,10 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     for (int w = cluster; w < n_work; w += n_clusters, ++t) {
       const int mp = w % m_pairs, nb = w / m_pairs;
       const int acc = t & 1;
-      mbar_wait(&tfull[acc], (t >> 1) & 1);
-      tc_fence_after();
       const int row = mp * 2 * TC_BM + rank * TC_BM + g * 32 + lane;
       const bool row_ok = row < M;
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
         uint32_t r[32];

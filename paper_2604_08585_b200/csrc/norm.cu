@@ -62,14 +62,18 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a,
   *reinterpret_cast<uint2*>(p) = u;
 }
 
+// With `delta` != null the residual update x += delta (the projection output,
+// model.py:375-376) is applied first and written back, fusing the residual add
+// that would otherwise be a read-modify-write in the GEMM epilogue.
 template <typename T>
-__global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __restrict__ x, int64_t m, int d,
-                                                               const float* __restrict__ g,
+__global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
+                                                               int64_t m, int d, const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps,
                                                                T* __restrict__ out) {
   __shared__ float red[LN_THREADS / 32];
   const int64_t row = blockIdx.x;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+  float4* xr = reinterpret_cast<float4*>(x + row * d);
+  const float4* dr = delta ? reinterpret_cast<const float4*>(delta + row * d) : nullptr;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
   const int n4 = d >> 2;
@@ -81,6 +85,17 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
     v[i] = ok ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
     gv[i] = ok ? g4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
     bv[i] = ok ? b4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (dr) {
+#pragma unroll
+    for (int i = 0; i < LN_V4; ++i) {
+      const int e = threadIdx.x + i * LN_THREADS;
+      if (e < n4) {
+        const float4 t = dr[e];
+        v[i].x += t.x; v[i].y += t.y; v[i].z += t.z; v[i].w += t.w;
+        xr[e] = v[i];
+      }
+    }
   }
   float s = 0.f;
 #pragma unroll
@@ -108,12 +123,18 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
 
 // generic fallback (d % 4 != 0): one CTA per row, strided scalar loop
 template <typename T>
-__global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(const float* __restrict__ x, int64_t m, int d,
-                                                                      const float* __restrict__ g,
+__global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(float* __restrict__ x,
+                                                                      const float* __restrict__ delta, int64_t m,
+                                                                      int d, const float* __restrict__ g,
                                                                       const float* __restrict__ b, float eps,
                                                                       T* __restrict__ out) {
   __shared__ float red[LN_THREADS / 32];
-  const float* xr = x + (int64_t)blockIdx.x * d;
+  float* xr = x + (int64_t)blockIdx.x * d;
+  if (delta) {
+    const float* dr = delta + (int64_t)blockIdx.x * d;
+    for (int e = threadIdx.x; e < d; e += LN_THREADS) xr[e] = xr[e] + dr[e];
+    __syncthreads();
+  }
   float s = 0.f;
   for (int e = threadIdx.x; e < d; e += LN_THREADS) s += xr[e];
   const float mean = block_sum_256(s, red) / d;
@@ -122,6 +143,15 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(const floa
   const float sd = sqrtf(block_sum_256(q, red) / d + eps);
   T* orow = out + (int64_t)blockIdx.x * d;
   for (int e = threadIdx.x; e < d; e += LN_THREADS) orow[e] = from_f<T>(((xr[e] - mean) / sd) * g[e] + b[e]);
+}
+
+__global__ void add_rows_kernel(float* __restrict__ x, const float* __restrict__ delta, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(x)[i];
+    const float4 t = reinterpret_cast<const float4*>(delta)[i];
+    a.x += t.x; a.y += t.y; a.z += t.z; a.w += t.w;
+    reinterpret_cast<float4*>(x)[i] = a;
+  }
 }
 
 // lm-head: grid (vocab tiles of 32, rows). Every CTA recomputes LN_f of its
@@ -212,22 +242,41 @@ int qcf_embed(const int32_t* tokens, const int32_t* rows, int32_t row_base, int6
   return QCF_OK;
 }
 
+int qcf_add_layernorm(float* x, const float* delta, int64_t m, int d, const float* g, const float* b,
+                      float eps, void* out, int out_dtype, qcf_stream_t stream);
+
 int qcf_layernorm(const float* x, int64_t m, int d, const float* g, const float* b, float eps,
                   void* out, int out_dtype, qcf_stream_t stream) {
+  return qcf_add_layernorm(const_cast<float*>(x), nullptr, m, d, g, b, eps, out, out_dtype, stream);
+}
+
+int qcf_add_rows(float* x, const float* delta, int64_t n, qcf_stream_t stream) {
+  QCF_REQUIRE(x && delta && n >= 0 && n % 4 == 0, QCF_EINVAL, "qcf_add_rows: bad args");
+  QCF_REQUIRE(!(((uintptr_t)x | (uintptr_t)delta) & 15), QCF_EINVAL, "qcf_add_rows: 16-byte alignment");
+  if (n == 0) return QCF_OK;
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+  qcf::add_rows_kernel<<<grid, 256, 0, qcf::as_stream(stream)>>>(x, delta, n4);
+  QCF_LAUNCH_CHECK("qcf_add_rows");
+  return QCF_OK;
+}
+
+int qcf_add_layernorm(float* x, const float* delta, int64_t m, int d, const float* g, const float* b,
+                      float eps, void* out, int out_dtype, qcf_stream_t stream) {
   QCF_REQUIRE(x && g && b && out && d > 0 && m >= 0, QCF_EINVAL, "qcf_layernorm: bad args");
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
   QCF_REQUIRE(m <= 0x7fffffff, QCF_EUNSUPPORTED, "qcf_layernorm: too many rows");
   const unsigned grid = (unsigned)m;
   const bool vec = (d % 4 == 0) && d <= qcf::LN_THREADS * 4 * qcf::LN_V4 &&
-                   !(((uintptr_t)x | (uintptr_t)g | (uintptr_t)b | (uintptr_t)out) & 15) &&
+                   !(((uintptr_t)x | (uintptr_t)g | (uintptr_t)b | (uintptr_t)out | (uintptr_t)delta) & 15) &&
                    (out_dtype == QCF_F32 || d % 8 == 0);
   if (out_dtype == QCF_F32) {
-    if (vec) qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
-    else qcf::layernorm_scalar_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (float*)out);
+    if (vec) qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (float*)out);
+    else qcf::layernorm_scalar_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (float*)out);
   } else if (out_dtype == QCF_BF16) {
-    if (vec) qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
-    else qcf::layernorm_scalar_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, m, d, g, b, eps, (__nv_bfloat16*)out);
+    if (vec) qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
+    else qcf::layernorm_scalar_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
   } else {
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_layernorm: bad dtype");
   }

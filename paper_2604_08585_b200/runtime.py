@@ -32,6 +32,8 @@ class Scratch:
     o: torch.Tensor      # dt  [cap, H*D] attention output
     hid: torch.Tensor    # dt  [cap, F]   relu(W1 x)
     ws: torch.Tensor     # u8  split-K workspace of the skinny-M GEMMs
+    delta: torch.Tensor  # f32 [cap, d] projection output awaiting its residual add
+    pending: bool = False  # delta not yet added into x (launch-sequencing state)
 
 
 class Executor:
@@ -63,7 +65,8 @@ class Executor:
                         torch.empty(cap, H, D, dtype=dt, device=dev),
                         torch.empty(cap, H * D, dtype=dt, device=dev),
                         torch.empty(cap, cfg.d_ff, dtype=dt, device=dev),
-                        torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev))
+                        torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev),
+                        torch.empty(cap, cfg.d_model, dtype=torch.float32, device=dev))
             self._scratch[k] = s
         return s
 
@@ -73,6 +76,22 @@ class Executor:
         call("qcf_embed", tokens.data_ptr(), rows.data_ptr() if rows is not None else None,
              row_base, m, self.w.emb.data_ptr(), self.cfg.d_model, sc.x.data_ptr(),
              cuda_stream(stream))
+        sc.pending = False
+
+    def _norm(self, sc: Scratch, m: int, g, b, s) -> None:
+        """a = LN(x), first folding a pending projection output into x
+        (the residual adds of model.py:375-376, fused into the LayerNorm)."""
+        call("qcf_add_layernorm", sc.x.data_ptr(), sc.delta.data_ptr() if sc.pending else None, m,
+             self.cfg.d_model, g.data_ptr(), b.data_ptr(), self.cfg.ln_eps, sc.a.data_ptr(),
+             self.w.qcf_dtype, s)
+        sc.pending = False
+
+    def flush(self, sc: Scratch, m: int, stream=None) -> None:
+        """Make x current (apply a pending residual add)."""
+        if sc.pending:
+            call("qcf_add_rows", sc.x.data_ptr(), sc.delta.data_ptr(), m * self.cfg.d_model,
+                 cuda_stream(stream))
+            sc.pending = False
 
     def gemm(self, sc: Scratch, a, lda, b, ldb, c, ldc, m, n, k, epi, out_dt, s) -> None:
         """qcf_gemm_ws: tcgen05 (2-CTA / 1-CTA / split-K skinny) for bf16, FFMA for f32."""
@@ -92,8 +111,7 @@ class Executor:
         dt = w.qcf_dtype
         s = cuda_stream(stream)
         nq = (H + 2 * Hkv) * D
-        call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln1_g.data_ptr(), lw.ln1_b.data_ptr(),
-             cfg.ln_eps, sc.a.data_ptr(), dt, s)
+        self._norm(sc, m, lw.ln1_g, lw.ln1_b, s)
         qdst = q_out if q_out is not None else sc.q
         if self.fused_qkv and m > 32:
             # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue
@@ -109,11 +127,12 @@ class Executor:
             return
         call("qcf_attention", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
              kmax.data_ptr(), m, H, Hkv, D, tab_k.shape[0], sc.o.data_ptr(), s)
-        self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.x, d, m, d, H * D, EPI_ADD_F32, QCF_F32, s)
-        call("qcf_layernorm", sc.x.data_ptr(), m, d, lw.ln2_g.data_ptr(), lw.ln2_b.data_ptr(),
-             cfg.ln_eps, sc.a.data_ptr(), dt, s)
+        self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.delta, d, m, d, H * D, EPI_STORE, QCF_F32, s)
+        sc.pending = True
+        self._norm(sc, m, lw.ln2_g, lw.ln2_b, s)
         self.gemm(sc, sc.a, d, lw.w1, d, sc.hid, F, m, F, d, EPI_RELU, dt, s)
-        self.gemm(sc, sc.hid, F, lw.w2, F, sc.x, d, m, d, F, EPI_ADD_F32, QCF_F32, s)
+        self.gemm(sc, sc.hid, F, lw.w2, F, sc.delta, d, m, d, F, EPI_STORE, QCF_F32, s)
+        sc.pending = True
 
     def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
               layers: range | None = None, q_store: torch.Tensor | None = None, stream=None) -> None:
@@ -123,6 +142,7 @@ class Executor:
         for li in layers:
             self.layer(li, sc, m, pos, dst, kmax, tab_k[li], tab_v[li],
                        q_out=q_store[li] if q_store is not None else None, stream=stream)
+        self.flush(sc, m, stream)
 
     def lm_head(self, sc: Scratch, rows: torch.Tensor, out: torch.Tensor, stream=None) -> None:
         """logits[r] = LN_f(x[rows[r]]) @ embᵀ (model.py:384-385)."""
