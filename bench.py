@@ -292,8 +292,11 @@ def main():
     gemm_shapes: dict[str, list] = {}
     for name, a, ms in recs:
         phases[name] = phases.get(name, 0.0) + ms
-        if name in ("qcf_gemm", "qcf_gemm_ws"):
-            m_, n_, k_ = a[7], a[8], a[9]
+        if name in ("qcf_gemm", "qcf_gemm_ws", "qcf_gemm_qkv_rope"):
+            if name == "qcf_gemm_qkv_rope":
+                m_, k_, n_ = a[4], a[5], (a[6] + 2 * a[7]) * a[8]
+            else:
+                m_, n_, k_ = a[7], a[8], a[9]
             gemm_flops += 2.0 * m_ * n_ * k_
             gemm_ms += ms
             n_gemm += 1
@@ -316,7 +319,8 @@ def main():
             traffic = json.loads(tf.read_text()).get("bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "qcf_gemm (tcgen05, bf16)", "achieved": achieved,
+    roofline = {"bound": "tensor", "kernel": "qcf_gemm* family (tcgen05 bf16: 2-CTA/1-CTA/split-K, fused QKV+RoPE)",
+                "achieved": achieved,
                 "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": (achieved / pk["bf16_tflops"]) if achieved else None, "traffic": traffic,
                 "launches_per_step": n_gemm, "share_of_step": gemm_ms / sum(phases.values()),
