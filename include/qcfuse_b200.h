@@ -40,6 +40,10 @@ enum qcf_status {
 
 enum qcf_dtype { QCF_F32 = 0, QCF_BF16 = 1 };
 
+/* GEMM B-operand (weight) layouts. TILE64 = [N/64][K/64][64][64]: every 64x64
+ * tile is 8 KB contiguous, so weight streaming reads whole DRAM pages. */
+enum qcf_b_layout { QCF_B_ROWMAJOR = 0, QCF_B_TILE64 = 1 };
+
 enum qcf_epilogue {
   QCF_EPI_STORE = 0,     /* C = acc                (C in out_dtype)          */
   QCF_EPI_RELU = 1,      /* C = max(acc, 0)        (C in out_dtype)          */
@@ -121,8 +125,8 @@ int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
  * returns 0. */
 size_t qcf_gemm_workspace(int64_t m, int64_t n, int64_t k);
 int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
-                int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, void* ws, size_t ws_bytes,
-                qcf_stream_t stream);
+                int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout, void* ws,
+                size_t ws_bytes, qcf_stream_t stream);
 /* Same contract, forced onto the SIMT path (cross-check of the tensor-core path). */
 int qcf_gemm_simt(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
                   void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
@@ -142,7 +146,7 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
  * Q/K at pos[i] and writes q_out[i], k_tab[dst_rows[i]], v_tab[dst_rows[i]].
  * Returns QCF_EUNSUPPORTED when d % 32 != 0 or m <= 32 (callers then use
  * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478. */
-int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k,
+int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m, int64_t k,
                       int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
                       const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
                       void* k_tab, void* v_tab, qcf_stream_t stream);

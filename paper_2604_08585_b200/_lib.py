@@ -19,6 +19,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("QCFUSE_B200_LIB", _HERE / "libqcfuse_b200.so"))
 
 QCF_F32, QCF_BF16 = 0, 1
+B_ROWMAJOR, B_TILE64 = 0, 1
 EPI_STORE, EPI_RELU, EPI_ADD_F32 = 0, 1, 2
 
 QCF_OK, QCF_EINVAL, QCF_ESHAPE, QCF_ECUDA, QCF_EUNSUPPORTED, QCF_EWORKSPACE = 0, -1, -2, -3, -4, -5
@@ -55,9 +56,9 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_gemm": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
     "qcf_gemm_simt": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
     "qcf_gemm_workspace": (_SZ, [_I64, _I64, _I64]),
-    "qcf_gemm_ws": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P, _SZ, _P]),
+    "qcf_gemm_ws": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _I, _P, _SZ, _P]),
     "qcf_rope_qkv_scatter": (_I, [_P, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _I, _P]),
-    "qcf_gemm_qkv_rope": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "qcf_gemm_qkv_rope": (_I, [_P, _I64, _P, _I64, _I, _I64, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
     "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),

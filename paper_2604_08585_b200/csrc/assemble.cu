@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
     T* __restrict__ fv, int64_t fstride, int row_elems, int d,
     const double* __restrict__ ctab, const double* __restrict__ stab) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int V = Vec16<T>::N;
   const int layer = blockIdx.y;
   const int vpr = row_elems / V;
@@ -87,6 +89,8 @@ __global__ void gather_rows_kernel(const T* __restrict__ sk, const T* __restrict
                                    const int32_t* __restrict__ rows, int64_t n_rows,
                                    T* __restrict__ dk, T* __restrict__ dv, int64_t dstride,
                                    int64_t row_elems) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int V = Vec16<T>::N;
   const int layer = blockIdx.y;
   const int64_t vpr = row_elems / V;
@@ -124,10 +128,10 @@ extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ct
   int gx = (int)std::min<int64_t>((per_layer + 255) / 256, 65535 * 4);
   dim3 grid(gx, n_layers);
   if (dtype == QCF_F32)
-    qcf::assemble_kernel<float><<<grid, 256, 0, s>>>(chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
+    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
         (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
   else if (dtype == QCF_BF16)
-    qcf::assemble_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(chunks, n_chunks, n_ctx + 1,
+    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1,
         (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
         (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
   else
@@ -148,10 +152,10 @@ extern "C" int qcf_gather_rows(const void* src_k, const void* src_v, int64_t src
   int gx = (int)std::min<int64_t>((n_rows * (row_elems / vec) + 255) / 256, 65535);
   dim3 grid(gx, n_layers);
   if (dtype == QCF_F32)
-    qcf::gather_rows_kernel<float><<<grid, 256, 0, s>>>((const float*)src_k, (const float*)src_v,
+    QCF_LAUNCH("gather_rows_kernel", qcf::gather_rows_kernel<float>, dim3(grid), dim3(256), 0, s, (const float*)src_k, (const float*)src_v,
         src_layer_stride, rows, n_rows, (float*)dst_k, (float*)dst_v, dst_layer_stride, row_elems);
   else
-    qcf::gather_rows_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)src_k,
+    QCF_LAUNCH("gather_rows_kernel", qcf::gather_rows_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)src_k,
         (const __nv_bfloat16*)src_v, src_layer_stride, rows, n_rows, (__nv_bfloat16*)dst_k,
         (__nv_bfloat16*)dst_v, dst_layer_stride, row_elems);
   QCF_LAUNCH_CHECK("qcf_gather_rows");

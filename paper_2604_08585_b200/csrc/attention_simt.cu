@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
                                                         const int32_t* __restrict__ kmax, int64_t m,
                                                         int h, int hkv, int64_t n_keys,
                                                         T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   float* Qs = sm;                        // [AQ][D+1]
   float* Ks = Qs + AQ * (D + 1);         // [AK][D+1]
@@ -134,7 +136,7 @@ static int launch_simt(const void* q, const void* k, const void* v, const int32_
     if (e != cudaSuccess) return cuda_status(e, "attn_simt attr");
   }
   dim3 grid(ceil_div(m, AQ), h);
-  attn_simt_kernel<T, D><<<grid, 128, smem, s>>>((const T*)q, (const T*)k, (const T*)v, kmax, m, h,
+  QCF_LAUNCH("attn_simt_kernel", attn_simt_kernel<T, D>, dim3(grid), dim3(128), smem, s, (const T*)q, (const T*)k, (const T*)v, kmax, m, h,
                                                  hkv, n_keys, (T*)out);
   QCF_LAUNCH_CHECK("qcf_attention(simt)");
   return QCF_OK;

@@ -104,7 +104,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     fence_barrier_init();
     s_kend = 0;
   }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   __syncthreads();
+  pdl_wait();  // barrier init + TMEM alloc overlap the previous kernel's tail
+  pdl_trigger();
   // key range of this tile = 1 + max kmax over its rows (rows are normally
   // sorted by position, but the kernel does not rely on it)
   if (threadIdx.x < AT_BM) {
@@ -113,7 +116,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
     if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -328,7 +330,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
   dim3 grid((unsigned)h, (unsigned)((m + AT_BM - 1) / AT_BM));
-  attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, s>>>(mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
+  QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
                                                    (__nv_bfloat16*)out);
   QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");
   return QCF_OK;

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <utility>
 #include <string>
 
 #include "../../include/qcfuse_b200.h"
@@ -73,4 +74,37 @@ __device__ __forceinline__ void rotate_pair_fast(float e, float o, float c, floa
   oo = e * s + o * c;
 }
 
+
+// ---- Programmatic Dependent Launch ---------------------------------------------
+// Every hot-path kernel is launched with programmatic stream serialisation: it
+// may be scheduled while its predecessor drains, runs its prologue, and blocks
+// in pdl_wait() (griddepcontrol.wait = predecessor complete + memory visible)
+// before touching global memory; pdl_trigger() lets the next kernel launch.
+// Both are no-ops when a kernel is launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define QCF_LAUNCH(where, ...)                                          \
+  do {                                                                  \
+    cudaError_t _e = ::qcf::launch_k(__VA_ARGS__);                     \
+    if (_e != cudaSuccess) return ::qcf::cuda_status(_e, where);        \
+  } while (0)
 }  // namespace qcf

@@ -58,21 +58,28 @@ extern "C" int qcf_attention(int dtype, const void* q, const void* k, const void
 extern "C" size_t qcf_gemm_workspace(int64_t m, int64_t n, int64_t k) { return qcf::gemm_workspace_bytes(m, n, k); }
 
 extern "C" int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c,
-                           int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, void* ws,
-                           size_t ws_bytes, qcf_stream_t stream) {
+                           int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout,
+                           void* ws, size_t ws_bytes, qcf_stream_t stream) {
   int st = qcf::gemm_check_args(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype);
   if (st != QCF_OK) return st;
+  QCF_REQUIRE(b_layout == QCF_B_ROWMAJOR || b_layout == QCF_B_TILE64, QCF_EINVAL, "qcf_gemm_ws: bad b_layout");
   if (m == 0 || n == 0) return QCF_OK;
+  auto s = qcf::as_stream(stream);
   if (dtype == QCF_BF16 && qcf::tc_ok() && ws) {
-    st = qcf::gemm_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, ws, ws_bytes,
-                             qcf::as_stream(stream));
+    st = qcf::gemm_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, b_layout, ws, ws_bytes, s);
     if (st != QCF_EUNSUPPORTED) return st;
+  }
+  if (b_layout == QCF_B_TILE64) {
+    QCF_REQUIRE(dtype == QCF_BF16 && qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_ws: tile-major B needs tcgen05");
+    st = qcf::gemm_tc_launch(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s, 1);
+    if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_ws: shape not covered for tile-major B");
+    return st;
   }
   return qcf_gemm(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, stream);
 }
 
-extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k,
-                                 int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
+extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m,
+                                 int64_t k, int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
                                  const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
                                  void* k_tab, void* v_tab, qcf_stream_t stream) {
   (void)n_pos;
@@ -83,7 +90,7 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
   if (m == 0) return QCF_OK;
   QCF_REQUIRE(qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_qkv_rope: needs an sm_100 device");
   const int st = qcf::gemm_qkv_rope_launch(a, lda, w, ldb, m, k, h, hkv, d, pos, dst_rows, cos_tbl, sin_tbl,
-                                           q_out, k_tab, v_tab, qcf::as_stream(stream));
+                                           q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout);
   if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, m > 32, alignment)");
   return st;
 }

@@ -13,6 +13,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const TIn* __restrict__ 
                                                         const TIn* __restrict__ B, int64_t ldb,
                                                         void* __restrict__ C, int64_t ldc, int64_t M,
                                                         int64_t N, int64_t K, int epi, int out_dtype) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) float As[SB_K][SB_M + 4];
   __shared__ __align__(16) float Bs[SB_K][SB_N + 4];
   const int tid = threadIdx.x;
@@ -61,10 +63,10 @@ int gemm_simt_launch(int dtype, const void* a, int64_t lda, const void* b, int64
   dim3 grid(ceil_div(n, SB_N), ceil_div(m, SB_M));
   QCF_REQUIRE(grid.y <= 65535, QCF_EUNSUPPORTED, "gemm_simt: M too large");
   if (dtype == QCF_F32)
-    gemm_simt_kernel<float><<<grid, 256, 0, s>>>((const float*)a, lda, (const float*)b, ldb, c, ldc,
+    QCF_LAUNCH("gemm_simt_kernel", gemm_simt_kernel<float>, dim3(grid), dim3(256), 0, s, (const float*)a, lda, (const float*)b, ldb, c, ldc,
                                                  m, n, k, epilogue, out_dtype);
   else
-    gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)a, lda,
+    QCF_LAUNCH("gemm_simt_kernel", gemm_simt_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)a, lda,
         (const __nv_bfloat16*)b, ldb, c, ldc, m, n, k, epilogue, out_dtype);
   QCF_LAUNCH_CHECK("qcf_gemm_simt");
   return QCF_OK;

@@ -32,6 +32,7 @@ constexpr int QCF_EPI_ROPE_QKV = 3;  // internal: RoPE + KV scatter epilogue of 
 
 struct EpiArgs {
   int kind, out_dtype;
+  int b_tiled;  // B stored tile-major (64x64 tiles, 8 KB contiguous) -> 4D TMA boxes
   const int32_t* pos;
   const int32_t* dst;
   const double* cos_tbl;
@@ -201,6 +202,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -216,7 +219,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 #pragma unroll
           for (int j = 0; j < Cfg::KATOMS; ++j) {
             tma_load_2d(sA + s * Cfg::A_BYTES + j * Cfg::A_ATOM, &map_a, &full[s], kb * KSTAGE + j * TC_BK, mb * TC_BM);
-            tma_load_2d(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM, &map_b, &full[s], kb * KSTAGE + j * TC_BK, nb * BN);
+            if (ea.b_tiled)
+              tma_load_4d(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM, &map_b, &full[s], 0, 0, kb * Cfg::KATOMS + j,
+                          nb * (BN / 64));
+            else
+              tma_load_2d(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM, &map_b, &full[s], kb * KSTAGE + j * TC_BK, nb * BN);
           }
         }
       }
@@ -336,6 +343,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -350,7 +359,10 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
           tma_load_2d_pair(sA + s * Cfg::A_BYTES, &map_a, &full[s], kb * TC_BK, arow);
-          tma_load_2d_pair(sB + s * Cfg::B_BYTES, &map_b, &full[s], kb * TC_BK, brow);
+          if (ea.b_tiled)
+            tma_load_4d_pair(sB + s * Cfg::B_BYTES, &map_b, &full[s], 0, 0, kb, brow / 64);
+          else
+            tma_load_2d_pair(sB + s * Cfg::B_BYTES, &map_b, &full[s], kb * TC_BK, brow);
         }
       }
     }
@@ -414,6 +426,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 // deterministic split-K reduction: C = epi(sum_s partial[s]) in split order
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M, int N,
                                      void* __restrict__ C, int64_t ldc, int epi, int out_dtype) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total4 = (int64_t)M * N / 4;
   const int64_t mn = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -477,6 +491,25 @@ int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, 
   return QCF_OK;
 }
 
+// B operand map: row-major [n][k] (2D) or tile-major [n/64][k/64][64][64] (4D),
+// box of `box_rows` rows x 64 k
+static int make_b_map(CUtensorMap* map, const void* ptr, int64_t n, int64_t k, int64_t ld, int box_rows,
+                      int tiled) {
+  if (!tiled) return make_kmajor_map(map, ptr, n, k, ld, box_rows);
+  EncodeTiledFn enc = get_encode();
+  QCF_REQUIRE(enc, QCF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  QCF_REQUIRE(n % 64 == 0 && k % 64 == 0 && box_rows % 64 == 0, QCF_EUNSUPPORTED, "tiled B needs n, k % 64 == 0");
+  cuuint64_t dims[4] = {64, 64, (cuuint64_t)(k / 64), (cuuint64_t)(n / 64)};
+  cuuint64_t strides[3] = {128, 8192, (cuuint64_t)(k / 64) * 8192};
+  cuuint32_t box[4] = {64, 64, 1, (cuuint32_t)(box_rows / 64)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  QCF_REQUIRE(r == CUDA_SUCCESS, QCF_ECUDA, "cuTensorMapEncodeTiled(4D) failed (%d)", (int)r);
+  return QCF_OK;
+}
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -495,7 +528,7 @@ static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c,
   const int epi = ea.kind, out_dtype = ea.out_dtype;
   using Cfg = TcCfg<BN, SKINNY>;
   CUtensorMap mb;
-  int st = make_kmajor_map(&mb, b, n, k, ldb, BN);
+  int st = make_b_map(&mb, b, n, k, ldb, BN, ea.b_tiled);
   if (st != QCF_OK) return st;
   static bool attr_set = false;
   if (!attr_set) {
@@ -506,13 +539,13 @@ static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c,
   }
   const int64_t work = ((m + TC_BM - 1) / TC_BM) * ((n + BN - 1) / BN) * splits;
   const int grid = (int)std::min<int64_t>(work, sm_count());
-  gemm_tc_kernel<BN, SKINNY><<<grid, TC_THREADS, Cfg::SMEM, s>>>(ma, mb, c, ldc, (int)m, (int)n, (int)k, ea,
+  QCF_LAUNCH("gemm_tc_kernel", gemm_tc_kernel<BN, SKINNY>, dim3(grid), dim3(TC_THREADS), Cfg::SMEM, s, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea,
                                                                  splits, a_box_rows, partial);
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05)");
   if (splits > 1) {
     const int64_t total4 = m * n / 4;
     const int rg = (int)std::min<int64_t>((total4 + 255) / 256, 4 * sm_count());
-    splitk_reduce_kernel<<<rg, 256, 0, s>>>(partial, splits, (int)m, (int)n, c, ldc, epi, out_dtype);
+    QCF_LAUNCH("splitk_reduce_kernel", splitk_reduce_kernel, dim3(rg), dim3(256), 0, s, partial, splits, (int)m, (int)n, c, ldc, epi, out_dtype);
     QCF_LAUNCH_CHECK("qcf_gemm(split-k reduce)");
   }
   return QCF_OK;
@@ -522,7 +555,7 @@ template <int BN>
 static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                        int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
   CUtensorMap mb;
-  int st = make_kmajor_map(&mb, b, n, k, ldb, BN / 2);
+  int st = make_b_map(&mb, b, n, k, ldb, BN / 2, ea.b_tiled);
   if (st != QCF_OK) return st;
   static bool attr_set = false;
   if (!attr_set) {
@@ -538,13 +571,15 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = Tc2Cfg<BN>::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 pair)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 pair)");
@@ -569,7 +604,8 @@ size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k) {
 }
 
 int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                   int64_t n, int64_t k, int epilogue, int out_dtype, void* ws, size_t ws_bytes, cudaStream_t s) {
+                   int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout, void* ws, size_t ws_bytes,
+                   cudaStream_t s) {
   const int sp = skinny_splits(m, n, k);
   if (sp <= 1 || ws_bytes < gemm_workspace_bytes(m, n, k) || (n % 4) || ((uintptr_t)ws & 15)) return QCF_EUNSUPPORTED;
   if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
@@ -578,23 +614,25 @@ int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void*
   CUtensorMap ma;
   int st = make_kmajor_map(&ma, a, m, k, lda, box);
   if (st != QCF_OK) return st;
-  return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype}, s, sp, box, (float*)ws);
+  return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s, sp, box,
+                             (float*)ws);
 }
 
 static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
                              int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s);
 
 int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                   int64_t n, int64_t k, int epilogue, int out_dtype, cudaStream_t s) {
-  return gemm_tc_launch_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype}, s);
+                   int64_t n, int64_t k, int epilogue, int out_dtype, cudaStream_t s, int b_layout) {
+  return gemm_tc_launch_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s);
 }
 
 int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k, int h,
                          int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
-                         const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s) {
+                         const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
+                         int b_layout) {
   if (d % 32 || m <= 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
   if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab) & 15) return QCF_EUNSUPPORTED;
-  EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
+  EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
   return gemm_tc_launch_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, s);

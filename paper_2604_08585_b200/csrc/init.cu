@@ -23,6 +23,8 @@ __device__ __forceinline__ float draw_weight(uint64_t seed, uint64_t step) {
 template <typename T>
 __global__ void init_uniform_kernel(uint64_t seed, uint64_t start, int64_t rows, int64_t cols,
                                     int transpose, T* __restrict__ out, int64_t ld) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -57,9 +59,9 @@ extern "C" int qcf_init_uniform(uint64_t seed, uint64_t start, int64_t rows, int
   QCF_REQUIRE(grid.y <= 65535, QCF_EUNSUPPORTED, "qcf_init_uniform: too many rows");
   auto s = qcf::as_stream(stream);
   if (out_dtype == QCF_F32)
-    qcf::init_uniform_kernel<float><<<grid, block, 0, s>>>(seed, start, rows, cols, transpose, (float*)out, ld_out);
+    QCF_LAUNCH("init_uniform_kernel", qcf::init_uniform_kernel<float>, dim3(grid), dim3(block), 0, s, seed, start, rows, cols, transpose, (float*)out, ld_out);
   else if (out_dtype == QCF_BF16)
-    qcf::init_uniform_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(seed, start, rows, cols, transpose, (__nv_bfloat16*)out, ld_out);
+    QCF_LAUNCH("init_uniform_kernel", qcf::init_uniform_kernel<__nv_bfloat16>, dim3(grid), dim3(block), 0, s, seed, start, rows, cols, transpose, (__nv_bfloat16*)out, ld_out);
   else
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_init_uniform: bad dtype %d", out_dtype);
   QCF_LAUNCH_CHECK("qcf_init_uniform");

@@ -10,6 +10,8 @@ namespace qcf {
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ rows,
                              int32_t row_base, int64_t m, const float* __restrict__ emb, int d,
                              float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x;
   if (i >= m) return;
   const int tok = rows ? tokens[rows[i] - row_base] : tokens[i];
@@ -70,6 +72,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict
                                                                int64_t m, int d, const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps,
                                                                T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[LN_THREADS / 32];
   const int64_t row = blockIdx.x;
   float4* xr = reinterpret_cast<float4*>(x + row * d);
@@ -128,6 +132,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(float* __r
                                                                       int d, const float* __restrict__ g,
                                                                       const float* __restrict__ b, float eps,
                                                                       T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[LN_THREADS / 32];
   float* xr = x + (int64_t)blockIdx.x * d;
   if (delta) {
@@ -146,6 +152,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_scalar_kernel(float* __r
 }
 
 __global__ void add_rows_kernel(float* __restrict__ x, const float* __restrict__ delta, int64_t n4) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(x)[i];
     const float4 t = reinterpret_cast<const float4*>(delta)[i];
@@ -164,6 +172,8 @@ __global__ void __launch_bounds__(LM_THREADS) lm_head_kernel(const float* __rest
                                                              const float* __restrict__ b, float eps,
                                                              const float* __restrict__ emb, int vocab,
                                                              float* __restrict__ logits) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float xs[];
   __shared__ float red[8];
   const int r = blockIdx.y;
@@ -211,6 +221,8 @@ __global__ void __launch_bounds__(LM_THREADS) lm_head_kernel(const float* __rest
 template <typename T>
 __global__ void key_norms_kernel(const T* __restrict__ k, int64_t n, int hkv, int d,
                                  float* __restrict__ norms) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (row >= n) return;
@@ -237,7 +249,7 @@ int qcf_embed(const int32_t* tokens, const int32_t* rows, int32_t row_base, int6
   QCF_REQUIRE(tokens && emb && x && d > 0 && m >= 0, QCF_EINVAL, "qcf_embed: bad args");
   if (m == 0) return QCF_OK;
   QCF_REQUIRE(m <= 0x7fffffff, QCF_EUNSUPPORTED, "qcf_embed: too many rows");
-  qcf::embed_kernel<<<(unsigned)m, 256, 0, qcf::as_stream(stream)>>>(tokens, rows, row_base, m, emb, d, x);
+  QCF_LAUNCH("embed_kernel", qcf::embed_kernel, dim3((unsigned)m), dim3(256), 0, qcf::as_stream(stream), tokens, rows, row_base, m, emb, d, x);
   QCF_LAUNCH_CHECK("qcf_embed");
   return QCF_OK;
 }
@@ -256,7 +268,7 @@ int qcf_add_rows(float* x, const float* delta, int64_t n, qcf_stream_t stream) {
   if (n == 0) return QCF_OK;
   const int64_t n4 = n / 4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
-  qcf::add_rows_kernel<<<grid, 256, 0, qcf::as_stream(stream)>>>(x, delta, n4);
+  QCF_LAUNCH("add_rows_kernel", qcf::add_rows_kernel, dim3(grid), dim3(256), 0, qcf::as_stream(stream), x, delta, n4);
   QCF_LAUNCH_CHECK("qcf_add_rows");
   return QCF_OK;
 }
@@ -272,11 +284,11 @@ int qcf_add_layernorm(float* x, const float* delta, int64_t m, int d, const floa
                    !(((uintptr_t)x | (uintptr_t)g | (uintptr_t)b | (uintptr_t)out | (uintptr_t)delta) & 15) &&
                    (out_dtype == QCF_F32 || d % 8 == 0);
   if (out_dtype == QCF_F32) {
-    if (vec) qcf::layernorm_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (float*)out);
-    else qcf::layernorm_scalar_kernel<float><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (float*)out);
+    if (vec) QCF_LAUNCH("layernorm_kernel", qcf::layernorm_kernel<float>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (float*)out);
+    else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<float>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (float*)out);
   } else if (out_dtype == QCF_BF16) {
-    if (vec) qcf::layernorm_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
-    else qcf::layernorm_scalar_kernel<__nv_bfloat16><<<grid, qcf::LN_THREADS, 0, s>>>(x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
+    if (vec) QCF_LAUNCH("layernorm_kernel", qcf::layernorm_kernel<__nv_bfloat16>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
+    else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<__nv_bfloat16>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
   } else {
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_layernorm: bad dtype");
   }
@@ -296,7 +308,7 @@ int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d, cons
     if (e != cudaSuccess) return qcf::cuda_status(e, "qcf_lm_head attr");
   }
   dim3 grid((unsigned)((vocab + qcf::LM_VT - 1) / qcf::LM_VT), (unsigned)n_rows);
-  qcf::lm_head_kernel<<<grid, qcf::LM_THREADS, smem, qcf::as_stream(stream)>>>(x, rows, d, g, b, eps, emb, vocab, logits);
+  QCF_LAUNCH("lm_head_kernel", qcf::lm_head_kernel, dim3(grid), dim3(qcf::LM_THREADS), smem, qcf::as_stream(stream), x, rows, d, g, b, eps, emb, vocab, logits);
   QCF_LAUNCH_CHECK("qcf_lm_head");
   return QCF_OK;
 }
@@ -308,9 +320,9 @@ int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dt
   auto s = qcf::as_stream(stream);
   unsigned grid = (unsigned)((n + 7) / 8);
   if (dtype == QCF_F32)
-    qcf::key_norms_kernel<float><<<grid, 256, 0, s>>>((const float*)k, n, hkv, d, norms);
+    QCF_LAUNCH("key_norms_kernel", qcf::key_norms_kernel<float>, dim3(grid), dim3(256), 0, s, (const float*)k, n, hkv, d, norms);
   else
-    qcf::key_norms_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)k, n, hkv, d, norms);
+    QCF_LAUNCH("key_norms_kernel", qcf::key_norms_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)k, n, hkv, d, norms);
   QCF_LAUNCH_CHECK("qcf_key_norms");
   return QCF_OK;
 }

@@ -14,6 +14,8 @@ __global__ void rope_qkv_scatter_kernel(const float* __restrict__ qkv, int64_t m
                                         const double* __restrict__ ctab,
                                         const double* __restrict__ stab, T* __restrict__ q_out,
                                         T* __restrict__ k_tab, T* __restrict__ v_tab) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x;
   if (i >= m) return;
   const int half = d / 2;
@@ -60,10 +62,10 @@ extern "C" int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv,
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
   if (dtype == QCF_F32)
-    qcf::rope_qkv_scatter_kernel<float, true><<<(unsigned)m, 256, 0, s>>>(qkv, m, h, hkv, d, pos,
+    QCF_LAUNCH("rope_qkv_scatter_kernel", qcf::rope_qkv_scatter_kernel<float, true>, dim3((unsigned)m), dim3(256), 0, s, qkv, m, h, hkv, d, pos,
         dst_rows, cos_tbl, sin_tbl, (float*)q_out, (float*)k_tab, (float*)v_tab);
   else if (dtype == QCF_BF16)
-    qcf::rope_qkv_scatter_kernel<__nv_bfloat16, false><<<(unsigned)m, 256, 0, s>>>(qkv, m, h, hkv, d,
+    QCF_LAUNCH("rope_qkv_scatter_kernel", qcf::rope_qkv_scatter_kernel<__nv_bfloat16, false>, dim3((unsigned)m), dim3(256), 0, s, qkv, m, h, hkv, d,
         pos, dst_rows, cos_tbl, sin_tbl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_tab,
         (__nv_bfloat16*)v_tab);
   else

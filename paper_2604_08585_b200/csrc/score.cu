@@ -10,42 +10,66 @@
 
 namespace qcf {
 
-constexpr int SC_TILE = 64;
+constexpr int SC_TILE = 64;  // keys per CTA
+constexpr int SC_TQ = 32;    // query rows per CTA (4 x 8 register-tiled)
 
+// logits S[h][t][n] = (q[t,h] . k[n,h]) * scale for a 64-key x 32-row tile of one
+// head; each of 128 threads owns a 4 (rows) x 4 (keys) register tile, operands
+// staged transposed in shared memory so a k-step is 2 vector loads for 16 FMAs.
 template <typename T, typename Acc>
-__global__ void __launch_bounds__(256) score_logits_kernel(const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__(128) score_logits_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                            int64_t n_ctx, int nq, int t0, int h,
                                                            int hkv, int d, Acc scale,
                                                            Acc* __restrict__ S) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
-  Acc* Qs = reinterpret_cast<Acc*>(smraw);          // [nt][d]
+  Acc* Qs = reinterpret_cast<Acc*>(smraw);      // [d][SC_TQ]
+  Acc* Ks = Qs + (size_t)d * SC_TQ;             // [d][SC_TILE]
   const int nt = nq - t0;
-  Acc* Ks = Qs + nt * d;                             // [SC_TILE][d+1]
   const int head = blockIdx.y, kvh = head / (h / hkv);
   const int64_t n0 = (int64_t)blockIdx.x * SC_TILE;
-  for (int e = threadIdx.x; e < nt * d; e += blockDim.x) {
-    int t = e / d, c = e % d;
-    Qs[e] = (Acc)to_f<T>(q[((int64_t)(t0 + t) * h + head) * d + c]);
+  const int tq0 = blockIdx.z * SC_TQ;
+  for (int e = threadIdx.x; e < SC_TQ * d; e += blockDim.x) {
+    const int t = e / d, c = e % d;
+    Qs[c * SC_TQ + t] = (tq0 + t < nt) ? (Acc)to_f<T>(q[((int64_t)(t0 + tq0 + t) * h + head) * d + c]) : (Acc)0;
   }
   for (int e = threadIdx.x; e < SC_TILE * d; e += blockDim.x) {
-    int j = e / d, c = e % d;
-    int64_t n = n0 + j;
-    Ks[j * (d + 1) + c] = n < n_ctx ? (Acc)to_f<T>(k[(n * hkv + kvh) * d + c]) : (Acc)0;
+    const int j = e / d, c = e % d;
+    const int64_t n = n0 + j;
+    Ks[c * SC_TILE + j] = n < n_ctx ? (Acc)to_f<T>(k[(n * hkv + kvh) * d + c]) : (Acc)0;
   }
   __syncthreads();
-  for (int p = threadIdx.x; p < nt * SC_TILE; p += blockDim.x) {
-    const int t = p / SC_TILE, j = p % SC_TILE;
-    const int64_t n = n0 + j;
-    if (n >= n_ctx) continue;
-    Acc acc = 0;
-    for (int c = 0; c < d; ++c) acc += Qs[t * d + c] * Ks[j * (d + 1) + c];
-    S[((int64_t)head * nt + t) * n_ctx + n] = acc * scale;
+  const int tj = threadIdx.x & 15, tt = threadIdx.x >> 4;   // 16 key quads x 8 row quads
+  Acc acc[4][4] = {};
+  for (int c = 0; c < d; ++c) {
+    Acc qv[4], kv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qv[i] = Qs[c * SC_TQ + tt * 4 + i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) kv[j] = Ks[c * SC_TILE + tj * 4 + j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] += qv[i] * kv[j];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = tq0 + tt * 4 + i;
+    if (t >= nt) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tj * 4 + j;
+      if (n < n_ctx) S[((int64_t)head * nt + t) * n_ctx + n] = acc[i][j] * scale;
+    }
   }
 }
 
 template <typename Acc>
 __global__ void score_rowstats_kernel(const Acc* __restrict__ S, int64_t n_ctx, Acc* __restrict__ rmax,
                                       Acc* __restrict__ rsum) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ Acc red[32];
   const int64_t r = blockIdx.x;
   const Acc* s = S + r * n_ctx;
@@ -81,6 +105,8 @@ __global__ void __launch_bounds__(256) score_colmean_kernel(const Acc* __restric
                                                             const Acc* __restrict__ rmax,
                                                             const Acc* __restrict__ rsum,
                                                             float* __restrict__ scores) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ Acc part[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n = (int64_t)blockIdx.x * 32 + lane;
@@ -108,20 +134,20 @@ static int score_impl(const void* q, const void* k, int64_t n_ctx, int nq, int h
   Acc* S = reinterpret_cast<Acc*>(ws);
   Acc* rmax = S + (int64_t)rows * n_ctx;
   Acc* rsum = rmax + rows;
-  const size_t smem = sizeof(Acc) * ((size_t)nt * d + (size_t)SC_TILE * (d + 1));
+  const size_t smem = sizeof(Acc) * (size_t)d * (SC_TQ + SC_TILE);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(score_logits_kernel<T, Acc>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "qcf_score attr");
   }
-  QCF_REQUIRE(smem <= 220 * 1024, QCF_EUNSUPPORTED, "qcf_score: query too long for one tile");
-  dim3 g1(ceil_div(n_ctx, SC_TILE), h);
-  score_logits_kernel<T, Acc><<<g1, 256, smem, s>>>((const T*)q, (const T*)k, n_ctx, nq, t0, h, hkv,
+  QCF_REQUIRE(smem <= 220 * 1024, QCF_EUNSUPPORTED, "qcf_score: head dim too large");
+  dim3 g1(ceil_div(n_ctx, SC_TILE), h, ceil_div(nt, SC_TQ));
+  QCF_LAUNCH("score_logits_kernel", score_logits_kernel<T, Acc>, dim3(g1), dim3(128), smem, s, (const T*)q, (const T*)k, n_ctx, nq, t0, h, hkv,
                                                     d, (Acc)scale, S);
   QCF_LAUNCH_CHECK("qcf_score logits");
-  score_rowstats_kernel<Acc><<<rows, 256, 0, s>>>(S, n_ctx, rmax, rsum);
+  QCF_LAUNCH("score_rowstats_kernel", score_rowstats_kernel<Acc>, dim3(rows), dim3(256), 0, s, S, n_ctx, rmax, rsum);
   QCF_LAUNCH_CHECK("qcf_score rowstats");
-  score_colmean_kernel<Acc><<<ceil_div(n_ctx, 32), 256, 0, s>>>(S, n_ctx, rows, rmax, rsum, scores);
+  QCF_LAUNCH("score_colmean_kernel", score_colmean_kernel<Acc>, dim3(ceil_div(n_ctx, 32)), dim3(256), 0, s, S, n_ctx, rows, rmax, rsum, scores);
   QCF_LAUNCH_CHECK("qcf_score colmean");
   return QCF_OK;
 }

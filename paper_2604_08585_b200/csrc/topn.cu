@@ -45,6 +45,8 @@ __device__ __forceinline__ int block_scan_incl(int v, int* warp_tot, int& total)
 __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restrict__ scores, int64_t n,
                                                           int64_t n_sel, int32_t base,
                                                           int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int hist[256];
   __shared__ int warp_tot[32];
   __shared__ uint32_t s_prefix;
@@ -103,7 +105,7 @@ extern "C" int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t b
   QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
   QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
   if (n_sel == 0) return QCF_OK;
-  qcf::topn_kernel<<<1, qcf::TN_THREADS, 0, qcf::as_stream(stream)>>>(scores, n, n_sel, base, idx_out);
+  QCF_LAUNCH("topn_kernel", qcf::topn_kernel, dim3(1), dim3(qcf::TN_THREADS), 0, qcf::as_stream(stream), scores, n, n_sel, base, idx_out);
   QCF_LAUNCH_CHECK("qcf_topn");
   return QCF_OK;
 }

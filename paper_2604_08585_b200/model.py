@@ -144,6 +144,7 @@ class ModelWeights:
     ln_f_gain: torch.Tensor
     ln_f_bias: torch.Tensor
     device: torch.device = field(default_factory=lambda: torch.device("cuda"))
+    b_layout: int = _lib.B_ROWMAJOR   # projection weights tile-major (B_TILE64) in bf16 mode
 
     @property
     def qcf_dtype(self) -> int:
@@ -178,7 +179,35 @@ class ModelWeights:
                                   t(_get(lw, "ln2_bias", "ln2_b"), torch.float32)))
         d = config.d_model
         ones = torch.ones(d, dtype=torch.float32, device=dev)
-        return cls(config, dtype, t(token_embedding, torch.float32), dl, ones, torch.zeros_like(ones), dev)
+        tiled = use_tiled_weights(config, dtype)
+        _tile_layers(dl, tiled)
+        return cls(config, dtype, t(token_embedding, torch.float32), dl, ones, torch.zeros_like(ones), dev,
+                   _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR)
+
+
+def tile64(w: torch.Tensor) -> torch.Tensor:
+    """[N][K] -> tile-major [N/64][K/64][64][64] (QCF_B_TILE64, include/qcfuse_b200.h)."""
+    n, k = w.shape
+    return w.view(n // 64, 64, k // 64, 64).permute(0, 2, 1, 3).contiguous().view(n, k)
+
+
+def untile64(w: torch.Tensor) -> torch.Tensor:
+    n, k = w.shape
+    return w.view(n // 64, k // 64, 64, 64).permute(0, 2, 1, 3).contiguous().view(n, k)
+
+
+def use_tiled_weights(config: ModelConfig, dtype: str) -> bool:
+    """bf16 on a tcgen05 device with every projection dim a multiple of 64."""
+    if dtype != "bf16" or not torch.cuda.is_available() or not _lib.lib.qcf_tc_available():
+        return False
+    return all(x % 64 == 0 for x in (config.d_model, config.d_ff, config.n_heads * config.d_head))
+
+
+def _tile_layers(layers: list, on: bool) -> None:
+    if not on:
+        return
+    for lw in layers:
+        lw.wqkv, lw.wo, lw.w1, lw.w2 = tile64(lw.wqkv), tile64(lw.wo), tile64(lw.w1), tile64(lw.w2)
 
 
 def _get(obj, *names):
@@ -202,6 +231,7 @@ def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
     call("qcf_init_uniform", seed, 0, V, d, 0, QCF_F32, emb.data_ptr(), d, s)
     off = V * d
     n_build = config.n_layers if layers is None else layers
+    tiled = use_tiled_weights(config, dtype)
     dl = []
     for _ in range(n_build):
         wqkv = torch.empty(3 * d, d, dtype=tdt, device=dev)
@@ -220,9 +250,12 @@ def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
         off += f * d
         ones = torch.ones(d, dtype=torch.float32, device=dev)
         zeros = torch.zeros(d, dtype=torch.float32, device=dev)
-        dl.append(DeviceLayer(wqkv, wo, w1, w2, ones, zeros, ones.clone(), zeros.clone()))
+        layer = DeviceLayer(wqkv, wo, w1, w2, ones, zeros, ones.clone(), zeros.clone())
+        _tile_layers([layer], tiled)
+        dl.append(layer)
     ones = torch.ones(d, dtype=torch.float32, device=dev)
-    return ModelWeights(config, dtype, emb, dl, ones, torch.zeros_like(ones), dev)
+    return ModelWeights(config, dtype, emb, dl, ones, torch.zeros_like(ones), dev,
+                        _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR)
 
 
 class RopeTable:

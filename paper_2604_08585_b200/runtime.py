@@ -96,7 +96,7 @@ class Executor:
     def gemm(self, sc: Scratch, a, lda, b, ldb, c, ldc, m, n, k, epi, out_dt, s) -> None:
         """qcf_gemm_ws: tcgen05 (2-CTA / 1-CTA / split-K skinny) for bf16, FFMA for f32."""
         call("qcf_gemm_ws", self.w.qcf_dtype, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), ldc,
-             m, n, k, epi, out_dt, sc.ws.data_ptr(), sc.ws.numel(), s)
+             m, n, k, epi, out_dt, self.w.b_layout, sc.ws.data_ptr(), sc.ws.numel(), s)
 
     def layer(self, li: int, sc: Scratch, m: int, pos: torch.Tensor, dst: torch.Tensor,
               kmax: torch.Tensor, tab_k: torch.Tensor, tab_v: torch.Tensor,
@@ -115,7 +115,7 @@ class Executor:
         qdst = q_out if q_out is not None else sc.q
         if self.fused_qkv and m > 32:
             # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue
-            call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, m, d, H, Hkv, D,
+            call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, self.w.b_layout, m, d, H, Hkv, D,
                  pos.data_ptr(), dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(),
                  self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), s)
         else:

@@ -279,7 +279,7 @@ def test_gemm_skinny_splitk_deterministic(L, m, n, k, epi):
     for _ in range(2):
         c = c0.clone() if epi == 2 else torch.empty(m, n, device="cuda",
                                                      dtype=torch.bfloat16 if epi == 1 else torch.float32)
-        L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c), n, m, n, k, epi, out_dt, p(ws), ws.numel(), S())
+        L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c), n, m, n, k, epi, out_dt, 0, p(ws), ws.numel(), S())
         outs.append(c)
     ref = a.float() @ b.float().T
     if epi == 1:
@@ -307,7 +307,7 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads):
     q1 = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
     k1 = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
     v1 = torch.zeros_like(k1)
-    L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
+    L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
            rope.n_pos, p(q1), p(k1), p(v1), S())
     qkv = torch.empty(m, N, device="cuda")
     L.call("qcf_gemm", L.QCF_BF16, p(a), K, p(w), K, p(qkv), N, m, N, K, 0, L.QCF_F32, S())
@@ -317,3 +317,25 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads):
     for x, y in ((q1, q2), (k1, k2), (v1, v2)):
         assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
     assert torch.equal(v1, v2)
+
+
+@pytest.mark.parametrize("m,n,k,epi", [(800, 12288, 4096, 0), (800, 4096, 14336, 0), (800, 14336, 4096, 1),
+                                       (32, 12288, 4096, 0), (32, 4096, 14336, 0), (128, 4096, 4096, 0),
+                                       (1536, 4096, 1024, 0), (5153, 12288, 256, 0)])
+def test_gemm_tile_major_weights_match_row_major(L, m, n, k, epi):
+    """QCF_B_TILE64 weights (8 KB contiguous 64x64 tiles, 4D TMA) give the same
+    result as the row-major path for every kernel variant (1-CTA, 2-CTA, skinny)."""
+    from paper_2604_08585_b200.model import tile64, untile64
+    torch.manual_seed(n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bt = tile64(b)
+    assert torch.equal(untile64(bt), b)
+    out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
+    tdt = torch.bfloat16 if epi == 1 else torch.float32
+    ws = torch.empty(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    c1 = torch.empty(m, n, device="cuda", dtype=tdt)
+    c2 = torch.empty(m, n, device="cuda", dtype=tdt)
+    L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c1), n, m, n, k, epi, out_dt, 0, p(ws), ws.numel(), S())
+    L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(bt), k, p(c2), n, m, n, k, epi, out_dt, 1, p(ws), ws.numel(), S())
+    assert torch.equal(c1, c2)

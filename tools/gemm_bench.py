@@ -3,7 +3,10 @@ import sys, json
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
+import os
 from paper_2604_08585_b200 import _lib
+from paper_2604_08585_b200.model import tile64
+LAY = int(os.environ.get("QCF_TILED", "1"))  # 1 = tile-major weights (production layout)
 
 SHAPES = [  # (m, n, k, epi, name)
     (800, 12288, 4096, 0, "qkv M=800"), (800, 4096, 4096, 2, "wo M=800"),
@@ -17,10 +20,11 @@ s = torch.cuda.current_stream().cuda_stream
 for m, n, k, epi, name in SHAPES:
     a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
     b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    b = tile64(b) if LAY else b
     out_dt = _lib.QCF_BF16 if epi == 1 else _lib.QCF_F32
     c = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16 if epi == 1 else torch.float32)
     ws = torch.empty(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
-    f = lambda: _lib.call("qcf_gemm_ws", _lib.QCF_BF16, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, epi, out_dt, ws.data_ptr(), ws.numel(), s)
+    f = lambda: _lib.call("qcf_gemm_ws", _lib.QCF_BF16, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, epi, out_dt, LAY, ws.data_ptr(), ws.numel(), s)
     for _ in range(3): f()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,7 +36,7 @@ for m, n, k, epi, name in SHAPES:
         sc = side.cuda_stream
         for _ in range(it):
             _lib.call("qcf_gemm_ws", _lib.QCF_BF16, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, epi,
-                      out_dt, ws.data_ptr(), ws.numel(), sc)
+                      out_dt, LAY, ws.data_ptr(), ws.numel(), sc)
     g.replay(); torch.cuda.synchronize()
     e0.record()
     g.replay()
