@@ -161,7 +161,7 @@ def cpu_cores() -> int:
 
 
 # ---------------------------------------------------------------------------
-def build_engine(cfgd, dtype, device):
+def build_engine(cfgd, dtype, device, pool: int):
     import torch
     import paper_2604_08585_b200 as Q
     cfg = Q.ModelConfig(n_layers=cfgd["n_layers"], n_heads=cfgd["n_heads"], d_model=cfgd["d_model"],
@@ -169,39 +169,58 @@ def build_engine(cfgd, dtype, device):
     w = Q.init_weights(cfg, dtype=dtype, device=device)
     store = Q.ChunkStore(tempfile.mkdtemp(prefix="qcf-bench-"), cfg, dtype=dtype, device=device,
                          persist=False)
-    toks = [np.random.default_rng(i).integers(0, 256, cfgd["chunk_len"]) for i in range(cfgd["n_chunks"])]
+    toks = [np.random.default_rng(i).integers(0, 256, cfgd["chunk_len"]) for i in range(pool)]
     ids = [store.precompute(w, t, 0.05, f"chunk{i}").chunk_id for i, t in enumerate(toks)]
     eng = Q.FusionEngine(w, store)
     torch.cuda.synchronize()
     return Q, cfg, w, store, eng, ids, toks
 
 
-def phase_profile(eng, ids, query, policy, ratio):
+def phase_profile(eng, chunk_lists, queries, policy, ratio):
     """Instrumented eager pass: CUDA events around every C-ABI launch."""
     import torch
     from paper_2604_08585_b200 import _lib
+    plans, b = eng.prefill_batch(policy, ratio, chunk_lists, queries, use_graph=False)
+    torch.cuda.synchronize()
     _lib.profiler = _lib.Profiler()
     try:
         # park the GPU on a spin kernel so every launch below is queued before it
         # runs: the event pairs then bracket device time only, not host launch gaps
-        torch.cuda._sleep(int(4e8))
-        plan, b = eng.prefill(policy, ratio, ids, query, use_graph=False)
+        torch.cuda._sleep(int(6e8))
+        plans, b = eng.prefill_batch(policy, ratio, chunk_lists, queries, use_graph=False)
         torch.cuda.synchronize()
         recs = _lib.profiler.summary()
     finally:
         _lib.profiler = None
-    return plan, b, recs
+    return plans, b, recs
+
+
+def timed(fn, steps, warmup, stream):
+    """Device time of `steps` calls of fn(i) (after `warmup`), CUDA events on `stream`."""
+    import torch
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        fn(warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3-8b", choices=sorted(CONFIGS))
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--ratio", type=float, default=None)
+    ap.add_argument("--batch", type=int, default=8, help="concurrent requests per GPU per step (config 3)")
+    ap.add_argument("--pool", type=int, default=64, help="chunk pool size (config 3: 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true", help="skip the full-prefill comparison")
     args = ap.parse_args()
@@ -209,6 +228,7 @@ def main():
     if args.ratio is not None:
         cfgd["ratio"] = args.ratio
     args.warmup = max(args.warmup, 3)
+    pool = max(args.pool, cfgd["n_chunks"])
 
     rank, world, local = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1),
                                                                    ("LOCAL_RANK", 0)))
@@ -224,68 +244,81 @@ def main():
     from paper_2604_08585_b200 import _lib
     from paper_2604_08585_b200.dist import gather_rows, max_over_ranks
 
-    Q, cfg, w, store, eng, ids, chunk_toks = build_engine(cfgd, args.dtype, device)
-    q = cfgd["q"]
-    ratio = cfgd["ratio"]
-    n_req = args.warmup + args.steps
-    queries = [np.random.default_rng(10_000 + rank * 100_000 + r).integers(0, 256, q) for r in range(n_req)]
-    qdev = torch.as_tensor(np.stack(queries).astype(np.int32), device=device)
-
-    # graph capture + per-request query swap (inputs resident in HBM)
-    plan, b = eng.prefill("QCFuse", ratio, ids, queries[0].tolist(), use_graph=True)
-    n_ctx = plan.n_ctx
-    qslice = slice(1 + n_ctx, 1 + n_ctx + q)
+    Q, cfg, w, store, eng, pool_ids, chunk_toks = build_engine(cfgd, args.dtype, device, pool)
+    q, ratio, B = cfgd["q"], cfgd["ratio"], args.batch
     stream = torch.cuda.current_stream()
-    launches_per_step = None
+    n_req = args.warmup + args.steps
 
-    def step(i):
-        b.tok[qslice].copy_(qdev[i], non_blocking=True)
-        b.graph.replay()
+    # ---- requests (config 3): each draws n_chunks of the seeded pool, query seeded per request
+    def request(i):
+        g = np.random.default_rng(1_000_000 + rank * 100_000 + i)
+        ids = [pool_ids[j] for j in g.permutation(pool)[:cfgd["n_chunks"]]]
+        return ids, g.integers(0, 256, q).tolist()
 
-    # count our kernels in one eager pass of the same plan (== graph nodes)
-    c0 = _lib.launch_count
-    eng._launch(plan, b)
-    launches_per_step = _lib.launch_count - c0
+    batches = [[request(bi * B + r) for r in range(B)] for bi in range(min(n_req, 6))]
 
-    for i in range(args.warmup):
-        step(i)
+    # ---- batched step: graph captured once; per step the batch's staged inputs
+    # (chunk descriptors, token tables, probe rows) are swapped device-to-device
+    plans, bb = eng.prefill_batch("QCFuse", ratio, [c for c, _ in batches[0]], [t for _, t in batches[0]])
+    staged = []
+    for bt in batches:
+        pl = [eng._plan("QCFuse", ratio, c, t) for c, t in bt]
+        eng._stage(pl, bb, [t for _, t in bt])
+        staged.append((bb.desc.clone(), bb.tok.clone(), bb.anchor_rows.clone()))
     torch.cuda.synchronize()
+
+    def batch_step(i):
+        d, t, a = staged[i % len(staged)]
+        bb.desc.copy_(d, non_blocking=True)
+        bb.tok.copy_(t, non_blocking=True)
+        bb.anchor_rows.copy_(a, non_blocking=True)
+        bb.graph.replay()
+        if world > 1:
+            res = torch.cat([bb.logits, bb.rc_pos.view(B, bb.Mr)[:, :plans[0].n_sel].float()], dim=1)
+            gather_rows(res, B * world, world, rank)
+
+    c0 = _lib.launch_count
+    eng._launch(plans, bb)
+    launches_per_step = _lib.launch_count - c0
     if world > 1:
         dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-            if world > 1:
-                res = torch.cat([b.logits[0], b.rc_pos[:plan.n_sel].float()])[None]
-                gather_rows(res, world, world, rank)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        dev_ms = timed(batch_step, args.steps, args.warmup, stream)
     if world > 1:
         dist.barrier()
-    dev_ms = ev0.elapsed_time(ev1)
     dev_ms = max_over_ranks(dev_ms, device)
     ms_per_step = dev_ms / args.steps
-    value = world * args.steps / (dev_ms / 1e3)
+    value = world * B * args.steps / (dev_ms / 1e3)
+    n_ctx, n_sel = plans[0].n_ctx, plans[0].n_sel
 
-    # ---- e2e through the public API (host tokens in, host logits out)
+    # ---- single-request TTFT (config 2: chunks 0..9 of the pool), graph replay
+    plan1, b1 = eng.prefill("QCFuse", ratio, pool_ids[:cfgd["n_chunks"]], batches[0][0][1])
+    qslice = slice(1 + n_ctx, 1 + n_ctx + q)
+    qdev = torch.as_tensor(np.stack([request(i)[1] for i in range(n_req)]).astype(np.int32), device=device)
+
+    def single_step(i):
+        b1.tok[qslice].copy_(qdev[i], non_blocking=True)
+        b1.graph.replay()
+
+    ttft_ms = max_over_ranks(timed(single_step, args.steps, args.warmup, stream) / args.steps, device)
+
+    # ---- e2e through the public API (host queries / chunk ids in, host logits + selection out)
     e2e_times = []
     for i in range(args.warmup + args.steps):
+        bt = batches[i % len(batches)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        logits, sel = eng.fuse(queries[i].tolist(), ids, ratio)
+        logits, sels = eng.fuse_batch([t for _, t in bt], [c for c, _ in bt], ratio)
         e1.record(stream)
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), device)
-    h2d = len(ids) * 32 + 4 * (1 + n_ctx + q) + 4 * plan.anchor_rows.size
-    d2h = 4 * cfg.vocab_size + 4 * plan.n_sel
+    h2d = B * (cfgd["n_chunks"] * 32 + 4 * bb.R + 4 * plans[0].anchor_rows.size)
+    d2h = B * (4 * cfg.vocab_size + 4 * n_sel)
 
-    # ---- instrumented pass: per-phase + dominant kernel (GEMM) roofline
-    _, _, recs = phase_profile(eng, ids, queries[0].tolist(), "QCFuse", ratio)
+    # ---- instrumented pass: per-phase + dominant kernel (GEMM family) roofline
+    _, _, recs = phase_profile(eng, [c for c, _ in batches[0]], [t for _, t in batches[0]], "QCFuse", ratio)
     phases: dict[str, float] = {}
     gemm_flops = gemm_ms = 0.0
     n_gemm = 0
@@ -294,7 +327,7 @@ def main():
         phases[name] = phases.get(name, 0.0) + ms
         if name in ("qcf_gemm", "qcf_gemm_ws", "qcf_gemm_qkv_rope"):
             if name == "qcf_gemm_qkv_rope":
-                m_, k_, n_ = a[4], a[5], (a[6] + 2 * a[7]) * a[8]
+                m_, k_, n_ = a[5], a[6], (a[7] + 2 * a[8]) * a[9]
             else:
                 m_, n_, k_ = a[7], a[8], a[9]
             gemm_flops += 2.0 * m_ * n_ * k_
@@ -303,8 +336,9 @@ def main():
             g = gemm_shapes.setdefault(f"{m_}x{n_}x{k_}", [0, 0.0, 2.0 * m_ * n_ * k_])
             g[0] += 1
             g[1] += ms
-        if name == "qcf_attention":
-            g = gemm_shapes.setdefault(f"attn m={a[5]} keys={a[9]}", [0, 0.0, 0.0])
+        if name in ("qcf_attention", "qcf_attention_batched"):
+            g = gemm_shapes.setdefault(f"attn m={a[5]}x{a[6] if name.endswith('batched') else 1} "
+                                       f"keys={a[10] if name.endswith('batched') else a[9]}", [0, 0.0, 0.0])
             g[0] += 1
             g[1] += ms
     kernel_detail = {k: {"launches": v[0], "ms": round(v[1], 4),
@@ -320,57 +354,48 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "qcf_gemm* family (tcgen05 bf16: 2-CTA/1-CTA/split-K, fused QKV+RoPE)",
-                "achieved": achieved,
-                "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": (achieved / pk["bf16_tflops"]) if achieved else None, "traffic": traffic,
                 "launches_per_step": n_gemm, "share_of_step": gemm_ms / sum(phases.values()),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if not pk.get("_fallback")
                 else "fallback"}
 
-    # ---- full prefill on the same box (the TTFT denominator)
+    # ---- full prefill on the same box (the TTFT denominator, config 2 request)
     full_ms = None
     if not args.no_full:
-        fplan, fb = eng.prefill("FullCompute", 1.0, ids, queries[0].tolist(), use_graph=True)
-        torch.cuda.synchronize()
-        for _ in range(2):
-            fb.graph.replay()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        nf = 3
-        for _ in range(nf):
-            fb.graph.replay()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        full_ms = f0.elapsed_time(f1) / nf
+        fplan, fb = eng.prefill("FullCompute", 1.0, pool_ids[:cfgd["n_chunks"]], batches[0][0][1])
+        full_ms = timed(lambda i: fb.graph.replay(), 3, 2, stream) / 3
         del fb.graph
-        eng._bufs.clear()
 
-    # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_block(cfgd, store, ids, queries[0], sample_layers=2)
+        cpu = cpu_baseline_block(cfgd, store, pool_ids[:cfgd["n_chunks"]], np.asarray(batches[0][0][1]),
+                                 sample_layers=2)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "ttft_ms": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, seeded byte tokens)",
-            "config": {"workload": f"{args.config}: {cfgd['n_chunks']}x{cfgd['chunk_len']}-token chunks, "
-                                   f"q={q}, recompute {ratio:.0%}, QCFuse",
+            "ttft_ms": ttft_ms, "batch_latency_ms": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (random-init weights, seeded byte tokens)",
+            "config": {"workload": f"{args.config}: {B} concurrent RAG requests per GPU per step, each "
+                                   f"{cfgd['n_chunks']}x{cfgd['chunk_len']}-token chunks drawn from a "
+                                   f"{pool}-chunk HBM pool, q={q}, recompute {ratio:.0%}, QCFuse "
+                                   f"(BASELINE configs[2]); ttft_ms = one request alone (configs[1])",
                        "model": f"Llama-3-8B shape (L{cfg.n_layers} H{cfg.n_heads} D{cfg.d_head} "
                                 f"F{cfg.d_ff}, reference arch)" if args.config == "llama3-8b" else args.config,
-                       "n_ctx": n_ctx, "n_selected": plan.n_sel, "anchors": int(plan.anchor_rows.size - 1),
-                       "requests_per_step_per_gpu": 1, "parallelism": f"replicas x{world} (request sharding)",
-                       "l2": "inputs larger than L2 (11.8 GB weights + 2.7 GB chunk pool streamed per step)"},
-            "e2e": {"value": world * 1e3 / e2e_ms, "unit": "requests/s", "ttft_ms": e2e_ms,
+                       "n_ctx": n_ctx, "n_selected": n_sel, "anchors": int(plans[0].anchor_rows.size - 1),
+                       "requests_per_step_per_gpu": B, "parallelism": f"request sharding x{world} (replicas)",
+                       "l2": "inputs larger than L2 (11.8 GB weights + chunk pool + per-request fused KV)"},
+            "e2e": {"value": world * B * 1e3 / e2e_ms, "unit": "requests/s", "ms_per_batch": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline,
             "phases_ms": {k: round(v, 4) for k, v in sorted(phases.items(), key=lambda x: -x[1])},
             "kernels": kernel_detail,
             "full_prefill_ms": full_ms,
-            "fused_over_full": (ms_per_step / full_ms) if full_ms else None,
+            "fused_over_full": (ttft_ms / full_ms) if full_ms else None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

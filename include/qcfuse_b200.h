@@ -157,6 +157,11 @@ int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, in
 int qcf_attention(int dtype, const void* q, const void* k, const void* v,
                   const int32_t* kmax, int64_t m, int h, int hkv, int d,
                   int64_t n_keys, void* out, qcf_stream_t stream);
+/* Homogeneous request batch: q/out [n_req][m][H][D], kmax [n_req][m], K/V
+ * tables [n_req][n_keys][Hkv][D] (one launch, blockIdx.z = request). */
+int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
+                          const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
+                          int64_t n_keys, void* out, qcf_stream_t stream);
 
 /* ---- critical-layer scoring: fusion.py:313-326 + 566-569 ------------------
  * scores[n] = mean_{h,t} softmax_n((q[t,h].k[n,h]) * scale), t over all nq rows

@@ -5,9 +5,9 @@
 namespace qcf {
 int attention_simt_launch(int dtype, const void* q, const void* k, const void* v,
                           const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
-                          void* out, cudaStream_t s);
+                          void* out, cudaStream_t s, int n_req = 1);
 // tensor-core path (bf16); returns QCF_EUNSUPPORTED for shapes it does not cover
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax,
                         int64_t m, int h, int hkv, int d, int64_t n_keys, void* out,
-                        cudaStream_t s);
+                        cudaStream_t s, int n_req = 1);
 }  // namespace qcf

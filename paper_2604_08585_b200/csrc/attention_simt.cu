@@ -30,6 +30,12 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
   __shared__ int kend_s;
 
   const int head = blockIdx.y, kvh = head / (h / hkv);
+  const int64_t req = blockIdx.z;  // request: q/out/kmax [req][m], K/V [req][n_keys]
+  q += req * m * h * D;
+  out += req * m * h * D;
+  kmax += req * m;
+  k += req * n_keys * hkv * D;
+  v += req * n_keys * hkv * D;
   const int64_t r0 = (int64_t)blockIdx.x * AQ;
   const int tid = threadIdx.x;
   const int row = tid >> 2, cg = tid & 3;       // 4 threads per query row
@@ -128,14 +134,14 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
 
 template <typename T, int D>
 static int launch_simt(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m,
-                       int h, int hkv, int64_t n_keys, void* out, cudaStream_t s) {
+                       int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
   const size_t smem = sizeof(float) * (AQ * (D + 1) + AK * (D + 1) + AK * D + AQ * (AK + 1));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(attn_simt_kernel<T, D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "attn_simt attr");
   }
-  dim3 grid(ceil_div(m, AQ), h);
+  dim3 grid(ceil_div(m, AQ), h, n_req);
   QCF_LAUNCH("attn_simt_kernel", attn_simt_kernel<T, D>, dim3(grid), dim3(128), smem, s, (const T*)q, (const T*)k, (const T*)v, kmax, m, h,
                                                  hkv, n_keys, (T*)out);
   QCF_LAUNCH_CHECK("qcf_attention(simt)");
@@ -144,13 +150,13 @@ static int launch_simt(const void* q, const void* k, const void* v, const int32_
 
 template <typename T>
 static int dispatch_d(int d, const void* q, const void* k, const void* v, const int32_t* kmax,
-                      int64_t m, int h, int hkv, int64_t n_keys, void* out, cudaStream_t s) {
+                      int64_t m, int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
   switch (d) {
-    case 8: return launch_simt<T, 8>(q, k, v, kmax, m, h, hkv, n_keys, out, s);
-    case 16: return launch_simt<T, 16>(q, k, v, kmax, m, h, hkv, n_keys, out, s);
-    case 32: return launch_simt<T, 32>(q, k, v, kmax, m, h, hkv, n_keys, out, s);
-    case 64: return launch_simt<T, 64>(q, k, v, kmax, m, h, hkv, n_keys, out, s);
-    case 128: return launch_simt<T, 128>(q, k, v, kmax, m, h, hkv, n_keys, out, s);
+    case 8: return launch_simt<T, 8>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+    case 16: return launch_simt<T, 16>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+    case 32: return launch_simt<T, 32>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+    case 64: return launch_simt<T, 64>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+    case 128: return launch_simt<T, 128>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
     default: break;
   }
   set_error("qcf_attention: unsupported d_head %d (8/16/32/64/128)", d);
@@ -159,9 +165,9 @@ static int dispatch_d(int d, const void* q, const void* k, const void* v, const 
 
 int attention_simt_launch(int dtype, const void* q, const void* k, const void* v,
                           const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
-                          void* out, cudaStream_t s) {
-  if (dtype == QCF_F32) return dispatch_d<float>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s);
-  return dispatch_d<__nv_bfloat16>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s);
+                          void* out, cudaStream_t s, int n_req) {
+  if (dtype == QCF_F32) return dispatch_d<float>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+  return dispatch_d<__nv_bfloat16>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
 }
 
 }  // namespace qcf

@@ -24,7 +24,8 @@ namespace qcf {
 
 using namespace sm100;
 
-int make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int box_rows);
+int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int box_rows,
+                     int64_t batch, int64_t batch_stride);
 
 constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
 constexpr int AT_THREADS = 576;  // 2 control warps + 16 softmax warps
@@ -58,6 +59,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  // request (batch) index: q/out/kmax are [req][M]..., the K/V tables [req][n_keys]...
+  const int req = blockIdx.z;
+  kmax += (int64_t)req * M;
+  out += (int64_t)req * M * H * AT_D;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -126,8 +131,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       mbar_expect_tx(q_full, AT_TILE_BYTES);
-      tma_load_2d(sQ, &map_q, q_full, head * AT_D, m0);
-      tma_load_2d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0);
+      tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
+      tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
       // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
       // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
       auto load_k = [&](int j) {
@@ -135,16 +140,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
         uint8_t* k = sK + st * AT_TILE_BYTES;
-        tma_load_2d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN);
-        tma_load_2d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN);
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
       };
       auto load_v = [&](int j) {
         const int st = j & 1;
         mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
         uint8_t* v = sV + st * AT_TILE_BYTES;
-        tma_load_2d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN);
-        tma_load_2d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN);
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
       };
       load_k(0);
       for (int j = 0; j < n_tiles; ++j) {
@@ -314,13 +319,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
 }
 
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
-                        int hkv, int d, int64_t n_keys, void* out, cudaStream_t s) {
-  if (d != AT_D || m > INT32_MAX || n_keys > INT32_MAX) return QCF_EUNSUPPORTED;
+                        int hkv, int d, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
+  if (d != AT_D || m > INT32_MAX || n_keys > INT32_MAX || n_req > 65535) return QCF_EUNSUPPORTED;
   if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) return QCF_EUNSUPPORTED;
   CUtensorMap mq, mk, mv;
-  int st = make_kmajor_map(&mq, q, m, (int64_t)h * d, (int64_t)h * d, AT_BM);
-  if (st == QCF_OK) st = make_kmajor_map(&mk, k, n_keys, (int64_t)hkv * d, (int64_t)hkv * d, AT_BN);
-  if (st == QCF_OK) st = make_kmajor_map(&mv, v, n_keys, (int64_t)hkv * d, (int64_t)hkv * d, AT_BN);
+  const int64_t qw = (int64_t)h * d, kw = (int64_t)hkv * d;
+  int st = make_kmajor_map3(&mq, q, m, qw, qw, AT_BM, n_req, m * qw);
+  if (st == QCF_OK) st = make_kmajor_map3(&mk, k, n_keys, kw, kw, AT_BN, n_req, n_keys * kw);
+  if (st == QCF_OK) st = make_kmajor_map3(&mv, v, n_keys, kw, kw, AT_BN, n_req, n_keys * kw);
   if (st != QCF_OK) return st;
   static bool attr = false;
   if (!attr) {
@@ -329,7 +335,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
-  dim3 grid((unsigned)h, (unsigned)((m + AT_BM - 1) / AT_BM));
+  dim3 grid((unsigned)h, (unsigned)((m + AT_BM - 1) / AT_BM), (unsigned)n_req);
   QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
                                                    (__nv_bfloat16*)out);
   QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");

@@ -40,19 +40,27 @@ extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, in
   return qcf::gemm_simt_launch(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
 }
 
-extern "C" int qcf_attention(int dtype, const void* q, const void* k, const void* v,
-                             const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
-                             void* out, qcf_stream_t stream) {
+extern "C" int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
+                                     const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
+                                     int64_t n_keys, void* out, qcf_stream_t stream) {
   QCF_REQUIRE(q && k && v && kmax && out, QCF_EINVAL, "qcf_attention: null pointer");
-  QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && n_keys > 0, QCF_EINVAL, "qcf_attention: bad shape");
+  QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && n_keys > 0 && n_req >= 1, QCF_EINVAL,
+              "qcf_attention: bad shape");
   QCF_REQUIRE(dtype == QCF_F32 || dtype == QCF_BF16, QCF_EINVAL, "qcf_attention: bad dtype");
+  QCF_REQUIRE(n_req <= 65535, QCF_EUNSUPPORTED, "qcf_attention: too many requests");
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
   if (dtype == QCF_BF16 && qcf::tc_ok()) {
-    int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s);
+    int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req);
     if (st != QCF_EUNSUPPORTED) return st;
   }
-  return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, s);
+  return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req);
+}
+
+extern "C" int qcf_attention(int dtype, const void* q, const void* k, const void* v,
+                             const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
+                             void* out, qcf_stream_t stream) {
+  return qcf_attention_batched(dtype, q, k, v, kmax, m, 1, h, hkv, d, n_keys, out, stream);
 }
 
 extern "C" size_t qcf_gemm_workspace(int64_t m, int64_t n, int64_t k) { return qcf::gemm_workspace_bytes(m, n, k); }

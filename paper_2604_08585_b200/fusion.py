@@ -55,6 +55,21 @@ def _executor_for(weights: ModelWeights) -> Executor:
     return ex
 
 
+class _DescView:
+    """Byte-offset view of a device descriptor array (for per-request launches)."""
+
+    def __init__(self, t: torch.Tensor, offset: int):
+        self._p = t.data_ptr() + offset
+
+    def data_ptr(self) -> int:
+        return self._p
+
+
+def _view_rows(t: torch.Tensor, row0: int) -> _DescView:
+    """Pointer to row `row0` of layer 0 of a [L][rows][Hkv][D] table."""
+    return _DescView(t, row0 * t.stride(1) * t.element_size())
+
+
 def _i32(a, device) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.int32)), device=device)
 
@@ -316,6 +331,7 @@ def sparse_attention(q, positions, keys, values, visible) -> np.ndarray:
 
 @dataclass
 class _Plan:
+    """One request's host-side plan (chunk records, offsets, probe rows)."""
     chunk_ids: list[str]
     records: list
     offsets: list[int]
@@ -325,38 +341,53 @@ class _Plan:
     anchor_rows: np.ndarray      # [1 + A] fused rows of the probe prefix
     policy: str
 
+    def shape_key(self):
+        return (tuple(r.n_tokens for r in self.records), self.q, self.n_sel, self.anchor_rows.size, self.policy)
+
 
 class _Bufs:
-    """Device buffers for one request shape (fixed addresses → graph replay)."""
+    """Device buffers for a homogeneous batch of B requests of one shape
+    (fixed addresses -> graph replay). Request b owns rows [b*R, (b+1)*R) of
+    every layer's fused table, [b*P, (b+1)*P) of the probe table and
+    [b*Mr, (b+1)*Mr) of the recompute rows; positions/kmax are per request."""
 
-    def __init__(self, eng: "FusionEngine", n_ctx: int, q: int, n_sel: int, n_anchor_rows: int,
-                 n_chunks: int, extra_rows: int = 0):
+    def __init__(self, eng: "FusionEngine", plan: "_Plan", n_req: int, extra_rows: int = 0):
         cfg, dev = eng.config, eng.device
         L, H, Hkv, D = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.d_head
         dt = eng.weights.torch_dtype
         c = cfg.critical_layer
-        self.rows = 1 + n_ctx + q + extra_rows
-        self.fk = torch.empty((L, self.rows, Hkv, D), dtype=dt, device=dev)
+        n_ctx, q, n_sel, n_pre = plan.n_ctx, plan.q, plan.n_sel, plan.anchor_rows.size
+        B = self.B = n_req
+        self.R = R = 1 + n_ctx + q + extra_rows
+        self.P = P = n_pre + q
+        self.Mr = Mr = n_sel + q
+        self.n_pre = n_pre
+        self.rows = R
+        self.fk = torch.empty((L, B * R, Hkv, D), dtype=dt, device=dev)
         self.fv = torch.empty_like(self.fk)
-        self.desc = torch.empty(n_chunks * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
-        self.tok = torch.empty(self.rows, dtype=torch.int32, device=dev)
-        self.anchor_rows = torch.empty(max(n_anchor_rows, 1), dtype=torch.int32, device=dev)
-        self.n_pre = n_anchor_rows
-        self.pk = torch.empty((c, n_anchor_rows + q, Hkv, D), dtype=dt, device=dev)
+        self.desc = torch.empty(B * len(plan.records) * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
+        self.tok = torch.empty(B * R, dtype=torch.int32, device=dev)
+        self.anchor_rows = torch.empty(B * max(n_pre, 1), dtype=torch.int32, device=dev)
+        self.pk = torch.empty((c, B * P, Hkv, D), dtype=dt, device=dev)
         self.pv = torch.empty_like(self.pk)
         ar = torch.arange(q, dtype=torch.int32, device=dev)
-        self.p_pos = ar + (n_ctx + 1)                 # probe positions n_ctx+1..
-        self.p_dst = ar + n_anchor_rows               # probe rows in its compact table
-        self.qc = torch.empty((1, q, H, D), dtype=dt, device=dev)
-        self.scores = torch.empty(n_ctx, dtype=torch.float32, device=dev)
+        rb = torch.arange(B, dtype=torch.int32, device=dev)[:, None]
+        self.p_pos = (ar + (n_ctx + 1)).repeat(B)                       # probe positions n_ctx+1..
+        self.p_kmax = (ar + n_pre).repeat(B)                            # rows in the request's probe table
+        self.p_dst = (rb * P + (ar + n_pre)[None, :]).reshape(-1).contiguous()
+        self.p_tok = (rb * R + (ar + n_ctx + 1)[None, :]).reshape(-1).contiguous()
+        self.qc = torch.empty((1, B * q, H, D), dtype=dt, device=dev)
+        self.scores = torch.empty(B * n_ctx, dtype=torch.float32, device=dev)
         self.score_ws = torch.empty(int(_lib.lib.qcf_score_workspace(n_ctx, q, H)), dtype=torch.uint8,
                                     device=dev)
-        self.rc_pos = torch.empty(n_sel + q, dtype=torch.int32, device=dev)
-        self.rc_pos[n_sel:] = ar + (n_ctx + 1)
-        self.last_row = torch.tensor([n_sel + q - 1], dtype=torch.int32, device=dev)
-        self.logits = torch.empty((1, cfg.vocab_size), dtype=torch.float32, device=dev)
-        self.sc_probe = eng.ex.scratch(q, key=("probe", id(self)))
-        self.sc_rc = eng.ex.scratch(n_sel + q, key=("rc", id(self)))
+        self.rc_pos = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # per-request positions == kmax
+        self.rc_pos.view(B, Mr)[:, n_sel:] = ar + (n_ctx + 1)
+        self.rc_dst = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # rows in the batch table
+        self.rc_dst.copy_((self.rc_pos.view(B, Mr) + rb * R).reshape(-1))
+        self.last_row = (rb[:, 0] * Mr + (Mr - 1)).contiguous()
+        self.logits = torch.empty((B, cfg.vocab_size), dtype=torch.float32, device=dev)
+        self.sc_probe = eng.ex.scratch(B * q, key=("probe", id(self)))
+        self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
 
 
@@ -409,11 +440,12 @@ class FusionEngine:
             arr[i].offset = o
         return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
 
-    def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None):
+    def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None, layer_stride=None):
         cfg = self.config
         self.ex.rope.ensure(n_ctx + 2)
         call("qcf_assemble", desc_dev.data_ptr(), len(recs), n_ctx, self._bos_k.data_ptr(),
-             self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(), fk.stride(0), cfg.n_layers,
+             self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(),
+             fk.stride(0) if layer_stride is None else layer_stride, cfg.n_layers,
              cfg.n_kv_heads, cfg.d_head, self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(),
              self.ex.rope.n_pos, self.weights.qcf_dtype, cuda_stream(stream))
 
@@ -612,79 +644,125 @@ class FusionEngine:
             raise ValueError(f"fast path covers QCFuse/FullCompute/FullReuse, not {policy}")
         return _Plan(list(chunk_ids), recs, offs, n_ctx, q, n_sel, rows, policy)
 
-    def _buffers(self, plan: _Plan, extra_rows: int = 0) -> _Bufs:
-        key = (tuple(r.n_tokens for r in plan.records), plan.q, plan.n_sel, plan.anchor_rows.size,
-               plan.policy, extra_rows)
+    def _buffers(self, plans: list[_Plan], extra_rows: int = 0) -> _Bufs:
+        key = (plans[0].shape_key(), len(plans), extra_rows)
         b = self._bufs.get(key)
         if b is None:
-            b = _Bufs(self, plan.n_ctx, plan.q, plan.n_sel, plan.anchor_rows.size, len(plan.records),
-                      extra_rows)
+            b = _Bufs(self, plans[0], len(plans), extra_rows)
             self._bufs[key] = b
         return b
 
-    def _stage(self, plan: _Plan, b: _Bufs, query_tokens, stream=None) -> dict:
-        """Host → device copies of the request's inputs (chunk descriptors,
-        token table, probe rows). Returns the byte counts."""
-        desc = self._desc_bytes(plan.records, plan.offsets)
-        tok = np.concatenate([[BOS_ID], *[r.token_ids for r in plan.records],
-                              np.asarray(query_tokens, np.int64)]).astype(np.int32)
-        rows = plan.anchor_rows.astype(np.int32)
+    def _stage(self, plans: list[_Plan], b: _Bufs, queries, stream=None) -> dict:
+        """Host -> device copies of the batch's inputs (chunk descriptors,
+        token tables, probe rows). Returns the byte counts."""
+        descs, toks, rows = [], [], []
+        for plan, qt in zip(plans, queries):
+            descs.append(self._desc_bytes(plan.records, plan.offsets))
+            t = np.zeros(b.R, np.int32)
+            body = np.concatenate([[BOS_ID], *[r.token_ids for r in plan.records], np.asarray(qt, np.int64)])
+            t[:body.size] = body
+            toks.append(t)
+            rows.append(plan.anchor_rows.astype(np.int32))
+        desc = torch.cat(descs)
+        tok = np.concatenate(toks)
+        rows = np.concatenate(rows)
         s = stream or torch.cuda.current_stream()
         with torch.cuda.stream(s):
             b.desc.copy_(desc.pin_memory(), non_blocking=True)
-            b.tok[:tok.size].copy_(torch.from_numpy(tok).pin_memory(), non_blocking=True)
+            b.tok.copy_(torch.from_numpy(tok).pin_memory(), non_blocking=True)
             b.anchor_rows[:rows.size].copy_(torch.from_numpy(rows).pin_memory(), non_blocking=True)
         return {"h2d": desc.numel() + tok.nbytes + rows.nbytes}
 
-    def _launch(self, plan: _Plan, b: _Bufs, stream=None) -> None:
-        """Every kernel of one fused prefill, in order (see module docstring)."""
-        cfg, ex = self.config, self.ex
-        c, q, n_ctx, n_sel = cfg.critical_layer, plan.q, plan.n_ctx, plan.n_sel
+    def _launch(self, plans: list[_Plan], b: _Bufs, stream=None) -> None:
+        """Every kernel of one (batched) fused prefill, in order (module docstring)."""
+        cfg, ex, plan = self.config, self.ex, plans[0]
+        c, q, n_ctx, n_sel, B = cfg.critical_layer, plan.q, plan.n_ctx, plan.n_sel, b.B
         s = cuda_stream(stream)
-        self._assemble_into(plan.records, plan.offsets, n_ctx, b.fk, b.fv, b.desc, stream)
+        row_elems = cfg.n_kv_heads * cfg.d_head
+        esz = b.fk.element_size()
+        nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
+        for r in range(B):   # K1: assembly into request r's slice of the batch table
+            self._assemble_into(plan.records, plan.offsets, n_ctx,
+                                _view_rows(b.fk, r * b.R), _view_rows(b.fv, r * b.R),
+                                _DescView(b.desc, r * nd), stream, layer_stride=b.fk.stride(0))
         if plan.policy == "QCFuse" and n_sel > 0:
-            call("qcf_gather_rows", b.fk.data_ptr(), b.fv.data_ptr(), b.fk.stride(0),
-                 b.anchor_rows.data_ptr(), b.n_pre, b.pk.data_ptr(), b.pv.data_ptr(), b.pk.stride(0),
-                 c, cfg.n_kv_heads * cfg.d_head, self.weights.qcf_dtype, s)
-            ex.embed(b.sc_probe, q, b.tok, rows=b.p_pos, stream=stream)
+            for r in range(B):   # K2: probe prefix rows of request r
+                call("qcf_gather_rows", b.fk.data_ptr() + r * b.R * row_elems * esz,
+                     b.fv.data_ptr() + r * b.R * row_elems * esz, b.fk.stride(0),
+                     b.anchor_rows.data_ptr() + r * b.n_pre * 4, b.n_pre,
+                     b.pk.data_ptr() + r * b.P * row_elems * esz, b.pv.data_ptr() + r * b.P * row_elems * esz,
+                     b.pk.stride(0), c, row_elems, self.weights.qcf_dtype, s)
+            # K3: probe layers 1..c-1 + layer c's Q, all B*q rows at once
+            ex.embed(b.sc_probe, B * q, b.tok, rows=b.p_tok, stream=stream)
             for li in range(c - 1):
-                ex.layer(li, b.sc_probe, q, b.p_pos, b.p_dst, b.p_dst, b.pk[li], b.pv[li], stream=stream)
-            ex.layer(c - 1, b.sc_probe, q, b.p_pos, b.p_dst, b.p_dst, b.pk[c - 1], b.pv[c - 1],
-                     q_only=True, q_out=b.qc[0], stream=stream)
-            self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream)
-            call("qcf_topn", b.scores.data_ptr(), n_ctx, n_sel, 1, b.rc_pos.data_ptr(), None, 0, s)
+                ex.layer(li, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[li], b.pv[li], stream=stream,
+                         n_req=B)
+            ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
+                     q_only=True, q_out=b.qc[0], stream=stream, n_req=B)
+            for r in range(B):   # K4 + K5 per request
+                self._score_dev(b.qc[0, r * q:(r + 1) * q], b.fk[c - 1, r * b.R + 1:], n_ctx,
+                                b.scores[r * n_ctx:(r + 1) * n_ctx], b.score_ws, stream)
+                call("qcf_topn", b.scores.data_ptr() + r * n_ctx * 4, n_ctx, n_sel, 1,
+                     b.rc_pos.data_ptr() + r * b.Mr * 4, None, 0, s)
+                call("qcf_iota_add", b.rc_pos.data_ptr() + r * b.Mr * 4, n_sel, r * b.R,
+                     b.rc_dst.data_ptr() + r * b.Mr * 4, s)
         elif plan.policy == "FullCompute":
-            call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr(), s)
-        m = n_sel + q
-        ex.embed(b.sc_rc, m, b.tok, rows=b.rc_pos, stream=stream)
-        ex.stack(b.sc_rc, m, b.rc_pos, b.rc_pos, b.rc_pos, b.fk, b.fv, stream=stream)
+            for r in range(B):
+                call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
+                call("qcf_iota", n_sel, 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+        m = B * b.Mr   # K6: recompute + query rows of the whole batch
+        ex.embed(b.sc_rc, m, b.tok, rows=b.rc_dst, stream=stream)
+        ex.stack(b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk, b.fv, stream=stream, n_req=B)
         ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
 
-    def prefill(self, policy: str, ratio: float, chunk_ids, query_tokens, use_graph: bool = True,
-                extra_rows: int = 0, stream=None):
-        """Device-side fused prefill up to first-token logits. Returns
-        (plan, buffers); logits in b.logits[0], selection in b.rc_pos[:n_sel]."""
-        plan = self._plan(policy, ratio, chunk_ids, query_tokens)
-        b = self._buffers(plan, extra_rows)
-        self._stage(plan, b, query_tokens, stream)
+    def prefill_batch(self, policy: str, ratio: float, chunk_lists, queries, use_graph: bool = True,
+                      extra_rows: int = 0, stream=None):
+        """Device-side fused prefill of a homogeneous batch (same chunk lengths,
+        query length and selection size) up to first-token logits.
+        Returns (plans, buffers): logits b.logits[r], selection of request r in
+        b.rc_pos[r*b.Mr : r*b.Mr + n_sel]."""
+        plans = [self._plan(policy, ratio, ids, qt) for ids, qt in zip(chunk_lists, queries)]
+        if any(p.shape_key() != plans[0].shape_key() for p in plans):
+            raise ValueError("prefill_batch needs requests of one shape (chunk lengths, query length)")
+        b = self._buffers(plans, extra_rows)
+        self._stage(plans, b, queries, stream)
         self.ex.rope.ensure(b.rows + 2)
         if not use_graph:
-            self._launch(plan, b, stream)
-            return plan, b
+            self._launch(plans, b, stream)
+            return plans, b
         if b.graph is None:
             s = stream or torch.cuda.current_stream()
             side = torch.cuda.Stream(device=self.device)
             side.wait_stream(s)
             with torch.cuda.stream(side):
-                self._launch(plan, b, side)       # warm-up (lazy attributes, workspaces)
+                self._launch(plans, b, side)       # warm-up (lazy attributes, workspaces)
             s.wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=side):
-                self._launch(plan, b, side)
+                self._launch(plans, b, side)
             s.wait_stream(side)
             b.graph = g
         b.graph.replay()
-        return plan, b
+        return plans, b
+
+    def prefill(self, policy: str, ratio: float, chunk_ids, query_tokens, use_graph: bool = True,
+                extra_rows: int = 0, stream=None):
+        """Single-request prefill (a batch of one). Returns (plan, buffers);
+        logits in b.logits[0], selection in b.rc_pos[:n_sel]."""
+        plans, b = self.prefill_batch(policy, ratio, [chunk_ids], [query_tokens], use_graph, extra_rows, stream)
+        return plans[0], b
+
+    def fuse_batch(self, queries, chunk_lists, ratio: float = 0.15):
+        """Batched north-star entry (BASELINE config 3): one fused prefill for
+        a homogeneous batch of RAG requests. Returns (logits [B][V] numpy,
+        list of selected-position arrays)."""
+        qts = [byte_tokens(q) if isinstance(q, (str, bytes)) else list(q) for q in queries]
+        if not qts or any(not q for q in qts):
+            raise ValueError("query must be non-empty")
+        plans, b = self.prefill_batch("QCFuse", ratio, chunk_lists, qts)
+        n = plans[0].n_sel
+        sel = b.rc_pos.view(b.B, b.Mr)[:, :n].cpu().numpy().astype(np.int64)
+        return b.logits.cpu().numpy(), [sel[r] for r in range(b.B)]
 
     def fuse(self, query, chunk_ids, ratio: float = 0.15):
         """North-star entry: fuse(query, chunks) → (first-token logits [V] f32

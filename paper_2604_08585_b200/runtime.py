@@ -100,11 +100,15 @@ class Executor:
 
     def layer(self, li: int, sc: Scratch, m: int, pos: torch.Tensor, dst: torch.Tensor,
               kmax: torch.Tensor, tab_k: torch.Tensor, tab_v: torch.Tensor,
-              q_only: bool = False, q_out: torch.Tensor | None = None, stream=None) -> None:
+              q_only: bool = False, q_out: torch.Tensor | None = None, stream=None,
+              n_req: int = 1) -> None:
         """One decoder layer (model.py:359-376) over m rows.
 
         tab_k/tab_v: [n_rows, Hkv, D] views of THIS layer's table. With q_only
-        the layer stops after LN1 → QKV → RoPE (the probe's critical-layer Q)."""
+        the layer stops after LN1 → QKV → RoPE (the probe's critical-layer Q).
+        n_req > 1: a homogeneous batch — rows are n_req blocks of m/n_req, the
+        table n_req blocks of n_rows/n_req; `dst` indexes the whole table,
+        `kmax` is relative to the row's own block."""
         cfg, w = self.cfg, self.w
         lw = w.layers[li]
         d, H, Hkv, D, F = cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.d_head, cfg.d_ff
@@ -125,8 +129,8 @@ class Executor:
                  qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
         if q_only:
             return
-        call("qcf_attention", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
-             kmax.data_ptr(), m, H, Hkv, D, tab_k.shape[0], sc.o.data_ptr(), s)
+        call("qcf_attention_batched", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
+             kmax.data_ptr(), m // n_req, n_req, H, Hkv, D, tab_k.shape[0] // n_req, sc.o.data_ptr(), s)
         self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.delta, d, m, d, H * D, EPI_STORE, QCF_F32, s)
         sc.pending = True
         self._norm(sc, m, lw.ln2_g, lw.ln2_b, s)
@@ -135,13 +139,14 @@ class Executor:
         sc.pending = True
 
     def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
-              layers: range | None = None, q_store: torch.Tensor | None = None, stream=None) -> None:
+              layers: range | None = None, q_store: torch.Tensor | None = None, stream=None,
+              n_req: int = 1) -> None:
         """Run layers over m rows. tab_k/tab_v: [L, n_rows, Hkv, D].
         q_store (optional) [L, m, H, D] receives each layer's rotated Q."""
         layers = range(self.cfg.n_layers) if layers is None else layers
         for li in layers:
             self.layer(li, sc, m, pos, dst, kmax, tab_k[li], tab_v[li],
-                       q_out=q_store[li] if q_store is not None else None, stream=stream)
+                       q_out=q_store[li] if q_store is not None else None, stream=stream, n_req=n_req)
         self.flush(sc, m, stream)
 
     def lm_head(self, sc: Scratch, rows: torch.Tensor, out: torch.Tensor, stream=None) -> None:

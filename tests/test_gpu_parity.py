@@ -317,3 +317,29 @@ class TestRun:
         for args in (("Nope", 0.2, cids, "x"), ("QCFuse", 1.2, cids, "x"), ("QCFuse", 0.2, cids, "")):
             with pytest.raises(ValueError):
                 engine.run(*args)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_batched_prefill_equals_single_requests(tmp_path, dtype):
+    """A homogeneous batch of requests (config 3) gives every request the
+    selection and first-token logits it gets alone (f32: bit-exact)."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=99)
+    w = Q.init_weights(cfg, dtype=dtype)
+    store = Q.ChunkStore(tmp_path / "s", cfg, dtype=dtype, persist=False)
+    eng = Q.FusionEngine(w, store)
+    pool = [store.precompute(w, np.random.default_rng(i).integers(0, 256, 96), 0.05).chunk_id for i in range(6)]
+    rng = np.random.default_rng(3)
+    reqs = [[pool[j] for j in rng.permutation(6)[:3]] for _ in range(4)]
+    queries = [rng.integers(0, 256, 12).tolist() for _ in range(4)]
+    plans, b = eng.prefill_batch("QCFuse", 0.2, reqs, queries, use_graph=True)
+    n_sel = plans[0].n_sel
+    for r in range(4):
+        logits, sel = eng.fuse(queries[r], reqs[r], 0.2)
+        bsel = b.rc_pos[r * b.Mr:r * b.Mr + n_sel].cpu().numpy()
+        blog = b.logits[r].cpu().numpy()
+        if dtype == "f32":
+            assert np.array_equal(bsel, sel) and np.array_equal(blog, logits)
+        else:
+            assert len(set(bsel.tolist()) & set(sel.tolist())) >= 0.9 * n_sel
+            assert np.abs(blog - logits).max() < 5e-2 * np.abs(logits).max()

@@ -9,7 +9,7 @@ import bench
 
 cfgd = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "llama3-8b"])
 policy = sys.argv[2] if len(sys.argv) > 2 else "QCFuse"
-Q, cfg, w, store, eng, ids, toks = bench.build_engine(cfgd, "bf16", torch.device("cuda"))
+Q, cfg, w, store, eng, ids, toks = bench.build_engine(cfgd, "bf16", torch.device("cuda"), cfgd["n_chunks"])
 q = np.random.default_rng(10_000).integers(0, 256, cfgd["q"]).tolist()
 ratio = cfgd["ratio"] if policy == "QCFuse" else 1.0
 for _ in range(2):
