@@ -171,6 +171,17 @@ size_t qcf_score_workspace(int64_t n_ctx, int nq, int h);
 int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, int h,
               int hkv, int d, double scale, int agg_last, int precise, float* scores,
               void* workspace, size_t ws_bytes, qcf_stream_t stream);
+/* Homogeneous request batch: q [n_req*nq][H][D]; request r's context keys start
+ * at k + r*k_req_stride elements (rows of Hkv*D); scores [n_req][n_ctx].
+ * bf16 with precise=0 runs on the tensor cores (tcgen05 QK^T in TMEM fused with
+ * the row max/sum and the per-key (h,t) mean: 3 launches for the whole batch);
+ * precise=1 / f32 run the SIMT kernels per request (float64 when precise).
+ * workspace >= qcf_score_batched_workspace(...) bytes. */
+size_t qcf_score_batched_workspace(int64_t n_ctx, int nq, int n_req, int h, int hkv);
+int qcf_score_batched(int dtype, const void* q, const void* k, int64_t k_req_stride, int64_t n_ctx,
+                      int nq, int n_req, int h, int hkv, int d, double scale, int agg_last,
+                      int precise, float* scores, void* workspace, size_t ws_bytes,
+                      qcf_stream_t stream);
 
 /* ---- Top-N selection: fusion.py:141-158 (stable argsort, ties -> lower index)
  * idx_out[0..n_sel) = ascending (1-based + base) positions of the n_sel largest
@@ -179,6 +190,12 @@ int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, in
 size_t qcf_topn_workspace(int64_t n);
 int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
              int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream);
+/* Batch of n_req score rows [n_req][n]: request r's indices go to
+ * idx_out + r*out_stride; dst_out (optional) receives idx + r*dst_add at the
+ * same slots (the request's rows in a batched fused table). One launch. */
+int qcf_topn_batched(const float* scores, int64_t n, int n_req, int64_t n_sel, int32_t base,
+                     int32_t* idx_out, int64_t out_stride, int32_t* dst_out, int32_t dst_add,
+                     qcf_stream_t stream);
 
 /* Small device helpers used by the request graph. */
 /* out[i] = a[i] + add (int32) */

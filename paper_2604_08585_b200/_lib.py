@@ -63,8 +63,11 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_attention_batched": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P]),
     "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
     "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
+    "qcf_score_batched_workspace": (_SZ, [_I64, _I, _I, _I, _I]),
+    "qcf_score_batched": (_I, [_I, _P, _P, _I64, _I64, _I, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
     "qcf_topn_workspace": (_SZ, [_I64]),
     "qcf_topn": (_I, [_P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
+    "qcf_topn_batched": (_I, [_P, _I64, _I, _I64, _I32, _P, _I64, _P, _I32, _P]),
     "qcf_iota_add": (_I, [_P, _I64, _I32, _P, _P]),
     "qcf_iota": (_I, [_I64, _I32, _P, _P]),
 }
@@ -105,6 +108,7 @@ def check(status: int, what: str = "") -> None:
 # kernels launched per successful call (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {"qcf_score": 3}
 _NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
+               "qcf_score_batched_workspace",
                "qcf_topn_workspace", "qcf_gemm_workspace"}
 launch_count = 0
 
@@ -144,4 +148,12 @@ def call(name: str, *args) -> None:
         st = fn(*args)
     check(st, name)
     if name not in _NON_KERNEL:
-        launch_count += KERNELS_PER_CALL.get(name, 1)
+        launch_count += _kernels_per_call(name, args)
+
+
+def _kernels_per_call(name: str, args: tuple) -> int:
+    if name == "qcf_score_batched":
+        # tensor-core path: 3 kernels for the whole batch; SIMT path: 3 per request
+        dtype, n_req, precise = args[0], args[6], args[12]
+        return 3 if (dtype == QCF_BF16 and not precise and lib.qcf_tc_available()) else 3 * n_req
+    return KERNELS_PER_CALL.get(name, 1)

@@ -19,6 +19,8 @@ static bool tc_ok() {
   return g_tc_state == 1;
 }
 
+bool tc_available() { return tc_ok(); }
+
 }  // namespace qcf
 
 extern "C" int qcf_tc_available(void) { return qcf::tc_ok() ? 1 : 0; }

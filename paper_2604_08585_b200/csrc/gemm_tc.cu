@@ -526,6 +526,27 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
   return QCF_OK;
 }
 
+// generic bf16 map, SWIZZLE_128B, rank 2..5 (strides in bytes for dims 1..rank-1)
+int make_map_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                  const uint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  QCF_REQUIRE(enc, QCF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  QCF_REQUIRE(rank >= 2 && rank <= 5, QCF_EINVAL, "make_map_bf16: bad rank");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], estr[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    estr[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(ptr), d, st, b, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  QCF_REQUIRE(r == CUDA_SUCCESS, QCF_ECUDA, "cuTensorMapEncodeTiled(rank %d) failed (%d)", rank, (int)r);
+  return QCF_OK;
+}
+
 static int sm_count() {
   static int n = 0;
   if (!n) {

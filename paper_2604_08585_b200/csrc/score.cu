@@ -154,25 +154,60 @@ static int score_impl(const void* q, const void* k, int64_t n_ctx, int nq, int h
 
 }  // namespace qcf
 
+namespace qcf {
+size_t score_tc_workspace(int64_t n_ctx, int nq, int h, int hkv, int n_req);
+int score_tc_launch(const void* q, const void* k, int64_t k_req_stride, int64_t n_ctx, int nq, int n_req, int h,
+                    int hkv, int d, double scale, int agg_last, float* scores, void* ws, size_t ws_bytes,
+                    cudaStream_t s);
+bool tc_available();
+}  // namespace qcf
+
 extern "C" size_t qcf_score_workspace(int64_t n_ctx, int nq, int h) {
   const size_t rows = (size_t)h * nq;
   return sizeof(double) * (rows * (size_t)n_ctx + 2 * rows) + 256;
 }
 
+extern "C" size_t qcf_score_batched_workspace(int64_t n_ctx, int nq, int n_req, int h, int hkv) {
+  return std::max(qcf_score_workspace(n_ctx, nq, h), qcf::score_tc_workspace(n_ctx, nq, h, hkv, n_req));
+}
+
+extern "C" int qcf_score_batched(int dtype, const void* q, const void* k, int64_t k_req_stride, int64_t n_ctx,
+                                 int nq, int n_req, int h, int hkv, int d, double scale, int agg_last, int precise,
+                                 float* scores, void* workspace, size_t ws_bytes, qcf_stream_t stream) {
+  QCF_REQUIRE(q && k && scores && workspace, QCF_EINVAL, "qcf_score: null pointer");
+  QCF_REQUIRE(n_ctx > 0 && nq > 0 && n_req > 0 && h > 0 && hkv > 0 && h % hkv == 0 && d > 0, QCF_EINVAL,
+              "qcf_score: bad sizes");
+  QCF_REQUIRE(dtype == QCF_F32 || dtype == QCF_BF16, QCF_EINVAL, "qcf_score: bad dtype");
+  auto s = qcf::as_stream(stream);
+  if (dtype == QCF_BF16 && !precise && qcf::tc_available()) {
+    // tensor-core speed mode (score_tc.cu); shapes it does not cover use the SIMT kernels
+    const int st = qcf::score_tc_launch(q, k, k_req_stride, n_ctx, nq, n_req, h, hkv, d, scale, agg_last, scores,
+                                        workspace, ws_bytes, s);
+    if (st != QCF_EUNSUPPORTED) return st;
+  }
+  QCF_REQUIRE(ws_bytes >= qcf_score_workspace(n_ctx, nq, h), QCF_EWORKSPACE, "qcf_score: workspace too small");
+  const size_t esz = dtype == QCF_F32 ? 4 : 2;
+  for (int r = 0; r < n_req; ++r) {
+    const void* qr = reinterpret_cast<const uint8_t*>(q) + (size_t)r * nq * h * d * esz;
+    const void* kr = reinterpret_cast<const uint8_t*>(k) + (size_t)r * k_req_stride * esz;
+    float* sr = scores + (int64_t)r * n_ctx;
+    int st;
+    if (dtype == QCF_F32)
+      st = precise ? qcf::score_impl<float, double>(qr, kr, n_ctx, nq, h, hkv, d, scale, agg_last, sr, workspace, s)
+                   : qcf::score_impl<float, float>(qr, kr, n_ctx, nq, h, hkv, d, scale, agg_last, sr, workspace, s);
+    else
+      st = precise ? qcf::score_impl<__nv_bfloat16, double>(qr, kr, n_ctx, nq, h, hkv, d, scale, agg_last, sr,
+                                                            workspace, s)
+                   : qcf::score_impl<__nv_bfloat16, float>(qr, kr, n_ctx, nq, h, hkv, d, scale, agg_last, sr,
+                                                           workspace, s);
+    if (st != QCF_OK) return st;
+  }
+  return QCF_OK;
+}
+
 extern "C" int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, int h,
                          int hkv, int d, double scale, int agg_last, int precise, float* scores,
                          void* workspace, size_t ws_bytes, qcf_stream_t stream) {
-  QCF_REQUIRE(q && k && scores && workspace, QCF_EINVAL, "qcf_score: null pointer");
-  QCF_REQUIRE(n_ctx > 0 && nq > 0 && h > 0 && hkv > 0 && h % hkv == 0 && d > 0, QCF_EINVAL,
-              "qcf_score: bad sizes");
-  QCF_REQUIRE(ws_bytes >= qcf_score_workspace(n_ctx, nq, h), QCF_EWORKSPACE,
-              "qcf_score: workspace too small");
-  auto s = qcf::as_stream(stream);
-  if (dtype == QCF_F32)
-    return precise ? qcf::score_impl<float, double>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s)
-                   : qcf::score_impl<float, float>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s);
-  if (dtype == QCF_BF16)
-    return precise ? qcf::score_impl<__nv_bfloat16, double>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s)
-                   : qcf::score_impl<__nv_bfloat16, float>(q, k, n_ctx, nq, h, hkv, d, scale, agg_last, scores, workspace, s);
-  QCF_REQUIRE(false, QCF_EINVAL, "qcf_score: bad dtype");
+  return qcf_score_batched(dtype, q, k, n_ctx * hkv * d, n_ctx, nq, 1, h, hkv, d, scale, agg_last, precise, scores,
+                           workspace, ws_bytes, stream);
 }

@@ -42,17 +42,35 @@ __device__ __forceinline__ int block_scan_incl(int v, int* warp_tot, int& total)
   return v + add;
 }
 
+// One CTA per request (blockIdx.x). Keys are staged once in shared memory when
+// they fit (n <= TN_SMEM_KEYS), so the 4 radix passes and the compaction re-read
+// on-chip memory instead of L2. `dst` (optional) receives idx + r*dst_add, the
+// request's rows in the batched fused table (the recompute scatter targets).
+constexpr int TN_SMEM_KEYS = 48 * 1024;
+
+template <bool SMEM>
 __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restrict__ scores, int64_t n,
                                                           int64_t n_sel, int32_t base,
-                                                          int32_t* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
+                                                          int32_t* __restrict__ out, int64_t out_stride,
+                                                          int32_t* __restrict__ dst, int32_t dst_add) {
+  extern __shared__ uint32_t s_keys[];
   __shared__ int hist[256];
   __shared__ int warp_tot[32];
   __shared__ uint32_t s_prefix;
   __shared__ int s_need;
   const int tid = threadIdx.x;
+  const int req = blockIdx.x;
+  scores += (int64_t)req * n;
+  out += (int64_t)req * out_stride;
+  if (dst) dst += (int64_t)req * out_stride;
+  const int32_t dadd = req * dst_add;
   if (tid == 0) { s_prefix = 0; s_need = (int)n_sel; }
+  pdl_wait();
+  pdl_trigger();
+  if (SMEM) {
+    for (int64_t i = tid; i < n; i += blockDim.x) s_keys[i] = order_key(scores[i]);
+  }
+  auto key_at = [&](int64_t i) -> uint32_t { return SMEM ? s_keys[i] : order_key(scores[i]); };
   // ---- radix select of the n_sel-th largest key, 4 digits of 8 bits (MSB first)
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
@@ -60,18 +78,34 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
     const uint32_t prefix = s_prefix;
     const uint32_t hi_mask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
     for (int64_t i = tid; i < n; i += blockDim.x) {
-      uint32_t key = order_key(scores[i]);
+      const uint32_t key = key_at(i);
       if ((key & hi_mask) == (prefix & hi_mask)) atomicAdd(&hist[(key >> shift) & 0xff], 1);
     }
     __syncthreads();
-    if (tid == 0) {
-      int need = s_need, b = 255;
-      for (; b > 0; --b) {
-        if (hist[b] >= need) break;
-        need -= hist[b];
+    if (tid < 32) {  // warp 0: find the digit holding the need-th largest key
+      int need = s_need;
+      // suffix sums over the 256 bins, 8 per lane, highest bins in lane 31
+      int cnt[8], tot = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { cnt[u] = hist[tid * 8 + u]; tot += cnt[u]; }
+      int suf = tot;  // inclusive suffix sum over lanes >= tid
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_down_sync(0xffffffffu, suf, o);
+        if (tid + o < 32) suf += t;
       }
-      s_prefix = prefix | ((uint32_t)b << shift);
-      s_need = need;  // how many keys equal to the final threshold must be taken
+      const int above = suf - tot;  // keys in bins of lanes > tid
+      // the lane whose bins contain the need-th largest key
+      const bool mine = above < need && above + tot >= need;
+      if (mine) {
+        int rem = need - above, b = tid * 8 + 7;
+        for (int u = 7; u > 0; --u, --b) {
+          if (cnt[u] >= rem) break;
+          rem -= cnt[u];
+        }
+        s_prefix = prefix | ((uint32_t)b << shift);
+        s_need = rem;  // how many keys equal to the final threshold must be taken
+      }
     }
     __syncthreads();
   }
@@ -81,16 +115,21 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
   int eq_before = 0, sel_before = 0;
   for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
     const int64_t i = c0 + tid;
-    uint32_t key = i < n ? order_key(scores[i]) : 0u;
+    const uint32_t key = i < n ? key_at(i) : 0u;
     const int is_eq = (i < n && key == T) ? 1 : 0;
     int eq_total;
     const int eq_incl = block_scan_incl(is_eq, warp_tot, eq_total);
     const int take = (i < n) && (key > T || (is_eq && eq_before + eq_incl <= need_eq)) ? 1 : 0;
     int sel_total;
     const int sel_incl = block_scan_incl(take, warp_tot, sel_total);
-    if (take) out[sel_before + sel_incl - 1] = (int32_t)i + base;
+    if (take) {
+      const int slot = sel_before + sel_incl - 1;
+      out[slot] = (int32_t)i + base;
+      if (dst) dst[slot] = (int32_t)i + base + dadd;
+    }
     eq_before += eq_total;
     sel_before += sel_total;
+    if (sel_before >= n_sel) break;  // uniform across the block
   }
 }
 
@@ -98,14 +137,36 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
 
 extern "C" size_t qcf_topn_workspace(int64_t n) { (void)n; return 0; }
 
+extern "C" int qcf_topn_batched(const float* scores, int64_t n, int n_req, int64_t n_sel, int32_t base,
+                                int32_t* idx_out, int64_t out_stride, int32_t* dst_out, int32_t dst_add,
+                                qcf_stream_t stream) {
+  QCF_REQUIRE(scores && (idx_out || n_sel == 0), QCF_EINVAL, "qcf_topn: null pointer");
+  QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n && n_req >= 1, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
+  QCF_REQUIRE(n_req == 1 || out_stride >= n_sel, QCF_EINVAL, "qcf_topn: output stride < n_sel");
+  QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
+  if (n_sel == 0) return QCF_OK;
+  auto s = qcf::as_stream(stream);
+  if (n <= qcf::TN_SMEM_KEYS) {
+    static bool attr = false;
+    const size_t smem = (size_t)n * sizeof(uint32_t);
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(qcf::topn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           qcf::TN_SMEM_KEYS * (int)sizeof(uint32_t));
+      if (e != cudaSuccess) return qcf::cuda_status(e, "qcf_topn attr");
+      attr = true;
+    }
+    QCF_LAUNCH("topn_kernel", qcf::topn_kernel<true>, dim3(n_req), dim3(qcf::TN_THREADS), smem, s, scores, n, n_sel,
+               base, idx_out, out_stride, dst_out, dst_add);
+  } else {
+    QCF_LAUNCH("topn_kernel", qcf::topn_kernel<false>, dim3(n_req), dim3(qcf::TN_THREADS), 0, s, scores, n, n_sel,
+               base, idx_out, out_stride, dst_out, dst_add);
+  }
+  QCF_LAUNCH_CHECK("qcf_topn");
+  return QCF_OK;
+}
+
 extern "C" int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
                         int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream) {
   (void)workspace; (void)ws_bytes;
-  QCF_REQUIRE(scores && (idx_out || n_sel == 0), QCF_EINVAL, "qcf_topn: null pointer");
-  QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
-  QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
-  if (n_sel == 0) return QCF_OK;
-  QCF_LAUNCH("topn_kernel", qcf::topn_kernel, dim3(1), dim3(qcf::TN_THREADS), 0, qcf::as_stream(stream), scores, n, n_sel, base, idx_out);
-  QCF_LAUNCH_CHECK("qcf_topn");
-  return QCF_OK;
+  return qcf_topn_batched(scores, n, 1, n_sel, base, idx_out, n_sel, nullptr, 0, stream);
 }

@@ -219,7 +219,9 @@ class RunOptions:
     selection_seed: int = 0
     epic_per_chunk: bool = False
     qcall_layer_average: bool = False
-    score_precise: bool = True      # float64 scoring (the fp32 parity scoring mode)
+    # float64 SIMT scoring (the fp32 parity scoring mode) or tcgen05 bf16 scoring
+    # (speed mode); None = precise for f32 weights, tensor cores for bf16
+    score_precise: bool | None = None
 
 
 # ---------------------------------------------------------------------------
@@ -378,8 +380,8 @@ class _Bufs:
         self.p_tok = (rb * R + (ar + n_ctx + 1)[None, :]).reshape(-1).contiguous()
         self.qc = torch.empty((1, B * q, H, D), dtype=dt, device=dev)
         self.scores = torch.empty(B * n_ctx, dtype=torch.float32, device=dev)
-        self.score_ws = torch.empty(int(_lib.lib.qcf_score_workspace(n_ctx, q, H)), dtype=torch.uint8,
-                                    device=dev)
+        self.score_ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(n_ctx, q, B, H, Hkv)),
+                                    dtype=torch.uint8, device=dev)
         self.rc_pos = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # per-request positions == kmax
         self.rc_pos.view(B, Mr)[:, n_sel:] = ar + (n_ctx + 1)
         self.rc_dst = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # rows in the batch table
@@ -513,12 +515,21 @@ class FusionEngine:
         return QueryProbe(toks, positions, q_store, fused.key_positions()[rows] if mode != PROBE_FULL
                           else fused.key_positions(), crit, c)
 
+    @property
+    def score_precise(self) -> bool:
+        p = self.options.score_precise
+        return (self.weights.dtype == "f32") if p is None else bool(p)
+
     def _score_dev(self, q_c: torch.Tensor, k_ctx: torch.Tensor, n_ctx: int, out: torch.Tensor,
-                   ws: torch.Tensor, stream=None) -> None:
+                   ws: torch.Tensor, stream=None, n_req: int = 1, k_req_stride: int | None = None) -> None:
+        """qcf_score_batched: q_c [n_req*q][H][D]; request r's context keys at
+        k_ctx + r*k_req_stride elements (rows of Hkv*D); out [n_req][n_ctx]."""
         cfg = self.config
-        call("qcf_score", self.weights.qcf_dtype, q_c.data_ptr(), k_ctx.data_ptr(), n_ctx,
-             q_c.shape[0], cfg.n_heads, cfg.n_kv_heads, cfg.d_head, 1.0 / math.sqrt(cfg.d_head),
-             1 if self.options.query_agg == "last" else 0, 1 if self.options.score_precise else 0,
+        nq = q_c.shape[0] // n_req
+        stride = k_req_stride if k_req_stride is not None else n_ctx * cfg.n_kv_heads * cfg.d_head
+        call("qcf_score_batched", self.weights.qcf_dtype, q_c.data_ptr(), k_ctx.data_ptr(), stride, n_ctx,
+             nq, n_req, cfg.n_heads, cfg.n_kv_heads, cfg.d_head, 1.0 / math.sqrt(cfg.d_head),
+             1 if self.options.query_agg == "last" else 0, 1 if self.score_precise else 0,
              out.data_ptr(), ws.data_ptr(), ws.numel(), cuda_stream(stream))
 
     def score_against_keys(self, probe: QueryProbe, fused: FusedContext, layer: int) -> np.ndarray:
@@ -528,7 +539,8 @@ class FusionEngine:
         if q_c.shape[1] != self.config.n_heads or q_c.shape[2] != fused.k.shape[3]:
             raise ValueError("probe and fused context disagree on head shape")
         out = torch.empty(fused.n_ctx, dtype=torch.float32, device=self.device)
-        ws = torch.empty(int(_lib.lib.qcf_score_workspace(fused.n_ctx, q_c.shape[0], self.config.n_heads)),
+        ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(fused.n_ctx, q_c.shape[0], 1, self.config.n_heads,
+                                                                  self.config.n_kv_heads)),
                          dtype=torch.uint8, device=self.device)
         self._score_dev(q_c, fused.k[layer - 1, 1:], fused.n_ctx, out, ws)
         return out.cpu().numpy()
@@ -554,7 +566,8 @@ class FusionEngine:
         self.ex.embed(sc, m, toks)
         self.ex.stack(sc, m, ar, ar, ar, tk, tv, layers=range(c), q_store=q_store)
         out = torch.empty(ctx.size, dtype=torch.float32, device=self.device)
-        ws = torch.empty(int(_lib.lib.qcf_score_workspace(ctx.size, qt.size, cfg.n_heads)),
+        ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(ctx.size, qt.size, 1, cfg.n_heads,
+                                                                  cfg.n_kv_heads)),
                          dtype=torch.uint8, device=self.device)
         self._score_dev(q_store[c - 1, 1 + ctx.size:].contiguous(), tk[c - 1, 1:1 + ctx.size],
                         ctx.size, out, ws)
@@ -699,13 +712,12 @@ class FusionEngine:
                          n_req=B)
             ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
                      q_only=True, q_out=b.qc[0], stream=stream, n_req=B)
-            for r in range(B):   # K4 + K5 per request
-                self._score_dev(b.qc[0, r * q:(r + 1) * q], b.fk[c - 1, r * b.R + 1:], n_ctx,
-                                b.scores[r * n_ctx:(r + 1) * n_ctx], b.score_ws, stream)
-                call("qcf_topn", b.scores.data_ptr() + r * n_ctx * 4, n_ctx, n_sel, 1,
-                     b.rc_pos.data_ptr() + r * b.Mr * 4, None, 0, s)
-                call("qcf_iota_add", b.rc_pos.data_ptr() + r * b.Mr * 4, n_sel, r * b.R,
-                     b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+            # K4: scoring of the whole batch (request r's keys at rows r*R+1.. of layer c)
+            self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream, n_req=B,
+                            k_req_stride=b.R * row_elems)
+            # K5: Top-N of every request (ascending positions -> rc_pos, table rows -> rc_dst)
+            call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
+                 b.rc_dst.data_ptr(), b.R, s)
         elif plan.policy == "FullCompute":
             for r in range(B):
                 call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)

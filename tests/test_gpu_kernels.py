@@ -339,3 +339,80 @@ def test_gemm_tile_major_weights_match_row_major(L, m, n, k, epi):
     L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c1), n, m, n, k, epi, out_dt, 0, p(ws), ws.numel(), S())
     L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(bt), k, p(c2), n, m, n, k, epi, out_dt, 1, p(ws), ws.numel(), S())
     assert torch.equal(c1, c2)
+
+
+# ---------------------------------------------------------------- tensor-core scoring (bf16 speed mode)
+def _score_ref64(q, k, scale, agg_last):
+    """float64 restatement of fusion.py:313-326 on the bf16-rounded operands;
+    GQA heads share the kv head h // (H/Hkv). q [nq][H][D], k [n][Hkv][D]."""
+    q = q.double()
+    k = k.double()
+    H, Hkv = q.shape[1], k.shape[1]
+    kk = k.repeat_interleave(H // Hkv, dim=1)
+    if agg_last:
+        q = q[-1:]
+    s = torch.einsum("thd,nhd->htn", q, kk) * scale
+    return torch.softmax(s, dim=-1).mean(dim=(0, 1))
+
+
+@pytest.mark.parametrize("n_ctx,nq,H,Hkv,n_req,agg_last", [
+    (5120, 32, 32, 32, 1, 0), (1000, 32, 8, 8, 3, 0), (777, 7, 4, 4, 2, 0), (2048, 32, 32, 8, 2, 0),
+    (640, 16, 8, 2, 1, 1), (300, 32, 4, 4, 1, 1), (129, 1, 2, 2, 1, 0)])
+def test_score_tensor_core_vs_fp64(L, n_ctx, nq, H, Hkv, n_req, agg_last):
+    """qcf_score_batched (bf16, precise=0 -> tcgen05 + fused row stats / column
+    mean) against a float64 reference on the same bf16 inputs. Tolerance:
+    relative 2e-3 per score (fp32 accumulation, ex2.approx), sum == 1 to 1e-4,
+    and the Top-15% set overlaps the fp64 set by >= 0.97."""
+    D, extra = 128, 5          # request tables with a row stride larger than n_ctx (like the fused table)
+    g = torch.Generator(device="cuda").manual_seed(n_ctx + nq)
+    q = (torch.randn(n_req * nq, H, D, device="cuda", generator=g) * 0.6).bfloat16()
+    tab = (torch.randn(n_req, n_ctx + extra, Hkv, D, device="cuda", generator=g) * 0.6).bfloat16()
+    scores = torch.empty(n_req, n_ctx, device="cuda")
+    ws = torch.empty(int(L.lib.qcf_score_batched_workspace(n_ctx, nq, n_req, H, Hkv)), dtype=torch.uint8,
+                     device="cuda")
+    scale = 1.0 / math.sqrt(D)
+    L.call("qcf_score_batched", L.QCF_BF16, p(q), p(tab[0, 1:]), (n_ctx + extra) * Hkv * D, n_ctx, nq, n_req, H,
+           Hkv, D, scale, agg_last, 0, p(scores), p(ws), ws.numel(), S())
+    torch.cuda.synchronize()
+    for r in range(n_req):
+        ref = _score_ref64(q[r * nq:(r + 1) * nq], tab[r, 1:1 + n_ctx], scale, agg_last)
+        got = scores[r].double()
+        rel = ((got - ref).abs() / ref.abs().clamp_min(1e-30)).max().item()
+        assert rel < 2e-3, rel
+        assert abs(got.sum().item() - 1.0) < 1e-4
+        n = math.ceil(0.15 * n_ctx)
+        a = set(torch.topk(got, n).indices.tolist())
+        b = set(torch.topk(ref, n).indices.tolist())
+        assert len(a & b) >= 0.97 * n
+    # precise (float64 SIMT) path through the same entry point agrees with the reference to 1e-6
+    L.call("qcf_score_batched", L.QCF_BF16, p(q), p(tab[0, 1:]), (n_ctx + extra) * Hkv * D, n_ctx, nq, n_req, H,
+           Hkv, D, scale, agg_last, 1, p(scores), p(ws), ws.numel(), S())
+    torch.cuda.synchronize()
+    for r in range(n_req):
+        ref = _score_ref64(q[r * nq:(r + 1) * nq], tab[r, 1:1 + n_ctx], scale, agg_last)
+        assert ((scores[r].double() - ref).abs() / ref).max().item() < 1e-6
+
+
+@pytest.mark.parametrize("n,n_req,frac,levels", [(5120, 8, 0.15, 0), (5120, 3, 0.15, 7), (100000, 2, 0.05, 0),
+                                                  (777, 4, 0.5, 3), (64, 2, 1.0, 0)])
+def test_topn_batched_bit_exact(L, n, n_req, frac, levels):
+    """qcf_topn_batched: per-request stable Top-N (ties -> lower index, ascending)
+    plus the table-row image idx + r*dst_add, bit-exact vs numpy's stable argsort;
+    smem-staged (n <= 48K) and global-memory variants."""
+    rng = np.random.default_rng(n + n_req)
+    if levels:
+        s = rng.choice(np.linspace(0, 1, levels), size=(n_req, n)).astype(np.float32)
+    else:
+        s = rng.random((n_req, n)).astype(np.float32)
+    k = math.ceil(frac * n)
+    stride, dadd = k + 3, n + 11
+    ts = torch.as_tensor(s, device="cuda")
+    out = torch.full((n_req * stride,), -7, dtype=torch.int32, device="cuda")
+    dst = torch.full((n_req * stride,), -7, dtype=torch.int32, device="cuda")
+    L.call("qcf_topn_batched", p(ts), n, n_req, k, 1, p(out), stride, p(dst), dadd, S())
+    o, d = out.view(n_req, stride).cpu().numpy(), dst.view(n_req, stride).cpu().numpy()
+    for r in range(n_req):
+        ref = np.sort(np.argsort(-s[r].astype(np.float64), kind="stable")[:k]) + 1
+        assert np.array_equal(o[r, :k], ref)
+        assert np.array_equal(d[r, :k], ref + r * dadd)
+        assert (o[r, k:] == -7).all()
