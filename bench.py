@@ -37,6 +37,10 @@ sys.path.insert(0, str(ROOT))
 CONFIGS = {
     "llama3-8b": dict(n_layers=32, n_heads=32, d_model=4096, d_head=128, d_ff=14336,
                       n_chunks=10, chunk_len=512, q=32, ratio=0.15),
+    "llama3-8b-gqa": dict(n_layers=32, n_heads=32, n_kv_heads=8, d_model=4096, d_head=128, d_ff=14336,
+                          n_chunks=10, chunk_len=512, q=32, ratio=0.15),
+    "mistral-7b-32k": dict(n_layers=32, n_heads=32, n_kv_heads=8, d_model=4096, d_head=128, d_ff=14336,
+                           n_chunks=64, chunk_len=512, q=32, ratio=0.15),
     "tiny": dict(n_layers=4, n_heads=4, d_model=256, d_head=64, d_ff=1024,
                  n_chunks=4, chunk_len=128, q=16, ratio=0.15),
 }
@@ -117,7 +121,8 @@ def cpu_sample(cfgd: dict, chunk_kv_host, chunk_tokens, anchors, query, sample_l
     and extrapolate each phase to the full stack (labelled as such)."""
     from oracle import qcfuse_oracle as O
     L = cfgd["n_layers"]
-    oc = O.Config(n_layers=max(4, sample_layers), n_heads=cfgd["n_heads"], d_model=cfgd["d_model"],
+    oc = O.Config(n_layers=max(4, sample_layers), n_heads=cfgd["n_heads"], n_kv_heads=cfgd.get("n_kv_heads"),
+                  d_model=cfgd["d_model"],
                   d_head=cfgd["d_head"], d_ff=cfgd["d_ff"], seed=1234,
                   critical_layer=2 if max(4, sample_layers) >= 4 else None)
     w = O.init_weights(oc, layers=sample_layers)
@@ -127,7 +132,8 @@ def cpu_sample(cfgd: dict, chunk_kv_host, chunk_tokens, anchors, query, sample_l
     t = {}
     t0 = time.perf_counter()
     # BOS row: computed once per engine in the reference (fusion.py:226), not per request
-    bos = [O.KV(np.zeros((1, oc.n_heads, oc.d_head), np.float32), np.zeros((1, oc.n_heads, oc.d_head), np.float32),
+    bos = [O.KV(np.zeros((1, oc.n_kv_heads, oc.d_head), np.float32),
+                np.zeros((1, oc.n_kv_heads, oc.d_head), np.float32),
                 np.zeros(1, np.int64)) for _ in range(sample_layers)]
     fused = O.assemble(w, chunks, bos)
     t["assemble"] = time.perf_counter() - t0
@@ -165,7 +171,8 @@ def build_engine(cfgd, dtype, device, pool: int):
     import torch
     import paper_2604_08585_b200 as Q
     cfg = Q.ModelConfig(n_layers=cfgd["n_layers"], n_heads=cfgd["n_heads"], d_model=cfgd["d_model"],
-                        d_head=cfgd["d_head"], d_ff=cfgd["d_ff"], seed=1234)
+                        d_head=cfgd["d_head"], d_ff=cfgd["d_ff"], seed=1234,
+                        n_kv_heads=cfgd.get("n_kv_heads"), critical_layer=cfgd.get("critical_layer"))
     w = Q.init_weights(cfg, dtype=dtype, device=device)
     store = Q.ChunkStore(tempfile.mkdtemp(prefix="qcf-bench-"), cfg, dtype=dtype, device=device,
                          persist=False)
@@ -383,8 +390,8 @@ def main():
                                    f"{cfgd['n_chunks']}x{cfgd['chunk_len']}-token chunks drawn from a "
                                    f"{pool}-chunk HBM pool, q={q}, recompute {ratio:.0%}, QCFuse "
                                    f"(BASELINE configs[2]); ttft_ms = one request alone (configs[1])",
-                       "model": f"Llama-3-8B shape (L{cfg.n_layers} H{cfg.n_heads} D{cfg.d_head} "
-                                f"F{cfg.d_ff}, reference arch)" if args.config == "llama3-8b" else args.config,
+                       "model": f"{args.config} shape (L{cfg.n_layers} H{cfg.n_heads} Hkv{cfg.n_kv_heads} "
+                                f"D{cfg.d_head} F{cfg.d_ff}, reference arch: LayerNorm, ReLU FFN, tied byte vocab)",
                        "n_ctx": n_ctx, "n_selected": n_sel, "anchors": int(plans[0].anchor_rows.size - 1),
                        "requests_per_step_per_gpu": B, "parallelism": f"request sharding x{world} (replicas)",
                        "l2": "inputs larger than L2 (11.8 GB weights + chunk pool + per-request fused KV)"},
@@ -430,7 +437,8 @@ def run_reference(args, cfgd, rank):
     L = cfgd["n_layers"]
     sample_layers = 1
     # chunk KV for the sample layers from the oracle itself (no GPU on this arm)
-    oc = O.Config(n_layers=4, n_heads=cfgd["n_heads"], d_model=cfgd["d_model"], d_head=cfgd["d_head"],
+    oc = O.Config(n_layers=4, n_heads=cfgd["n_heads"], n_kv_heads=cfgd.get("n_kv_heads"), d_model=cfgd["d_model"],
+                  d_head=cfgd["d_head"],
                   d_ff=cfgd["d_ff"], seed=1234)
     w1 = O.init_weights(oc, layers=sample_layers)
     toks = [np.random.default_rng(i).integers(0, 256, cfgd["chunk_len"]) for i in range(cfgd["n_chunks"])]

@@ -79,10 +79,17 @@ class Config:
     ln_eps: float = 1e-5
     seed: int = 1234
     critical_layer: int | None = None
+    # GQA extension (the reference is MHA-only): query head h reads kv head
+    # h // (n_heads / n_kv_heads); None = n_heads, which IS the reference
+    n_kv_heads: int | None = None
 
     def __post_init__(self):
         if self.critical_layer is None:                     # model.py:87-89
             object.__setattr__(self, "critical_layer", math.ceil(self.n_layers / 2))
+        if self.n_kv_heads is None:
+            object.__setattr__(self, "n_kv_heads", self.n_heads)
+        if self.n_heads % self.n_kv_heads:
+            raise ValueError("n_heads must be a multiple of n_kv_heads")
         if self.d_model != self.n_heads * self.d_head:      # model.py:92-105
             raise ValueError("d_model must equal n_heads * d_head")
         if self.n_layers < 4:
@@ -117,11 +124,13 @@ class Weights:
 
 
 def weight_shapes(cfg: Config) -> list[tuple[int, int]]:
-    """Stream order: embedding, then per layer wq wk wv wo w1 w2 (model.py:232-235)."""
+    """Stream order: embedding, then per layer wq wk wv wo w1 w2 (model.py:232-235);
+    GQA: wk/wv are [d, Hkv*D] at the same stream positions."""
     d, f = cfg.d_model, cfg.d_ff
+    kvd = cfg.n_kv_heads * cfg.d_head
     shapes = [(cfg.vocab_size, d)]
     for _ in range(cfg.n_layers):
-        shapes += [(d, d), (d, d), (d, d), (d, d), (d, f), (f, d)]
+        shapes += [(d, d), (d, kvd), (d, kvd), (d, d), (d, f), (f, d)]
     return shapes
 
 
@@ -183,10 +192,16 @@ def softmax_rows(s: np.ndarray) -> np.ndarray:
     return (e / e.sum(axis=-1, keepdims=True)).astype(np.float32)
 
 
+def repeat_kv(k: np.ndarray, n_heads: int) -> np.ndarray:
+    """GQA: [n, Hkv, D] → [n, H, D], query head h reading kv head h // (H/Hkv)."""
+    return k if k.shape[1] == n_heads else np.repeat(k, n_heads // k.shape[1], axis=1)
+
+
 def attention(q, k, v, mask):
     """Masked SDPA (model.py:326-338): scores divided by float32(√D), -inf
-    outside the mask. q [m,H,D], k/v [n,H,D], mask [m,n] → (out [m,H,D], w [H,m,n])."""
+    outside the mask. q [m,H,D], k/v [n,Hkv,D], mask [m,n] → (out [m,H,D], w [H,m,n])."""
     d = q.shape[-1]
+    k, v = repeat_kv(k, q.shape[1]), repeat_kv(v, q.shape[1])
     s = np.matmul(q.transpose(1, 0, 2), k.transpose(1, 2, 0)) / np.float32(math.sqrt(d))
     s = np.where(mask[None], s, np.float32(-np.inf))
     w = softmax_rows(s)
@@ -222,7 +237,7 @@ def forward(w: Weights, tokens, positions, past: list[KV] | None = None,
     cfg = w.cfg
     tokens = np.asarray(tokens, np.int64)
     positions = np.asarray(positions, np.int64)
-    H, D = cfg.n_heads, cfg.d_head
+    H, Hkv, D = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
     x = w.emb[tokens]
     n = tokens.size
     self_mask = positions[None, :] <= positions[:, None]
@@ -232,8 +247,8 @@ def forward(w: Weights, tokens, positions, past: list[KV] | None = None,
         lw = w.layers[li]
         a = layer_norm(x, lw.ln1_g, lw.ln1_b, cfg.ln_eps)
         q = rope((a @ lw.wq).reshape(n, H, D), positions, cfg.rope_theta)
-        k = rope((a @ lw.wk).reshape(n, H, D), positions, cfg.rope_theta)
-        v = (a @ lw.wv).reshape(n, H, D)
+        k = rope((a @ lw.wk).reshape(n, Hkv, D), positions, cfg.rope_theta)
+        v = (a @ lw.wv).reshape(n, Hkv, D)
         if past is not None:
             pk = past[li]
             k_all = np.concatenate([pk.keys, k])
@@ -410,8 +425,9 @@ def probe(w: Weights, chunks: list[Chunk], fused: Fused, query, mode="anchors",
 
 def score_against_keys(q_c: np.ndarray, k_ctx: np.ndarray, d_head: int, agg="mean") -> np.ndarray:
     """softmax over context keys of (Q·K)·(1/√D), mean over (h,t) or last t
-    (fusion.py:313-326, 566-569). q_c [q,H,D], k_ctx [n_ctx,H,D]."""
+    (fusion.py:313-326, 566-569). q_c [q,H,D], k_ctx [n_ctx,Hkv,D]."""
     scale = 1.0 / math.sqrt(d_head)
+    k_ctx = repeat_kv(k_ctx, q_c.shape[1])
     s = np.matmul(q_c.transpose(1, 0, 2), k_ctx.transpose(1, 2, 0)) * scale
     e = np.exp(s - s.max(axis=-1, keepdims=True))
     wts = e / e.sum(axis=-1, keepdims=True)
@@ -445,15 +461,15 @@ def recompute(w: Weights, fused: Fused, sel) -> Fused:
     if sel.size:
         if sel.min() < 1 or sel.max() > fused.n_ctx:
             raise ValueError("selection indices out of context range")
-        H, D = cfg.n_heads, cfg.d_head
+        H, Hkv, D = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
         x = w.emb[fused.tokens[sel - 1]]
         vis = np.arange(fused.n_ctx + 1)[None, :] <= sel[:, None]
         m = sel.size
         for li, lw in enumerate(w.layers):
             a = layer_norm(x, lw.ln1_g, lw.ln1_b, cfg.ln_eps)
             q = rope((a @ lw.wq).reshape(m, H, D), sel, cfg.rope_theta)
-            k = rope((a @ lw.wk).reshape(m, H, D), sel, cfg.rope_theta)
-            v = (a @ lw.wv).reshape(m, H, D)
+            k = rope((a @ lw.wk).reshape(m, Hkv, D), sel, cfg.rope_theta)
+            v = (a @ lw.wv).reshape(m, Hkv, D)
             keys[li][sel] = k
             vals[li][sel] = v
             o, _ = attention(q, keys[li], vals[li], vis)

@@ -9,5 +9,6 @@ from .fusion import (POLICIES, PROBE_ANCHORS, PROBE_FULL, PROBE_NONE, FusedConte
                      QueryProbe, RecomputeTrace, RunOptions, RunResult, SelectionResult, select_topn,
                      sparse_attention, top_n_positions)
 from .pipeline import CostModel
+from .calibrate import calibrate_layer, layer_overlaps
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -551,14 +551,17 @@ class FusionEngine:
     def oracle_importance(self, context_tokens, query_tokens) -> np.ndarray:
         """Critical-layer importance from a full GPU forward over
         [BOS | context | query] (fusion.py:331-346)."""
+        return self.importance_at(context_tokens, query_tokens, self.config.critical_layer)
+
+    def importance_at(self, context_tokens, query_tokens, layer: int) -> np.ndarray:
+        """oracle_importance at any layer (the full forward runs layers 1..layer)."""
         ctx = np.asarray(context_tokens, np.int64)
         qt = np.asarray(query_tokens, np.int64)
         toks = _i32(np.concatenate([[BOS_ID], ctx, qt]), self.device)
-        c = self.config.critical_layer
+        c = int(layer)
         m = toks.numel()
         cfg = self.config
-        q_store = torch.empty((cfg.n_layers, m, cfg.n_heads, cfg.d_head), dtype=self.weights.torch_dtype,
-                              device=self.device)
+        q_store = torch.empty((c, m, cfg.n_heads, cfg.d_head), dtype=self.weights.torch_dtype, device=self.device)
         tk, tv = self.ex.new_table(m)
         ar = torch.arange(m, dtype=torch.int32, device=self.device)
         self.ex.rope.ensure(m + 1)

@@ -47,10 +47,15 @@ class ModelConfig:
     ln_eps: float = 1e-5
     seed: int = 1234
     critical_layer: int | None = None  # 1-based; defaults to ceil(n_layers / 2)
+    # GQA extension (not in the reference, which is MHA-only): kv heads shared by
+    # n_heads / n_kv_heads query heads; None = n_heads (reference-exact MHA)
+    n_kv_heads: int | None = None
 
     def __post_init__(self):
         if self.critical_layer is None:
             object.__setattr__(self, "critical_layer", math.ceil(self.n_layers / 2))
+        if self.n_kv_heads is None:
+            object.__setattr__(self, "n_kv_heads", self.n_heads)
         self.validate()
 
     def validate(self) -> None:
@@ -66,19 +71,26 @@ class ModelConfig:
             raise ValueError("d_head must be even for rotary pairs")
         if self.rope_theta <= 0 or self.ln_eps <= 0:
             raise ValueError("rope_theta and ln_eps must be positive")
-
-    @property
-    def n_kv_heads(self) -> int:
-        return self.n_heads
+        if self.n_kv_heads < 1 or self.n_heads % self.n_kv_heads != 0:
+            raise ValueError("n_heads must be a multiple of n_kv_heads")
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff",
-                                              "vocab_size", "rope_theta", "ln_eps", "seed",
-                                              "critical_layer")}
+        """model.py:108-118; n_kv_heads appears only for GQA so MHA fingerprints
+        equal the reference's (store.py:46-49)."""
+        out = {k: getattr(self, k) for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff",
+                                             "vocab_size", "rope_theta", "ln_eps", "seed",
+                                             "critical_layer")}
+        if self.n_kv_heads != self.n_heads:
+            out["n_kv_heads"] = self.n_kv_heads
+        return out
+
+    @property
+    def kv_dim(self) -> int:
+        return self.n_kv_heads * self.d_head
 
     def layer_params(self) -> int:
         d, f = self.d_model, self.d_ff
-        return 4 * d * d + 2 * d * f
+        return 2 * d * d + 2 * d * self.kv_dim + 2 * d * f
 
 
 def tokenize(text) -> list[int]:
@@ -200,7 +212,7 @@ def use_tiled_weights(config: ModelConfig, dtype: str) -> bool:
     """bf16 on a tcgen05 device with every projection dim a multiple of 64."""
     if dtype != "bf16" or not torch.cuda.is_available() or not _lib.lib.qcf_tc_available():
         return False
-    return all(x % 64 == 0 for x in (config.d_model, config.d_ff, config.n_heads * config.d_head))
+    return all(x % 64 == 0 for x in (config.d_model, config.d_ff, config.n_heads * config.d_head, config.kv_dim))
 
 
 def _tile_layers(layers: list, on: bool) -> None:
@@ -220,7 +232,8 @@ def _get(obj, *names):
 def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
                  layers: int | None = None) -> ModelWeights:
     """GPU restatement of init_weights (model.py:225-257): stream order
-    embedding, then per layer wq wk wv wo w1 w2, each row-major."""
+    embedding, then per layer wq wk wv wo w1 w2, each row-major. GQA: wk/wv are
+    [d][Hkv*D] in the same stream order (reduces to the reference at Hkv == H)."""
     config.validate()
     dev = torch.device(device)
     qdt, tdt = DTYPES[dtype]
@@ -233,15 +246,18 @@ def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
     n_build = config.n_layers if layers is None else layers
     tiled = use_tiled_weights(config, dtype)
     dl = []
+    kvd = config.kv_dim
     for _ in range(n_build):
-        wqkv = torch.empty(3 * d, d, dtype=tdt, device=dev)
+        wqkv = torch.empty(d + 2 * kvd, d, dtype=tdt, device=dev)
         wo = torch.empty(d, d, dtype=tdt, device=dev)
         w1 = torch.empty(f, d, dtype=tdt, device=dev)
         w2 = torch.empty(d, f, dtype=tdt, device=dev)
         esz = wqkv.element_size()
-        for j in range(3):  # wq, wk, wv -> rows [j*d, (j+1)*d) of wqkv
-            call("qcf_init_uniform", seed, off, d, d, 1, qdt, wqkv.data_ptr() + j * d * d * esz, d, s)
-            off += d * d
+        row = 0
+        for cols in (d, kvd, kvd):  # wq, wk, wv -> consecutive row blocks of wqkv (K-major)
+            call("qcf_init_uniform", seed, off, d, cols, 1, qdt, wqkv.data_ptr() + row * d * esz, d, s)
+            off += d * cols
+            row += cols
         call("qcf_init_uniform", seed, off, d, d, 1, qdt, wo.data_ptr(), d, s)
         off += d * d
         call("qcf_init_uniform", seed, off, d, f, 1, qdt, w1.data_ptr(), d, s)

@@ -43,7 +43,7 @@ class ScheduleTrace:
 
 
 def layer_times(n_sel: int, n_ctx: int, config: ModelConfig, cost: CostModel) -> tuple[float, float]:
-    fetch = cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_heads, config.d_head))
+    fetch = cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_kv_heads, config.d_head))
     return fetch, cost.compute_alpha * n_sel * n_ctx * config.n_heads * config.d_head + cost.compute_beta
 
 
@@ -68,12 +68,12 @@ def schedule_pipelined(fetch, compute, pre_phase: float = 0.0) -> ScheduleTrace:
 
 def policy_prephase(policy: str, n_ctx: int, n_query: int, config: ModelConfig, cost: CostModel) -> float:
     unit = config.n_heads * config.d_head
-    full = cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_heads, config.d_head))
+    full = cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_kv_heads, config.d_head))
     if policy in ("FullCompute", "FullReuse", "EPIC", "Random"):
         return 0.0
     if policy in ("QCFuse", "QCLast"):
         return (cost.compute_alpha * n_query * n_ctx * unit + cost.compute_beta
-                + cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_heads, config.d_head) // 2))
+                + cost.tier.fetch_seconds(layer_kv_bytes(n_ctx, config.n_kv_heads, config.d_head) // 2))
     if policy == "QCAll":
         return config.n_layers * full
     if policy in ("CacheBlend", "KVShare"):

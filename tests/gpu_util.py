@@ -20,7 +20,7 @@ def to_model_config(oc: O.Config):
     import paper_2604_08585_b200 as Q
     return Q.ModelConfig(n_layers=oc.n_layers, n_heads=oc.n_heads, d_model=oc.d_model,
                          d_head=oc.d_head, d_ff=oc.d_ff, rope_theta=oc.rope_theta, ln_eps=oc.ln_eps,
-                         seed=oc.seed, critical_layer=oc.critical_layer)
+                         seed=oc.seed, critical_layer=oc.critical_layer, n_kv_heads=oc.n_kv_heads)
 
 
 def device_weights(ow: O.Weights, dtype: str):

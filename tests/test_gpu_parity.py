@@ -343,3 +343,55 @@ def test_batched_prefill_equals_single_requests(tmp_path, dtype):
         else:
             assert len(set(bsel.tolist()) & set(sel.tolist())) >= 0.9 * n_sel
             assert np.abs(blog - logits).max() < 5e-2 * np.abs(logits).max()
+
+
+# ---------------------------------------------------------------- GQA extension (BASELINE configs[3] shape family)
+def _gqa_case(tmp_path, dtype, H, Hkv, D, d_ff, lens, q, ratio, seed=5):
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    oc = O.Config(n_layers=4, n_heads=H, n_kv_heads=Hkv, d_model=H * D, d_head=D, d_ff=d_ff, seed=seed)
+    ow = O.init_weights(oc)
+    rng = np.random.default_rng(seed)
+    chunks = [O.precompute_chunk(ow, rng.integers(0, 256, n), 0.1) for n in lens]
+    query = rng.integers(0, 256, q).tolist()
+    ref = O.run(ow, chunks, query, ratio)
+    w = device_weights(ow, dtype)
+    store = Q.ChunkStore(tmp_path / "s", w.config, dtype=dtype, persist=False)
+    ids = load_oracle_chunks(store, chunks)
+    eng = Q.FusionEngine(w, store)
+    logits, sel = eng.fuse(query, ids, ratio)
+    return ref, logits, sel, oc, ow
+
+
+@pytest.mark.parametrize("H,Hkv", [(4, 2), (4, 1), (8, 2)])
+def test_gqa_f32_matches_oracle(tmp_path, H, Hkv):
+    """GQA in the f32 parity mode: selection bit-exact and first-token logits
+    within 1e-4 of the oracle restatement (which reduces to the reference at
+    Hkv == H and repeats kv heads otherwise)."""
+    ref, logits, sel, _, _ = _gqa_case(tmp_path, "f32", H, Hkv, 16, 128, [40, 33, 51], 8, 0.25)
+    assert np.array_equal(sel, ref.selection)
+    assert np.abs(logits - ref.first_logits).max() < 1e-4
+
+
+def test_gqa_bf16_tensor_core_path(tmp_path):
+    """GQA-4 at D=128 runs the tcgen05 GEMM / attention / scoring kernels;
+    bf16 speed-mode bounds vs the f32 oracle (overlap >= 0.85, rel logit err < 5e-2)."""
+    ref, logits, sel, _, _ = _gqa_case(tmp_path, "bf16", 8, 2, 128, 2048, [160, 128, 192], 32, 0.15)
+    overlap = len(set(sel.tolist()) & set(ref.selection.tolist())) / len(sel)
+    err = np.abs(logits - ref.first_logits).max() / np.abs(ref.first_logits).max()
+    print(f"GQA bf16 overlap {overlap:.3f} rel logit err {err:.3e}")
+    assert overlap >= 0.85 and err < 5e-2
+
+
+def test_gqa_init_bit_exact(tmp_path):
+    """On-device splitmix64 init with GQA wk/wv shapes equals the oracle's draws."""
+    import paper_2604_08585_b200 as Q
+    from paper_2604_08585_b200.model import untile64
+    cfg = Q.ModelConfig(n_layers=4, n_heads=8, n_kv_heads=2, d_model=512, d_head=64, d_ff=256, seed=77)
+    w = Q.init_weights(cfg, dtype="f32")
+    ow = O.init_weights(O.Config(n_layers=4, n_heads=8, n_kv_heads=2, d_model=512, d_head=64, d_ff=256, seed=77))
+    for li in (0, 3):
+        wqkv = w.layers[li].wqkv.cpu().numpy()
+        ref = np.concatenate([ow.layers[li].wq, ow.layers[li].wk, ow.layers[li].wv], axis=1).T
+        assert np.array_equal(wqkv, ref)
+        assert np.array_equal(w.layers[li].w2.cpu().numpy(), ow.layers[li].w2.T)

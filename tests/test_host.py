@@ -183,3 +183,23 @@ def test_gather_two_ranks_gloo(n_total):
     rows, t = q.get()
     assert rows == [float(i) for i in range(n_total)]
     assert t == 2.0
+
+
+def test_oracle_gqa_equals_mha_with_repeated_kv_weights():
+    """The GQA restatement's semantics: a GQA model equals the MHA model whose
+    wk/wv repeat each kv head's columns for the H/Hkv query heads sharing it."""
+    from oracle import qcfuse_oracle as O
+    g = O.Config(n_layers=4, n_heads=4, n_kv_heads=2, d_model=32, d_head=8, d_ff=64, seed=3)
+    m = O.Config(n_layers=4, n_heads=4, d_model=32, d_head=8, d_ff=64, seed=3)
+    wg = O.init_weights(g)
+    layers = []
+    for lw in wg.layers:
+        rep = lambda w: np.repeat(w.reshape(32, 2, 8), 2, axis=1).reshape(32, 32)  # noqa: E731
+        layers.append(O.Layer(lw.wq, rep(lw.wk), rep(lw.wv), lw.wo, lw.w1, lw.w2, lw.ln1_g, lw.ln1_b,
+                              lw.ln2_g, lw.ln2_b))
+    wm = O.Weights(m, wg.emb, layers, wg.lnf_g, wg.lnf_b)
+    toks = np.random.default_rng(0).integers(0, 256, 21)
+    a = O.forward_full(wg, toks, 0)
+    b = O.forward_full(wm, toks, 0)
+    assert np.allclose(a.logits, b.logits, atol=1e-6)
+    assert np.array_equal(np.repeat(a.kv[2].keys, 2, axis=1), b.kv[2].keys)
