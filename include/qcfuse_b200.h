@@ -162,6 +162,11 @@ int qcf_attention(int dtype, const void* q, const void* k, const void* v,
 int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
                           const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
                           int64_t n_keys, void* out, qcf_stream_t stream);
+/* Tuning knob (process-wide): tcgen05 attention kernel 1 = one 128-row query
+ * tile per CTA, P staged through shared memory; 2 = two query tiles per CTA
+ * ping-ponging on the tensor core, P kept in TMEM; 0 (default) = 2 when the
+ * tile pairs span more than one wave of CTAs, else 1. */
+int qcf_set_attention_kernel(int version);
 
 /* ---- critical-layer scoring: fusion.py:313-326 + 566-569 ------------------
  * scores[n] = mean_{h,t} softmax_n((q[t,h].k[n,h]) * scale), t over all nq rows

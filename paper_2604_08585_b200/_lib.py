@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_gemm_qkv_rope": (_I, [_P, _I64, _P, _I64, _I, _I64, _I64, _I, _I, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_attention_batched": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P]),
+    "qcf_set_attention_kernel": (_I, [_I]),
     "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
     "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
     "qcf_score_batched_workspace": (_SZ, [_I64, _I, _I, _I, _I]),
@@ -108,7 +109,7 @@ def check(status: int, what: str = "") -> None:
 # kernels launched per successful call (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {"qcf_score": 3}
 _NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
-               "qcf_score_batched_workspace",
+               "qcf_score_batched_workspace", "qcf_set_attention_kernel",
                "qcf_topn_workspace", "qcf_gemm_workspace"}
 launch_count = 0
 

@@ -16,6 +16,7 @@
 // Query rows arrive sorted by position (selection is ascending), so a tile's
 // key range is [0, max kmax] and only its tail tiles are partially masked.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "attention.cuh"
 #include "sm100.cuh"
@@ -318,6 +319,430 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------------------
+// v2: two query tiles per CTA (ping-pong) with P kept in tensor memory.
+//
+// One CTA = (two 128-row query tiles, one head). TMEM: S_t / P_t (cols 128t..)
+// and O_t (cols 256+128t..) for t = 0, 1. Per key tile j the MMA thread issues,
+// in order,  PV(0,j-1)? .. : S(0,j) S(1,j) PV(0,j) S(0,j+1) PV(1,j) S(1,j+1) ...
+// so the tensor core computes one tile's QK^T / PV while the other tile's
+// softmax warps run. P_t,j is written as packed bf16 over the first 64 columns
+// of S_t,j (tcgen05.st) and consumed straight from TMEM as the A operand of
+// O_t += P_t,j . V_j (the .kind::f16 [a-tmem] form) -- no shared-memory round
+// trip. tcgen05 ops of one thread complete in order, so S_t,j+1 (issued after
+// PV_t,j) cannot overwrite P_t,j early, and "S_t,j+1 complete" also means
+// "PV_t,j complete": the lazy O rescale needs no extra barrier.
+// Softmax: 8 warps per tile = 4 TMEM lane quarters x 2 column halves (64 keys /
+// 64 output dims each); the two halves of a row exchange their max via smem.
+// Pairing of query tiles: adjacent (2p, 2p+1) when the grid spans several
+// waves, mirrored (p, n-1-p) -- equal work per CTA -- when it fits in one.
+// ---------------------------------------------------------------------------
+constexpr int A2_THREADS = 576;
+#ifndef A2_EMU16
+#define A2_EMU16 7  // of every 16 column pairs, this many take the FMA-pipe exp2 (balances MUFU vs FMA)
+#endif
+constexpr int A2_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q[2], K[2], V[2]
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&o)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
+      "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
+      "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]));
+}
+
+// ---- softmax arithmetic helpers (packed f32x2 FFMA2/FADD2, 3-input max, exp2
+// emulated on the FMA pipe for part of the columns: B200's MUFU ex2 rate (16/clk/SM)
+// would otherwise bound the softmax below the tensor core's rate)
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// 2^x for two lanes on the FMA pipe: x = n + f, n = rint(x) via the 1.5*2^23
+// magic add, 2^f on [-0.5, 0.5] by a cubic (rel. err 7.5e-5, far below bf16's
+// 3.9e-3 rounding of P), exponent bits added back. Inputs clamped to >= -127.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float a, b;
+  f2_split(x2, a, b);
+  x2 = f2(fmaxf(a, -127.f), fmaxf(b, -127.f));
+  const uint64_t magic = f2(12582912.f, 12582912.f), nmagic = f2(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(x2, magic);
+  float ra0, rb0;
+  f2_split(fadd2(t, nmagic), ra0, rb0);                // rint(x)
+  const uint64_t fr = fadd2(x2, f2(-ra0, -rb0));       // x - rint(x) in [-0.5, 0.5]
+  uint64_t p = ffma2(fr, f2(0.05517095f, 0.05517095f), f2(0.24260963f, 0.24260963f));
+  p = ffma2(p, fr, f2(0.69326096f, 0.69326096f));
+  p = ffma2(p, fr, f2(0.99992817f, 0.99992817f));
+  float pa, pb, ta, tb;
+  f2_split(p, pa, pb);
+  f2_split(t, ta, tb);
+  const float ra = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+  const float rb = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+  return f2(ra, rb);
+}
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__global__ void __launch_bounds__(A2_THREADS, 1)
+attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
+                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int mirrored) {
+  const int req = blockIdx.z;
+  kmax += (int64_t)req * M;
+  out += (int64_t)req * M * H * AT_D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                          // [2 tiles]
+  uint8_t* sK = smem + 2 * AT_TILE_BYTES;      // [2 stages]
+  uint8_t* sV = smem + 4 * AT_TILE_BYTES;      // [2 stages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * AT_TILE_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;    // [2]
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [2 tiles]
+  uint64_t* p_full = bars + 11;   // [2 tiles]
+  uint64_t* o_full = bars + 13;   // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  __shared__ float red[2][2][2][AT_BM];  // [tile][j parity][column half][row]
+  __shared__ int s_kend[2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int n_pairs = (n_qt + 1) / 2;
+  const int pidx = n_pairs - 1 - (int)blockIdx.y;  // adjacent pairs: longest (latest rows) first
+  int tile0, tile1;
+  if (mirrored) {
+    tile0 = pidx;
+    tile1 = n_qt - 1 - pidx;
+    if (tile1 == tile0) tile1 = -1;
+  } else {
+    tile0 = 2 * pidx;
+    tile1 = 2 * pidx + 1 < n_qt ? 2 * pidx + 1 : -1;
+  }
+  const int head = blockIdx.x;
+  const int kvh = head / (H / Hkv);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 8);  // one elected arrive per softmax warp of the tile
+      mbar_init(&o_full[s], 1);
+    }
+    fence_barrier_init();
+    s_kend[0] = s_kend[1] = 0;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x < 2 * AT_BM) {  // key range of each tile = 1 + max kmax over its rows
+    const int t = threadIdx.x / AT_BM;
+    const int tl = t ? tile1 : tile0;
+    int v = 0;
+    if (tl >= 0) {
+      const int row = tl * AT_BM + (threadIdx.x % AT_BM);
+      v = row < M ? kmax[row] + 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) atomicMax(&s_kend[t], min(v, n_keys));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nt0 = (s_kend[0] + AT_BN - 1) / AT_BN;
+  const int nt1 = (s_kend[1] + AT_BN - 1) / AT_BN;
+  const int nmax = max(nt0, nt1);
+
+  if (warp == 0) {
+    if (lane == 0 && nmax > 0) {  // ---------------- TMA producer
+      mbar_expect_tx(q_full, (nt0 > 0 ? AT_TILE_BYTES : 0) + (nt1 > 0 ? AT_TILE_BYTES : 0));
+      for (int t = 0; t < 2; ++t) {
+        const int n_t = t ? nt1 : nt0, tl = t ? tile1 : tile0;
+        if (n_t == 0) continue;
+        tma_load_3d(sQ + t * AT_TILE_BYTES, &map_q, q_full, head * AT_D, tl * AT_BM, req);
+        tma_load_3d(sQ + t * AT_TILE_BYTES + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, tl * AT_BM, req);
+      }
+      auto load_k = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
+        uint8_t* k = sK + st * AT_TILE_BYTES;
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      };
+      auto load_v = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
+        uint8_t* v = sV + st * AT_TILE_BYTES;
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      };
+      load_k(0);
+      for (int j = 0; j < nmax; ++j) {
+        if (j + 1 < nmax) load_k(j + 1);
+        load_v(j);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nmax > 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);  // B (V) MN-major
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_s = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint8_t* q = sQ + t * AT_TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk) {
+          const uint64_t a = umma_desc_k_sw128(q + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+          const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
+                             (uint64_t)((kk & 3) * 2);
+          mma_bf16(tmem + t * 128, a, b, idesc_s, kk != 0);
+        }
+        mma_commit(&s_full[t]);
+        const bool last_user = (t == 1) || (j >= nt1);
+        if (last_user) mma_commit(&k_empty[st]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&p_full[t], j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk) {
+          const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
+          const uint32_t pa = tmem + t * 128 + (kk >> 2) * 64 + (kk & 3) * 8;  // P cols of keys 16kk..16kk+15
+          mma_bf16_ts(tmem + 256 + t * 128, pa, b, idesc_o, (j | kk) != 0);
+        }
+        const bool last_user = (t == 1) || (j >= nt1);
+        if (last_user) mma_commit(&v_empty[st]);
+        if (j == (t ? nt1 : nt0) - 1) mma_commit(&o_full[t]);
+      };
+      if (nt0 > 0) issue_s(0, 0);
+      if (nt1 > 0) issue_s(1, 0);
+      for (int j = 0; j < nmax; ++j) {
+        if (j < nt0) {
+          issue_pv(0, j);
+          if (j + 1 < nt0) issue_s(0, j + 1);
+        }
+        if (j < nt1) {
+          issue_pv(1, j);
+          if (j + 1 < nt1) issue_s(1, j + 1);
+        }
+      }
+    }
+  } else {  // ---------------- softmax / rescale / epilogue: warps 2..17
+    const int t = (warp - 2) >> 3;        // query tile
+    const int ch = ((warp - 2) >> 2) & 1; // column half: keys / output dims 64ch..64ch+63
+    const int g = warp & 3;               // TMEM lane quarter
+    const int r = g * 32 + lane;
+    const int n_my = t ? nt1 : nt0;
+    const int my_tile = t ? tile1 : tile0;
+    const int row = my_tile * AT_BM + r;
+    const int my_kmax = (my_tile >= 0 && row < M) ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const int bar_id = 1 + t * 4 + g;     // the 2 warps (column halves) of these 32 rows
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_my; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const int lim = my_kmax - j * AT_BN - ch * 64;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= 63);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      float pmax = -INFINITY;
+      if (!none_vis) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // pass 1: row max over this half's 64 columns
+          uint32_t v[32];
+          tmem_ld32(tS + ch * 64 + hh * 32, v);
+          tmem_ld_wait();
+          if (all_vis) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              pmax = fmaxf(pmax, (hh * 32 + i <= lim) ? __uint_as_float(v[i]) : -INFINITY);
+          }
+        }
+      }
+      red[t][j & 1][ch][r] = pmax * scale_log2;
+      named_bar(bar_id, 64);
+      const float tmax = fmaxf(red[t][j & 1][0][r], red[t][j & 1][1][r]);
+      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
+        m_ref = tmax;
+        l *= alpha;
+      }
+      // pass 2: P = exp2(s*scale - m_ref) as packed bf16 over the first 32 of this
+      // half's own 64 S columns (P cols 64ch + 16hh .. +15): no overlap with the
+      // other half's S, so no second exchange is needed before the store
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t pk[16];
+        if (none_vis) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        } else {
+          uint32_t v[32];
+          tmem_ld32(tS + ch * 64 + hh * 32, v);
+          tmem_ld_wait();
+          if (all_vis) {
+            const uint64_t sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_ref, -m_ref);
+            uint64_t l2 = f2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
+              uint64_t p2;
+              if (((i >> 1) & 15) < A2_EMU16) {
+                p2 = exp2_poly2(x2);
+              } else {
+                float a, b;
+                f2_split(x2, a, b);
+                p2 = f2(ex2_approx(a), ex2_approx(b));
+              }
+              l2 = fadd2(l2, p2);
+              float p0, p1;
+              f2_split(p2, p0, p1);
+              pk[i >> 1] = bf16x2_bits(p0, p1);
+            }
+            float la, lb;
+            f2_split(l2, la, lb);
+            l += la + lb;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
+              float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
+              p0 = (hh * 32 + i <= lim) ? p0 : 0.f;
+              p1 = (hh * 32 + i + 1 <= lim) ? p1 : 0.f;
+              l += p0 + p1;
+              pk[i >> 1] = bf16x2_bits(p0, p1);
+            }
+          }
+        }
+        tmem_st16(tS + ch * 64 + hh * 16, pk);
+      }
+      // lazy O rescale; PV(t, j-1) is complete (S(t, j) was issued after it, in order)
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t o[32];
+          tmem_ld32(tO + ch * 64 + hh * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tO + ch * 64 + hh * 32, o);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    // epilogue: combine the two half-row sums, then O / l for this warp's 64 output dims
+    if (n_my > 0) {
+      named_bar(bar_id, 64);
+      red[t][0][ch][r] = l;
+      named_bar(bar_id, 64);
+      const float lt = red[t][0][0][r] + red[t][0][1][r];
+      mbar_wait(&o_full[t], 0);
+      tc_fence_after();
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t o[32];
+        tmem_ld32(tO + ch * 64 + hh * 32, o);
+        tmem_ld_wait();
+        if (row < M && my_kmax >= 0) {
+          __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + ch * 64 + hh * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 pk4;
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv,
+                                            __uint_as_float(o[i + 2 * u + 1]) * inv);
+            *reinterpret_cast<uint4*>(dst + i) = pk4;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+static int g_attn_ver = -1;  // QCF_ATTN env / qcf_set_attention_kernel: 1 = single-tile, 2 = ping-pong (default)
+
+void set_attention_kernel(int v) { g_attn_ver = (v == 1 || v == 2) ? v : 0; }
+
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
                         int hkv, int d, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
   if (d != AT_D || m > INT32_MAX || n_keys > INT32_MAX || n_req > 65535) return QCF_EUNSUPPORTED;
@@ -328,16 +753,40 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   if (st == QCF_OK) st = make_kmajor_map3(&mk, k, n_keys, kw, kw, AT_BN, n_req, n_keys * kw);
   if (st == QCF_OK) st = make_kmajor_map3(&mv, v, n_keys, kw, kw, AT_BN, n_req, n_keys * kw);
   if (st != QCF_OK) return st;
+  if (g_attn_ver < 0) {
+    const char* e = getenv("QCF_ATTN");
+    g_attn_ver = (e && atoi(e) == 1) ? 1 : (e && atoi(e) == 2) ? 2 : 0;  // 0 = by grid size
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
     if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
-  dim3 grid((unsigned)h, (unsigned)((m + AT_BM - 1) / AT_BM), (unsigned)n_req);
-  QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m, h, hkv, (int)n_keys, scale_log2,
-                                                   (__nv_bfloat16*)out);
+  const int n_qt = (int)((m + AT_BM - 1) / AT_BM);
+  const int n_pairs = (n_qt + 1) / 2;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  const bool one_wave = (int64_t)h * n_pairs * n_req <= sms;
+  // auto: tile pairs need more than one wave of CTAs to beat single tiles (a lone
+  // long tile per CTA cannot ping-pong); measured in tools/attn_bench.py
+  const int ver = g_attn_ver ? g_attn_ver : (one_wave ? 1 : 2);
+  if (ver == 2) {
+    // one wave or less: mirrored pairs balance the per-CTA key ranges
+    const int mirrored = one_wave ? 1 : 0;
+    dim3 grid((unsigned)h, (unsigned)n_pairs, (unsigned)n_req);
+    QCF_LAUNCH("attn_tc2_kernel", attn_tc2_kernel, dim3(grid), dim3(A2_THREADS), A2_SMEM, s, mq, mk, mv, kmax, (int)m,
+               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
+  } else {
+    dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
+    QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m,
+               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out);
+  }
   QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");
   return QCF_OK;
 }

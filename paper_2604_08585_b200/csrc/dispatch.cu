@@ -20,6 +20,7 @@ static bool tc_ok() {
 }
 
 bool tc_available() { return tc_ok(); }
+void set_attention_kernel(int v);
 
 }  // namespace qcf
 
@@ -103,4 +104,10 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
                                            q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout);
   if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, m > 32, alignment)");
   return st;
+}
+
+extern "C" int qcf_set_attention_kernel(int version) {
+  QCF_REQUIRE(version >= 0 && version <= 2, QCF_EINVAL, "qcf_set_attention_kernel: version 0 (auto), 1 or 2");
+  qcf::set_attention_kernel(version);
+  return QCF_OK;
 }

@@ -67,7 +67,11 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a,
 // With `delta` != null the residual update x += delta (the projection output,
 // model.py:375-376) is applied first and written back, fusing the residual add
 // that would otherwise be a read-modify-write in the GEMM epilogue.
-template <typename T>
+// V float4 per thread (d = 4*V*256 at most): x and delta are loaded up front,
+// gain/bias only at the store (L1/L2 resident), so registers stay low and
+// several rows per SM keep their loads in flight (the kernel is HBM-bound:
+// 4+4 B read, 4+2 B written per element).
+template <typename T, int V>
 __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                                                int64_t m, int d, const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps,
@@ -81,33 +85,28 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
   const int n4 = d >> 2;
-  float4 v[LN_V4], gv[LN_V4], bv[LN_V4];
+  float4 v[V], t[V];
 #pragma unroll
-  for (int i = 0; i < LN_V4; ++i) {
+  for (int i = 0; i < V; ++i) {
     const int e = threadIdx.x + i * LN_THREADS;
-    const bool ok = e < n4;
-    v[i] = ok ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
-    gv[i] = ok ? g4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
-    bv[i] = ok ? b4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[i] = e < n4 ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    t[i] = (dr && e < n4) ? __ldcs(dr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (dr) {
 #pragma unroll
-    for (int i = 0; i < LN_V4; ++i) {
+    for (int i = 0; i < V; ++i) {
       const int e = threadIdx.x + i * LN_THREADS;
-      if (e < n4) {
-        const float4 t = dr[e];
-        v[i].x += t.x; v[i].y += t.y; v[i].z += t.z; v[i].w += t.w;
-        xr[e] = v[i];
-      }
+      v[i].x += t[i].x; v[i].y += t[i].y; v[i].z += t[i].z; v[i].w += t[i].w;
+      if (e < n4) xr[e] = v[i];
     }
   }
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  for (int i = 0; i < V; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   const float mean = block_sum_256(s, red) / d;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_V4; ++i) {
+  for (int i = 0; i < V; ++i) {
     if (threadIdx.x + i * LN_THREADS < n4) {
       const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
       q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
@@ -117,12 +116,30 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict
   const float sd = sqrtf(var + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b  (model.py:308)
   T* orow = out + row * d;
 #pragma unroll
-  for (int i = 0; i < LN_V4; ++i) {
+  for (int i = 0; i < V; ++i) {
     const int e = threadIdx.x + i * LN_THREADS;
-    if (e < n4)
-      store4<T>(orow + 4 * e, ((v[i].x - mean) / sd) * gv[i].x + bv[i].x, ((v[i].y - mean) / sd) * gv[i].y + bv[i].y,
-                ((v[i].z - mean) / sd) * gv[i].z + bv[i].z, ((v[i].w - mean) / sd) * gv[i].w + bv[i].w);
+    if (e < n4) {
+      const float4 gv = g4[e], bv = b4[e];
+      store4<T>(orow + 4 * e, ((v[i].x - mean) / sd) * gv.x + bv.x, ((v[i].y - mean) / sd) * gv.y + bv.y,
+                ((v[i].z - mean) / sd) * gv.z + bv.z, ((v[i].w - mean) / sd) * gv.w + bv.w);
+    }
   }
+}
+
+template <typename T>
+static int launch_ln_vec(float* x, const float* delta, int64_t m, int d, const float* g, const float* b, float eps,
+                         T* out, cudaStream_t s) {
+  const int n4 = d / 4;
+  const unsigned grid = (unsigned)m;
+  if (n4 <= LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 1>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else if (n4 <= 2 * LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 2>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else if (n4 <= 4 * LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 4>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, LN_V4>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  return QCF_OK;
 }
 
 // generic fallback (d % 4 != 0): one CTA per row, strided scalar loop
@@ -284,11 +301,15 @@ int qcf_add_layernorm(float* x, const float* delta, int64_t m, int d, const floa
                    !(((uintptr_t)x | (uintptr_t)g | (uintptr_t)b | (uintptr_t)out | (uintptr_t)delta) & 15) &&
                    (out_dtype == QCF_F32 || d % 8 == 0);
   if (out_dtype == QCF_F32) {
-    if (vec) QCF_LAUNCH("layernorm_kernel", qcf::layernorm_kernel<float>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (float*)out);
-    else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<float>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (float*)out);
+    if (vec) {
+      const int st = qcf::launch_ln_vec<float>(x, delta, m, d, g, b, eps, (float*)out, s);
+      if (st != QCF_OK) return st;
+    } else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<float>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (float*)out);
   } else if (out_dtype == QCF_BF16) {
-    if (vec) QCF_LAUNCH("layernorm_kernel", qcf::layernorm_kernel<__nv_bfloat16>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
-    else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<__nv_bfloat16>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
+    if (vec) {
+      const int st = qcf::launch_ln_vec<__nv_bfloat16>(x, delta, m, d, g, b, eps, (__nv_bfloat16*)out, s);
+      if (st != QCF_OK) return st;
+    } else QCF_LAUNCH("layernorm_scalar_kernel", qcf::layernorm_scalar_kernel<__nv_bfloat16>, dim3(grid), dim3(qcf::LN_THREADS), 0, s, x, delta, m, d, g, b, eps, (__nv_bfloat16*)out);
   } else {
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_layernorm: bad dtype");
   }

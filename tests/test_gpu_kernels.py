@@ -416,3 +416,38 @@ def test_topn_batched_bit_exact(L, n, n_req, frac, levels):
         assert np.array_equal(o[r, :k], ref)
         assert np.array_equal(d[r, :k], ref + r * dadd)
         assert (o[r, k:] == -7).all()
+
+
+def _torch_attention_gqa(q, k, v, kmax):
+    H, Hkv = q.shape[1], k.shape[1]
+    return torch_attention(q, k.repeat_interleave(H // Hkv, dim=1), v.repeat_interleave(H // Hkv, dim=1), kmax)
+
+
+@pytest.mark.parametrize("version", [1, 2])
+@pytest.mark.parametrize("m,n,H,Hkv,n_req,sort", [
+    (800, 5153, 4, 4, 3, True), (130, 1000, 8, 2, 2, True), (64, 300, 2, 1, 1, True),
+    (1000, 1200, 32, 8, 8, True), (256, 700, 2, 2, 1, False), (383, 900, 4, 4, 2, False)])
+def test_attention_tc_batched_gqa_versions(L, version, m, n, H, Hkv, n_req, sort):
+    """Both tcgen05 attention kernels (1: single tile, P via smem; 2: ping-pong
+    tile pairs, P in TMEM; adjacent and mirrored pairings) on batched, GQA,
+    ragged-M and unsorted-row inputs vs an fp32 torch reference (tol 2e-2)."""
+    torch.manual_seed(m * 7 + n)
+    D = 128
+    q = torch.randn(n_req, m, H, D, device="cuda").bfloat16()
+    k = torch.randn(n_req, n, Hkv, D, device="cuda").bfloat16()
+    v = torch.randn(n_req, n, Hkv, D, device="cuda").bfloat16()
+    kmax = torch.randint(0, n, (n_req, m), device="cuda")
+    if sort:
+        kmax = torch.sort(kmax, dim=1).values
+    kmax = kmax.int().contiguous()
+    out = torch.empty_like(q)
+    L.call("qcf_set_attention_kernel", version)
+    try:
+        L.call("qcf_attention_batched", L.QCF_BF16, p(q), p(k), p(v), p(kmax), m, n_req, H, Hkv, D, n, p(out), S())
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_attention_kernel", 0)
+    for r in range(n_req):
+        ref = _torch_attention_gqa(q[r], k[r], v[r], kmax[r].long())
+        err = (out[r].float() - ref).abs().max().item()
+        assert err < 2e-2, (r, err)
