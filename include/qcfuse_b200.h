@@ -167,6 +167,10 @@ int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v
  * ping-ponging on the tensor core, P kept in TMEM; 0 (default) = 2 when the
  * tile pairs span more than one wave of CTAs, else 1. */
 int qcf_set_attention_kernel(int version);
+/* Tuning knob (process-wide): tcgen05 GEMM tile plan for M > 32. 0 (default) =
+ * wave-quantisation model; 1 = 2-CTA 256x256; 2 = 1-CTA 128x256; 3 = 128x128;
+ * 4 = 128x64 (falls back to auto when the shape does not fit the plan). */
+int qcf_set_gemm_plan(int plan);
 
 /* ---- critical-layer scoring: fusion.py:313-326 + 566-569 ------------------
  * scores[n] = mean_{h,t} softmax_n((q[t,h].k[n,h]) * scale), t over all nq rows
@@ -187,6 +191,19 @@ int qcf_score_batched(int dtype, const void* q, const void* k, int64_t k_req_str
                       int nq, int n_req, int h, int hkv, int d, double scale, int agg_last,
                       int precise, float* scores, void* workspace, size_t ws_bytes,
                       qcf_stream_t stream);
+
+/* ---- comparison policies: CacheBlend / KVShare, fusion.py:352-392 ----
+ * KV deviation of the layer-1 recompute pass: out[n] = sum_h ||new_k - old_k||_2
+ * + sum_h ||new_v - old_v||_2 (float64 norms, f32 out); tables [n][Hkv][D]. */
+int qcf_kv_deviation(int dtype, const void* old_k, const void* old_v, const void* new_k, const void* new_v,
+                     int64_t n, int hkv, int d, float* out, qcf_stream_t stream);
+/* Received attention: out[j] = mean_{h, rows t} softmax_j((q[t,h].k[j]) * scale) over
+ * keys j <= row_pos[t] (model.py:326-338 weights, averaged as fusion.py:390).
+ * q [n_rows][H][D], k [n_keys][Hkv][D]; float64 accumulation; rows are
+ * processed in chunks that fit the caller's workspace (>= 8*(n_keys + H*n_keys + 2H) + 256 B). */
+int qcf_received_attention(int dtype, const void* q, const void* k, int64_t n_keys, int n_rows, int h,
+                           int hkv, int d, double scale, const int32_t* row_pos, float* out,
+                           void* workspace, size_t ws_bytes, qcf_stream_t stream);
 
 /* ---- Top-N selection: fusion.py:141-158 (stable argsort, ties -> lower index)
  * idx_out[0..n_sel) = ascending (1-based + base) positions of the n_sel largest

@@ -536,3 +536,50 @@ def full_prefill_logits(w: Weights, fused: Fused, query) -> np.ndarray:
     """Full computation over [BOS | ctx | query] (fusion.py:496-517 first_logits)."""
     stream = np.concatenate([[BOS_ID], fused.tokens, np.asarray(query, np.int64)])
     return forward_full(w, stream, 0).logits[-1]
+
+
+# --------------------------------------------------------------------------
+# comparison policies (SURVEY §8f rank 4)                   fusion.py:352-411
+# --------------------------------------------------------------------------
+
+def layer1_recompute_pass(w: Weights, fused: Fused):
+    """Layer 1 recomputed for every context token from raw embeddings at its
+    fused position; attention over [BOS | new context K/V], key pos <= row pos
+    (fusion.py:352-373). Returns (new K [n,Hkv,D], new V, weights [H,n,1+n])."""
+    cfg = w.cfg
+    lw = w.layers[0]
+    n = fused.n_ctx
+    H, Hkv, D = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
+    pos = np.arange(1, n + 1, dtype=np.int64)
+    a = layer_norm(w.emb[fused.tokens], lw.ln1_g, lw.ln1_b, cfg.ln_eps)
+    q = rope((a @ lw.wq).reshape(n, H, D), pos, cfg.rope_theta)
+    k = rope((a @ lw.wk).reshape(n, Hkv, D), pos, cfg.rope_theta)
+    v = (a @ lw.wv).reshape(n, Hkv, D)
+    keys = fused.keys[0].copy()
+    vals = fused.values[0].copy()
+    keys[1:], vals[1:] = k, v
+    visible = np.arange(n + 1)[None, :] <= pos[:, None]
+    _, attn = attention(q, keys, vals, visible)
+    return k, v, attn
+
+
+def kv_deviation(fused: Fused, new_k, new_v) -> np.ndarray:
+    """sum_h ||ΔK||_2 + sum_h ||ΔV||_2 per context row, float64 norms -> f32
+    (fusion.py:375-380)."""
+    dk = np.linalg.norm((new_k - fused.keys[0][1:]).astype(np.float64), axis=2).sum(axis=1)
+    dv = np.linalg.norm((new_v - fused.values[0][1:]).astype(np.float64), axis=2).sum(axis=1)
+    return (dk + dv).astype(np.float32)
+
+
+def cacheblend_scores(w: Weights, fused: Fused) -> np.ndarray:
+    """CacheBlend ranking: layer-1 KV deviation (fusion.py:382-386)."""
+    k, v, _ = layer1_recompute_pass(w, fused)
+    return kv_deviation(fused, k, v)
+
+
+def kvshare_scores(w: Weights, fused: Fused) -> np.ndarray:
+    """KVShare ranking: deviation x attention received by each context column,
+    mean over heads and rows (fusion.py:388-392)."""
+    k, v, attn = layer1_recompute_pass(w, fused)
+    received = attn[:, :, 1:].mean(axis=(0, 1))
+    return kv_deviation(fused, k, v) * received.astype(np.float32)

@@ -21,6 +21,7 @@ static bool tc_ok() {
 
 bool tc_available() { return tc_ok(); }
 void set_attention_kernel(int v);
+void set_gemm_plan(int p);
 
 }  // namespace qcf
 
@@ -109,5 +110,11 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
 extern "C" int qcf_set_attention_kernel(int version) {
   QCF_REQUIRE(version >= 0 && version <= 2, QCF_EINVAL, "qcf_set_attention_kernel: version 0 (auto), 1 or 2");
   qcf::set_attention_kernel(version);
+  return QCF_OK;
+}
+
+extern "C" int qcf_set_gemm_plan(int plan) {
+  QCF_REQUIRE(plan >= 0 && plan <= 4, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 4");
+  qcf::set_gemm_plan(plan);
   return QCF_OK;
 }

@@ -624,6 +624,9 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 }
 
 static int g_pair_mode = -1;  // QCF_GEMM_PAIR env: 0 off, 1 on (default on)
+static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64
+
+void set_gemm_plan(int p) { g_gemm_plan = (p >= 0 && p <= 4) ? p : 0; }
 
 // Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
 // weights; A box trimmed to the live rows. Returns splits (1 = no workspace).
@@ -692,6 +695,13 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
   }
   const int sms = sm_count();
   const int64_t mt = (m + TC_BM - 1) / TC_BM;
+  switch (g_gemm_plan) {  // forced plan (tuning / measurement)
+    case 1: if (m >= 192 && n >= 256) return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
+    case 2: if (n >= 256) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
+    case 3: if (n >= 128) return launch_bn<128>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
+    case 4: return launch_bn<64>(ma, b, ldb, c, ldc, m, n, k, ea, s);
+    default: break;
+  }
   // 2-CTA 256-row tiles vs 1-CTA 128-row tiles: estimate each one's useful
   // fraction (wave quantisation x row padding; 1-CTA pays ~15% for its
   // shallower TMA lookahead) and take the better one

@@ -20,7 +20,8 @@ template <typename T, typename Acc>
 __global__ void __launch_bounds__(128) score_logits_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                            int64_t n_ctx, int nq, int t0, int h,
                                                            int hkv, int d, Acc scale,
-                                                           Acc* __restrict__ S) {
+                                                           Acc* __restrict__ S,
+                                                           const int32_t* __restrict__ row_pos) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -60,7 +61,9 @@ __global__ void __launch_bounds__(128) score_logits_kernel(const T* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t n = n0 + tj * 4 + j;
-      if (n < n_ctx) S[((int64_t)head * nt + t) * n_ctx + n] = acc[i][j] * scale;
+      // causal variant (received attention): key n visible to row t iff n <= row_pos[t]
+      const bool vis = !row_pos || n <= (int64_t)row_pos[t0 + t];
+      if (n < n_ctx) S[((int64_t)head * nt + t) * n_ctx + n] = vis ? acc[i][j] * scale : (Acc)-INFINITY;
     }
   }
 }
@@ -104,7 +107,9 @@ template <typename Acc>
 __global__ void __launch_bounds__(256) score_colmean_kernel(const Acc* __restrict__ S, int64_t n_ctx, int rows,
                                                             const Acc* __restrict__ rmax,
                                                             const Acc* __restrict__ rsum,
-                                                            float* __restrict__ scores) {
+                                                            float* __restrict__ scores,
+                                                            Acc* __restrict__ colacc, int first,
+                                                            int last, Acc inv_total) {
   pdl_wait();
   pdl_trigger();
   __shared__ Acc part[8][32];
@@ -121,7 +126,13 @@ __global__ void __launch_bounds__(256) score_colmean_kernel(const Acc* __restric
     Acc t = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += part[w][lane];
-    scores[n] = (float)(t / (Acc)rows);
+    if (colacc) {  // row-chunked column sums (received attention): accumulate, scale at the end
+      t += first ? (Acc)0 : colacc[n];
+      if (last) scores[n] = (float)(t * inv_total);
+      else colacc[n] = t;
+    } else {
+      scores[n] = (float)(t / (Acc)rows);
+    }
   }
 }
 
@@ -143,12 +154,55 @@ static int score_impl(const void* q, const void* k, int64_t n_ctx, int nq, int h
   QCF_REQUIRE(smem <= 220 * 1024, QCF_EUNSUPPORTED, "qcf_score: head dim too large");
   dim3 g1(ceil_div(n_ctx, SC_TILE), h, ceil_div(nt, SC_TQ));
   QCF_LAUNCH("score_logits_kernel", score_logits_kernel<T, Acc>, dim3(g1), dim3(128), smem, s, (const T*)q, (const T*)k, n_ctx, nq, t0, h, hkv,
-                                                    d, (Acc)scale, S);
+                                                    d, (Acc)scale, S, (const int32_t*)nullptr);
   QCF_LAUNCH_CHECK("qcf_score logits");
   QCF_LAUNCH("score_rowstats_kernel", score_rowstats_kernel<Acc>, dim3(rows), dim3(256), 0, s, S, n_ctx, rmax, rsum);
   QCF_LAUNCH_CHECK("qcf_score rowstats");
-  QCF_LAUNCH("score_colmean_kernel", score_colmean_kernel<Acc>, dim3(ceil_div(n_ctx, 32)), dim3(256), 0, s, S, n_ctx, rows, rmax, rsum, scores);
+  QCF_LAUNCH("score_colmean_kernel", score_colmean_kernel<Acc>, dim3(ceil_div(n_ctx, 32)), dim3(256), 0, s, S, n_ctx, rows, rmax, rsum, scores,
+             (Acc*)nullptr, 1, 1, (Acc)0);
   QCF_LAUNCH_CHECK("qcf_score colmean");
+  return QCF_OK;
+}
+
+// Received attention (KVShare, fusion.py:388-392 with the layer-1 pass of
+// 352-373): out[n] = mean over (h, rows) of softmax_n(q[t,h].k[n] * scale) with
+// key n visible to row t iff n <= row_pos[t]. Rows are processed in chunks
+// that fit the workspace; column sums accumulate in Acc across chunks.
+template <typename T, typename Acc>
+static int received_impl(const void* q, const void* k, int64_t n_keys, int n_rows, int h, int hkv, int d,
+                         double scale, const int32_t* row_pos, float* out, void* ws, size_t ws_bytes,
+                         cudaStream_t s) {
+  const size_t per_row = sizeof(Acc) * ((size_t)h * n_keys + 2 * (size_t)h);
+  const size_t fixed = sizeof(Acc) * (size_t)n_keys + 256;
+  QCF_REQUIRE(ws_bytes >= fixed + per_row, QCF_EWORKSPACE, "qcf_received_attention: workspace too small");
+  const int chunk = (int)std::min<size_t>((size_t)n_rows, (ws_bytes - fixed) / per_row);
+  Acc* colacc = reinterpret_cast<Acc*>(ws);
+  Acc* S = colacc + n_keys;
+  const size_t smem = sizeof(Acc) * (size_t)d * (SC_TQ + SC_TILE);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(score_logits_kernel<T, Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "qcf_received_attention attr");
+  }
+  QCF_REQUIRE(smem <= 220 * 1024, QCF_EUNSUPPORTED, "qcf_received_attention: head dim too large");
+  const size_t esz = sizeof(T);
+  for (int r0 = 0; r0 < n_rows; r0 += chunk) {
+    const int nr = std::min(chunk, n_rows - r0);
+    const int rows = h * nr;
+    Acc* rmax = S + (int64_t)rows * n_keys;
+    Acc* rsum = rmax + rows;
+    const void* qc = reinterpret_cast<const uint8_t*>(q) + (size_t)r0 * h * d * esz;
+    dim3 g1(ceil_div(n_keys, SC_TILE), h, ceil_div(nr, SC_TQ));
+    QCF_LAUNCH("score_logits_kernel", score_logits_kernel<T, Acc>, dim3(g1), dim3(128), smem, s, (const T*)qc,
+               (const T*)k, n_keys, nr, 0, h, hkv, d, (Acc)scale, S, row_pos + r0);
+    QCF_LAUNCH_CHECK("qcf_received_attention logits");
+    QCF_LAUNCH("score_rowstats_kernel", score_rowstats_kernel<Acc>, dim3(rows), dim3(256), 0, s, S, n_keys, rmax, rsum);
+    QCF_LAUNCH_CHECK("qcf_received_attention rowstats");
+    QCF_LAUNCH("score_colmean_kernel", score_colmean_kernel<Acc>, dim3(ceil_div(n_keys, 32)), dim3(256), 0, s, S,
+               n_keys, rows, rmax, rsum, out, colacc, r0 == 0 ? 1 : 0, r0 + nr >= n_rows ? 1 : 0,
+               (Acc)(1.0 / ((double)h * n_rows)));
+    QCF_LAUNCH_CHECK("qcf_received_attention colmean");
+  }
   return QCF_OK;
 }
 
@@ -210,4 +264,20 @@ extern "C" int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx,
                          void* workspace, size_t ws_bytes, qcf_stream_t stream) {
   return qcf_score_batched(dtype, q, k, n_ctx * hkv * d, n_ctx, nq, 1, h, hkv, d, scale, agg_last, precise, scores,
                            workspace, ws_bytes, stream);
+}
+
+extern "C" int qcf_received_attention(int dtype, const void* q, const void* k, int64_t n_keys, int n_rows, int h,
+                                      int hkv, int d, double scale, const int32_t* row_pos, float* out,
+                                      void* workspace, size_t ws_bytes, qcf_stream_t stream) {
+  QCF_REQUIRE(q && k && row_pos && out && workspace, QCF_EINVAL, "qcf_received_attention: null pointer");
+  QCF_REQUIRE(n_keys > 0 && n_rows > 0 && h > 0 && hkv > 0 && h % hkv == 0 && d > 0, QCF_EINVAL,
+              "qcf_received_attention: bad sizes");
+  auto s = qcf::as_stream(stream);
+  if (dtype == QCF_F32)
+    return qcf::received_impl<float, double>(q, k, n_keys, n_rows, h, hkv, d, scale, row_pos, out, workspace,
+                                             ws_bytes, s);
+  if (dtype == QCF_BF16)
+    return qcf::received_impl<__nv_bfloat16, double>(q, k, n_keys, n_rows, h, hkv, d, scale, row_pos, out,
+                                                     workspace, ws_bytes, s);
+  QCF_REQUIRE(false, QCF_EINVAL, "qcf_received_attention: bad dtype");
 }

@@ -615,10 +615,61 @@ class FusionEngine:
             return self.qclast_select(query_tokens, fused, ratio)
         if policy == "QCAll":
             return self.qcall_select(query_tokens, fused, ratio)
-        if policy in ("CacheBlend", "KVShare"):
-            raise NotImplementedError(f"{policy} is a comparison baseline outside the fused hot path "
-                                      "(SURVEY §8f rank 4)")
+        if policy == "CacheBlend":
+            return self.cacheblend_select(fused, ratio)
+        if policy == "KVShare":
+            return self.kvshare_select(fused, ratio)
         return self.qcfuse_select(query_tokens, fused, ratio)
+
+    # ---- layer-1 deviation baselines (fusion.py:352-392) on the device
+    def _layer1_recompute_pass(self, fused: FusedContext, want_attention: bool = False):
+        """Layer 1 recomputed for every context token from raw embeddings
+        (fusion.py:352-373): returns (new K [n][Hkv][D], new V, received
+        attention [n] or None). The reference's full attention weights are
+        reduced on the device to what KVShare consumes: their mean over heads
+        and rows for each context column (fusion.py:390)."""
+        cfg, dev, n = self.config, self.device, fused.n_ctx
+        tk = fused.k[0, :n + 1].clone()
+        tv = fused.v[0, :n + 1].clone()
+        pos = torch.arange(1, n + 1, dtype=torch.int32, device=dev)
+        tok = _i32(np.concatenate([[BOS_ID], fused.token_ids]), dev)
+        sc = self.ex.scratch(n, key="layer1")
+        self.ex.embed(sc, n, tok, rows=pos)
+        self.ex.rope.ensure(n + 2)
+        q = torch.empty((n, cfg.n_heads, cfg.d_head), dtype=self.weights.torch_dtype, device=dev)
+        self.ex.layer(0, sc, n, pos, pos, pos, tk, tv, q_only=True, q_out=q)
+        received = None
+        if want_attention:
+            out = torch.empty(n + 1, dtype=torch.float32, device=dev)
+            per_row = 8 * (cfg.n_heads * (n + 1) + 2 * cfg.n_heads)
+            ws = torch.empty(8 * (n + 1) + 256 + per_row * min(n, max(1, (256 << 20) // per_row)),
+                             dtype=torch.uint8, device=dev)
+            scale = 1.0 / float(np.float32(math.sqrt(cfg.d_head)))   # model.py:334 divides by float32(sqrt(D))
+            call("qcf_received_attention", self.weights.qcf_dtype, q.data_ptr(), tk.data_ptr(), n + 1, n,
+                 cfg.n_heads, cfg.n_kv_heads, cfg.d_head, scale, pos.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                 ws.numel(), cuda_stream())
+            received = out[1:]
+        return tk[1:], tv[1:], received
+
+    def _kv_deviation(self, fused: FusedContext, new_k: torch.Tensor, new_v: torch.Tensor) -> torch.Tensor:
+        """fusion.py:375-380 on the device (qcf_kv_deviation)."""
+        cfg, n = self.config, fused.n_ctx
+        out = torch.empty(n, dtype=torch.float32, device=self.device)
+        call("qcf_kv_deviation", self.weights.qcf_dtype, fused.k[0, 1:n + 1].data_ptr(),
+             fused.v[0, 1:n + 1].data_ptr(), new_k.data_ptr(), new_v.data_ptr(), n, cfg.n_kv_heads, cfg.d_head,
+             out.data_ptr(), cuda_stream())
+        return out
+
+    def cacheblend_select(self, fused: FusedContext, ratio: float) -> SelectionResult:
+        """fusion.py:382-386: Top-N of the layer-1 KV deviation."""
+        k, v, _ = self._layer1_recompute_pass(fused)
+        return select_topn(self._kv_deviation(fused, k, v).cpu().numpy(), ratio, "CacheBlend")
+
+    def kvshare_select(self, fused: FusedContext, ratio: float) -> SelectionResult:
+        """fusion.py:388-392: Top-N of deviation x received attention."""
+        k, v, received = self._layer1_recompute_pass(fused, want_attention=True)
+        dev = self._kv_deviation(fused, k, v).cpu().numpy()
+        return select_topn(dev * received.cpu().numpy().astype(np.float32), ratio, "KVShare")
 
     # ------------------------------------------------------------------
     # recomputation (fusion.py:446-490)

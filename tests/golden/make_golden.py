@@ -183,3 +183,48 @@ def extra_fixtures():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "extra":
     extra_fixtures()
+
+
+def baseline_fixtures():
+    """Reference selections of the comparison policies (fusion.py:352-411):
+    CacheBlend / KVShare (layer-1 deviation, received attention), QCLast, QCAll,
+    on the reference conftest config and BASELINE config 1 -> baselines.npz."""
+    model, store_mod, fusion = _import_reference()
+    out = {}
+    cases = [("small", dict(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234), (20, 24, 17), 6, 0.3),
+             ("small2", dict(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234), (33, 12), 4, 0.15),
+             ("tiny", dict(n_layers=4, n_heads=4, d_model=256, d_head=64, d_ff=1024, seed=1234), (128, 128), 16, 0.15)]
+    for name, cfgk, sizes, nq, ratio in cases:
+        cfg = model.ModelConfig(**cfgk)
+        w = model.init_weights(cfg)
+        tmp = Path(tempfile.mkdtemp(prefix="qcf-golden-"))
+        try:
+            st = store_mod.ChunkStore(tmp / "store", cfg)
+            eng = fusion.FusionEngine(w, st)
+            cids, toks_all = [], []
+            for i, n in enumerate(sizes):
+                toks = np.random.default_rng(300 + i).integers(0, 256, n)
+                toks_all.append(toks.astype(np.int64))
+                cids.append(st.precompute(w, [int(t) for t in toks], 0.1, f"c{i}").chunk_id)
+            query = [int(t) for t in np.random.default_rng(900).integers(0, 256, nq)]
+            fused = eng.assemble_context(cids)
+            new_k, new_v, attn = eng._layer1_recompute_pass(fused)
+            dev = eng._kv_deviation(fused, new_k, new_v)
+            out[f"{name}_cfg"] = json.dumps(cfg.to_dict())
+            out[f"{name}_ratio"] = ratio
+            out[f"{name}_query"] = np.asarray(query, np.int64)
+            out[f"{name}_n_chunks"] = len(sizes)
+            for i, t in enumerate(toks_all):
+                out[f"{name}_chunk{i}_tokens"] = t
+            out[f"{name}_deviation"] = dev.astype(np.float32)
+            out[f"{name}_received"] = attn[:, :, 1:].mean(axis=(0, 1)).astype(np.float32)
+            for pol in ("CacheBlend", "KVShare", "QCLast", "QCAll"):
+                out[f"{name}_{pol}"] = eng.select(pol, ratio, fused, query).indices.astype(np.int64)
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+    np.savez_compressed(HERE / "baselines.npz", **out)
+    print("wrote", HERE / "baselines.npz")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "baselines":
+    baseline_fixtures()

@@ -8,6 +8,8 @@ Two anchors:
 The second half restates the reference's own test_fusion.py cases against the
 B200 engine (same assertions, same tolerances)."""
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -395,3 +397,64 @@ def test_gqa_init_bit_exact(tmp_path):
         ref = np.concatenate([ow.layers[li].wq, ow.layers[li].wk, ow.layers[li].wv], axis=1).T
         assert np.array_equal(wqkv, ref)
         assert np.array_equal(w.layers[li].w2.cpu().numpy(), ow.layers[li].w2.T)
+
+
+# ---------------------------------------------------------------- comparison policies
+@pytest.mark.parametrize("name", ["small", "small2", "tiny"])
+def test_baseline_policies_match_reference(tmp_path, name):
+    """CacheBlend / KVShare (layer-1 deviation pass on the GPU) and QCLast /
+    QCAll select exactly the reference's index sets in the f32 parity mode
+    (fixtures: tests/golden/make_golden.py baselines); deviation and received
+    attention within 1e-5 / 1e-6 of the reference's."""
+    import json
+    from pathlib import Path
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    z = np.load(Path(__file__).parent / "golden" / "baselines.npz")
+    d = json.loads(str(z[f"{name}_cfg"]))
+    oc = O.Config(**{k: d[k] for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff", "rope_theta", "ln_eps",
+                                       "seed", "critical_layer")})
+    ow = O.init_weights(oc)
+    chunks = [O.precompute_chunk(ow, z[f"{name}_chunk{i}_tokens"], 0.1) for i in range(int(z[f"{name}_n_chunks"]))]
+    w = device_weights(ow, "f32")
+    store = Q.ChunkStore(tmp_path / "s", w.config, dtype="f32", persist=False)
+    ids = load_oracle_chunks(store, chunks)
+    eng = Q.FusionEngine(w, store)
+    fused = eng.assemble_context(ids)
+    k, v, received = eng._layer1_recompute_pass(fused, want_attention=True)
+    dev = eng._kv_deviation(fused, k, v).cpu().numpy()
+    assert np.allclose(dev, z[f"{name}_deviation"], rtol=1e-5)
+    assert np.abs(received.cpu().numpy() - z[f"{name}_received"]).max() < 1e-6
+    r = float(z[f"{name}_ratio"])
+    q = z[f"{name}_query"].tolist()
+    for pol in ("CacheBlend", "KVShare", "QCLast", "QCAll"):
+        got = eng.select(pol, r, fused, q).indices
+        assert np.array_equal(got, z[f"{name}_{pol}"]), pol
+    res = eng.run("KVShare", r, ids, q, max_new=1)
+    assert np.array_equal(res.selection.indices, z[f"{name}_KVShare"])
+
+
+def test_received_attention_row_chunking(tmp_path):
+    """qcf_received_attention gives the same column means whether all rows fit
+    the workspace or are processed in many chunks (bf16 inputs, GQA)."""
+    from paper_2604_08585_b200 import _lib as L
+    torch.manual_seed(0)
+    n, H, Hkv, D = 300, 8, 2, 128
+    q = (torch.randn(n, H, D, device="cuda") * 0.5).bfloat16()
+    k = (torch.randn(n + 1, Hkv, D, device="cuda") * 0.5).bfloat16()
+    pos = torch.arange(1, n + 1, dtype=torch.int32, device="cuda")
+    outs = []
+    for rows_fit in (n, 7):
+        ws_bytes = 8 * (n + 1) + 256 + rows_fit * 8 * (H * (n + 1) + 2 * H)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        out = torch.empty(n + 1, device="cuda")
+        L.call("qcf_received_attention", L.QCF_BF16, q.data_ptr(), k.data_ptr(), n + 1, n, H, Hkv, D,
+               1.0 / math.sqrt(D), pos.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(),
+               torch.cuda.current_stream().cuda_stream)
+        outs.append(out.cpu().numpy())
+    kk = k.float().repeat_interleave(H // Hkv, dim=1)
+    s = torch.einsum("thd,nhd->htn", q.float(), kk) / math.sqrt(D)
+    mask = torch.arange(n + 1, device="cuda")[None, :] <= pos[:, None]
+    ref = torch.softmax(s.masked_fill(~mask[None], float("-inf")), dim=-1).mean(dim=(0, 1)).cpu().numpy()
+    assert np.abs(outs[0] - ref).max() < 1e-6
+    assert np.abs(outs[1] - outs[0]).max() < 1e-7

@@ -7,6 +7,7 @@ package itself; the known-answer vectors are the reference's own
 """
 
 import hashlib
+from pathlib import Path
 import json
 
 import numpy as np
@@ -119,3 +120,31 @@ def test_ratio_one_equals_full_prefill(golden_dir):
     out = O.run(w, chunks, z["query"], 1.0)
     full = O.full_prefill_logits(w, out.fused, z["query"])
     assert np.abs(out.first_logits - full).max() < 1e-4
+
+
+def _baseline_case(name):
+    import json
+    from oracle import qcfuse_oracle as O
+    z = np.load(Path(__file__).parent / "golden" / "baselines.npz")
+    d = json.loads(str(z[f"{name}_cfg"]))
+    oc = O.Config(**{k: d[k] for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff", "rope_theta", "ln_eps",
+                                       "seed", "critical_layer")})
+    ow = O.init_weights(oc)
+    chunks = [O.precompute_chunk(ow, z[f"{name}_chunk{i}_tokens"], 0.1) for i in range(int(z[f"{name}_n_chunks"]))]
+    return z, oc, ow, chunks, O.assemble(ow, chunks)
+
+
+@pytest.mark.parametrize("name", ["small", "small2", "tiny"])
+def test_oracle_cacheblend_kvshare_vs_reference(name):
+    """Oracle restatement of the layer-1 deviation policies reproduces the
+    reference's deviations / received attention and its CacheBlend/KVShare
+    index sets (fixtures by tests/golden/make_golden.py baselines)."""
+    from oracle import qcfuse_oracle as O
+    z, oc, ow, chunks, fused = _baseline_case(name)
+    k, v, attn = O.layer1_recompute_pass(ow, fused)
+    dev = O.kv_deviation(fused, k, v)
+    assert np.allclose(dev, z[f"{name}_deviation"], rtol=1e-5)
+    assert np.allclose(attn[:, :, 1:].mean(axis=(0, 1)), z[f"{name}_received"], rtol=1e-4, atol=1e-7)
+    r = float(z[f"{name}_ratio"])
+    assert np.array_equal(O.select_topn(O.cacheblend_scores(ow, fused), r), z[f"{name}_CacheBlend"])
+    assert np.array_equal(O.select_topn(O.kvshare_scores(ow, fused), r), z[f"{name}_KVShare"])

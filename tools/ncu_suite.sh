@@ -1,19 +1,28 @@
 #!/bin/bash
-# Profiling pass for profiles/: launch list of one fused prefill + ncu --set full
-# of each GEMM shape and the attention kernel. Run under gpurun.
+# Profiling pass for profiles/ (run under gpurun, one GPU):
+#   launches_b8.csv / launches_b1.csv : ncu --metrics gpu__time_duration.sum --clock-control none
+#       launch lists of the bench's batched step (8 requests) and of one request alone
+#   gemm_<m>x<n>x<k>.csv : ncu --set full of each GEMM shape of the batched step
+#   <kernel>.ncu-rep      : ncu --set full of attention / scoring / LayerNorm / assembly / Top-N
+#       inside the batched step
 set -x
 OUT=gpurun_out/ncu
 mkdir -p $OUT
 ncu --nvtx --nvtx-include "profile_step/" --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $OUT/launches.csv python tools/profile_step.py > $OUT/launches.log 2>&1
-for shape in "800 12288 4096 9" "800 4096 4096 2" "800 14336 4096 1" "800 4096 14336 2" \
-             "32 12288 4096 0" "32 4096 4096 2" "32 14336 4096 1" "32 4096 14336 2"; do
+    --log-file $OUT/launches_b8.csv python tools/profile_step.py llama3-8b QCFuse 8 > $OUT/launches_b8.log 2>&1
+ncu --nvtx --nvtx-include "profile_step/" --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches_b1.csv python tools/profile_step.py llama3-8b QCFuse 1 > $OUT/launches_b1.log 2>&1
+for shape in "6400 12288 4096 9" "6400 4096 4096 2" "6400 14336 4096 1" "6400 4096 14336 2" \
+             "256 12288 4096 0" "256 4096 4096 2" "256 14336 4096 1" "256 4096 14336 2" \
+             "800 12288 4096 9" "800 4096 4096 2" "800 14336 4096 1" "800 4096 14336 2"; do
   set -- $shape
   ncu --set full --clock-control none -k regex:"gemm_tc|splitk" -s 2 -c 2 --csv --page raw \
       python tools/one_gemm.py $1 $2 $3 $4 > $OUT/gemm_$1x$2x$3.csv 2> /dev/null
 done
-ncu --nvtx --nvtx-include "profile_step/" --set full --import-source on --clock-control none -k regex:attn_tc -s 15 -c 1 \
-    -o $OUT/attn python tools/profile_step.py > /dev/null 2>&1
-ncu --nvtx --nvtx-include "profile_step/" --set full --clock-control none -k regex:assemble -c 1 \
-    -o $OUT/assemble python tools/profile_step.py > /dev/null 2>&1
+for k in "attn:attn_tc2:15" "score1:score_tc_kernel:0" "score2:score_tc_kernel:1" "layernorm:layernorm:40" \
+         "assemble:assemble:0" "topn:topn:0"; do
+  IFS=: read name regex skip <<< "$k"
+  ncu --nvtx --nvtx-include "profile_step/" --set full --import-source on --clock-control none -k regex:$regex \
+      -s $skip -c 1 -o $OUT/$name python tools/profile_step.py llama3-8b QCFuse 8 > /dev/null 2>&1
+done
 ls -la $OUT

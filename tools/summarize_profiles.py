@@ -19,8 +19,8 @@ def raw_rows(text):
     return rows[i], rows[i + 2:] if len(rows) > i + 2 and rows[i + 1] and rows[i + 1][0] == "" else rows[i + 1:]
 
 
-def launch_list():
-    rows = list(csv.reader((SRC / "launches.csv").read_text().splitlines()))
+def launch_list(fname="launches.csv"):
+    rows = list(csv.reader((SRC / fname).read_text().splitlines()))
     i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, data = rows[i], rows[i + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -115,20 +115,34 @@ def rep_summary(name, keys):
 
 
 if __name__ == "__main__":
-    ll = launch_list()
-    (OUT / f"{TAG}_launches_summary.json").write_text(json.dumps(ll, indent=1))
-    (OUT / f"{TAG}_launches.csv").write_text((SRC / "launches.csv").read_text())
+    lists = {}
+    for fname, label in (("launches_b8.csv", "b8"), ("launches_b1.csv", "b1"), ("launches.csv", "")):
+        if (SRC / fname).exists():
+            ll = launch_list(fname)
+            suffix = f"_{label}" if label else ""
+            (OUT / f"{TAG}_launches{suffix}_summary.json").write_text(json.dumps(ll, indent=1))
+            (OUT / f"{TAG}_launches{suffix}.csv").write_text((SRC / fname).read_text())
+            lists[label or "step"] = ll
     gt = gemm_table()
     (OUT / f"{TAG}_gemm_ncu.json").write_text(json.dumps(gt, indent=1))
     keys = ["Kernel Name", "launch__grid_size", "gpu__time_duration.sum", "dram__bytes_read.sum",
             "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
-            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_active.avg"]
-    other = {n: rep_summary(n, keys) for n in ("attn", "assemble")}
-    (OUT / f"{TAG}_attn_assemble_ncu.json").write_text(json.dumps(other, indent=1))
-    # per-launch DRAM traffic of the GEMM family over one step (weights x shape counts)
-    counts = {"800x12288x4096": 32, "800x4096x4096": 32, "800x14336x4096": 32, "800x4096x14336": 32,
-              "32x12288x4096": 16, "32x4096x4096": 15, "32x14336x4096": 15, "32x4096x14336": 15}
+            "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_active.avg",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "smsp__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__average_warp_latency_issue_stalled_long_scoreboard", "launch__registers_per_thread"]
+    names = [p.stem for p in sorted(SRC.glob("*.ncu-rep"))]
+    other = {n: rep_summary(n, keys) for n in names}
+    (OUT / f"{TAG}_kernels_ncu.json").write_text(json.dumps(other, indent=1))
+    # per-launch DRAM traffic of the GEMM family over the bench's batched step
+    counts = {"6400x12288x4096": 32, "6400x4096x4096": 32, "6400x14336x4096": 32, "6400x4096x14336": 32,
+              "256x12288x4096": 16, "256x4096x4096": 15, "256x14336x4096": 15, "256x4096x14336": 15}
+    if not any(k in gt for k in counts):
+        counts = {"800x12288x4096": 32, "800x4096x4096": 32, "800x14336x4096": 32, "800x4096x14336": 32,
+                  "32x12288x4096": 16, "32x4096x4096": 15, "32x14336x4096": 15, "32x4096x14336": 15}
     tot_b = tot_n = 0
     for k, c in counts.items():
         if k in gt and gt[k]["dram_read_MB"] is not None:
@@ -137,7 +151,8 @@ if __name__ == "__main__":
     if tot_n:
         (OUT / "gemm_traffic.json").write_text(json.dumps(
             {"bytes_per_launch": tot_b / tot_n, "source": f"profiles/{TAG}_gemm_ncu.json (ncu --set full, cold L2), "
-             "weighted by the per-step launch count of each shape"}, indent=1))
-    print(json.dumps(ll["kernels"], indent=1)[:3000])
-    print(json.dumps(gt, indent=1)[:4000])
+             "weighted by the per-step launch count of each shape of the bench's step"}, indent=1))
+    for k, ll in lists.items():
+        print(k, json.dumps(ll["kernels"], indent=1)[:2500])
+    print(json.dumps(gt, indent=1)[:6000])
     print(json.dumps(other, indent=1))
