@@ -119,10 +119,14 @@ int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dt
 int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
              void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue,
              int out_dtype, qcf_stream_t stream);
-/* Same contract with a caller-owned workspace: skinny M (the probe's q rows)
- * splits K across CTAs so the weights stream at HBM rate; partials are summed
- * in a fixed order (deterministic). ws may be NULL when qcf_gemm_workspace()
- * returns 0. */
+/* Same contract with a caller-owned workspace (qcf_gemm_workspace() bytes,
+ * ZERO-FILLED once before first use; the kernels leave its flag words zeroed):
+ *  - skinny M (the probe's q rows) splits K across CTAs so the weights stream
+ *    at HBM rate; partials are summed in a fixed order (deterministic);
+ *  - opt-in (qcf_set_gemm_plan +8) stream-K for the 2-CTA kernel: equal k-block
+ *    ranges per CTA pair, split tiles fixed up through the workspace in
+ *    cluster order (deterministic).
+ * ws may be NULL (no split-K / stream-K). */
 size_t qcf_gemm_workspace(int64_t m, int64_t n, int64_t k);
 int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
                 int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout, void* ws,
@@ -149,7 +153,7 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
 int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m, int64_t k,
                       int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
                       const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
-                      void* k_tab, void* v_tab, qcf_stream_t stream);
+                      void* k_tab, void* v_tab, void* ws, size_t ws_bytes, qcf_stream_t stream);
 
 /* ---- location-aware attention: fusion.py:194-208 -> model.py:326-338 -------
  * out[i,h] = sum_{j<=kmax[i]} softmax_j(q[i,h].k[j,h/(H/Hkv)] / float(sqrt(D))) v[j]
@@ -169,7 +173,8 @@ int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v
 int qcf_set_attention_kernel(int version);
 /* Tuning knob (process-wide): tcgen05 GEMM tile plan for M > 32. 0 (default) =
  * wave-quantisation model; 1 = 2-CTA 256x256; 2 = 1-CTA 128x256; 3 = 128x128;
- * 4 = 128x64 (falls back to auto when the shape does not fit the plan). */
+ * 4 = 128x64 (falls back to auto when the shape does not fit the plan);
+ * +8 = stream-K schedule for the 2-CTA kernel (off by default: slower here). */
 int qcf_set_gemm_plan(int plan);
 
 /* ---- critical-layer scoring: fusion.py:313-326 + 566-569 ------------------

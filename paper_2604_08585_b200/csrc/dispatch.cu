@@ -83,9 +83,13 @@ extern "C" int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b,
   }
   if (b_layout == QCF_B_TILE64) {
     QCF_REQUIRE(dtype == QCF_BF16 && qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_ws: tile-major B needs tcgen05");
-    st = qcf::gemm_tc_launch(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s, 1);
+    st = qcf::gemm_tc_launch(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s, 1, ws, ws_bytes);
     if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_ws: shape not covered for tile-major B");
     return st;
+  }
+  if (dtype == QCF_BF16 && qcf::tc_ok()) {
+    st = qcf::gemm_tc_launch(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s, 0, ws, ws_bytes);
+    if (st != QCF_EUNSUPPORTED) return st;
   }
   return qcf_gemm(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, stream);
 }
@@ -93,7 +97,7 @@ extern "C" int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b,
 extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m,
                                  int64_t k, int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
                                  const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
-                                 void* k_tab, void* v_tab, qcf_stream_t stream) {
+                                 void* k_tab, void* v_tab, void* ws, size_t ws_bytes, qcf_stream_t stream) {
   (void)n_pos;
   QCF_REQUIRE(a && w && pos && dst_rows && cos_tbl && sin_tbl && q_out && k_tab && v_tab, QCF_EINVAL,
               "qcf_gemm_qkv_rope: null pointer");
@@ -102,7 +106,7 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
   if (m == 0) return QCF_OK;
   QCF_REQUIRE(qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_qkv_rope: needs an sm_100 device");
   const int st = qcf::gemm_qkv_rope_launch(a, lda, w, ldb, m, k, h, hkv, d, pos, dst_rows, cos_tbl, sin_tbl,
-                                           q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout);
+                                           q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout, ws, ws_bytes);
   if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, m > 32, alignment)");
   return st;
 }
@@ -114,7 +118,7 @@ extern "C" int qcf_set_attention_kernel(int version) {
 }
 
 extern "C" int qcf_set_gemm_plan(int plan) {
-  QCF_REQUIRE(plan >= 0 && plan <= 4, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 4");
+  QCF_REQUIRE((plan & 7) <= 4 && plan >= 0 && plan < 16, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 4, +8 = stream-K on");
   qcf::set_gemm_plan(plan);
   return QCF_OK;
 }

@@ -28,7 +28,14 @@ using namespace sm100;
 constexpr int TC_BM = 128, TC_BK = 64;
 constexpr int TC_THREADS = 192;
 
-constexpr int QCF_EPI_ROPE_QKV = 3;  // internal: RoPE + KV scatter epilogue of the QKV GEMM
+constexpr int QCF_EPI_ROPE_QKV = 3;
+// Stream-K for the 2-CTA kernel: OFF by default. Measured on B200 (tools/gemm_plans.py):
+// the contiguous per-cluster k-ranges lose the L2 sharing of weight k-slices that
+// the data-parallel schedule gets from clusters running the same n-tile in
+// lockstep, and the owner's fix-up waits for clusters that finish last; at the
+// fused-path shapes it was 5-60% slower. qcf_set_gemm_plan(+8) turns it on.
+static int g_streamk = 0;
+static int g_group_m = -1;  // raster group (m pairs) of the 2-CTA kernel; QCF_GEMM_GROUP env  // internal: RoPE + KV scatter epilogue of the QKV GEMM
 
 struct EpiArgs {
   int kind, out_dtype;
@@ -308,10 +315,54 @@ struct Tc2Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
+// Stream-K (sk = 1): the pair's work is the contiguous range of global k-block
+// iterations [c*T/P, (c+1)*T/P) over all (unit, k-block) pairs (T = units x
+// k-blocks, P = clusters), so every cluster does the same number of MMAs and no
+// wave is partially idle. A unit split across clusters is finished by the
+// cluster that computed its FIRST k-blocks (it reaches them last, at the end of
+// its range): later clusters spill their fp32 pieces to `sk_part` (one slot per
+// CTA; a cluster spills at most its first segment) and raise a flag; the owner
+// waits for the flags, adds the pieces in cluster order (deterministic), applies
+// the epilogue and clears the flags for the next launch.
+struct SegIter {
+  int64_t g, g1;        // stream-K: global iteration range
+  int u, u_stride, n_units, kb_units;
+  bool sk;
+  __device__ __forceinline__ bool next(int& unit, int& kb0, int& kb1) {
+    if (sk) {
+      if (g >= g1) return false;
+      unit = (int)(g / kb_units);
+      kb0 = (int)(g - (int64_t)unit * kb_units);
+      { const int64_t e = (int64_t)kb0 + (g1 - g); kb1 = e < kb_units ? (int)e : kb_units; }
+      g += kb1 - kb0;
+      return true;
+    }
+    if (u >= n_units) return false;
+    unit = u;
+    kb0 = 0;
+    kb1 = kb_units;
+    u += u_stride;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea) {
+                void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int sk,
+                int* __restrict__ sk_flags, float* __restrict__ sk_part, int group_m) {
   using Cfg = Tc2Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -330,6 +381,31 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const int n_tiles = (N + BN - 1) / BN;
   const int n_work = m_pairs * n_tiles;
   const int k_blocks = (K + TC_BK - 1) / TC_BK;
+  const int64_t T = (int64_t)n_work * k_blocks;
+  // unit -> (m pair, n tile): m fastest inside groups of `group_m` m pairs, so a
+  // wave of clusters covers a compact (group_m x ~clusters/group_m) block of the
+  // output: both its A rows and its weight columns stay L2-resident
+  const int gsz = min(group_m, m_pairs);
+  auto coords = [&](int w, int& mp, int& nb) {
+    const int grp = w / (gsz * n_tiles);
+    const int first = grp * gsz;
+    const int gm = min(gsz, m_pairs - first);
+    const int idx = w - grp * gsz * n_tiles;
+    mp = first + idx % gm;
+    nb = idx / gm;
+  };
+  auto sk_start = [&](int c) -> int64_t { return (int64_t)c * T / n_clusters; };
+  auto segs = [&]() {
+    SegIter it;
+    it.g = sk_start(cluster);
+    it.g1 = sk_start(cluster + 1);
+    it.u = cluster;
+    it.u_stride = n_clusters;
+    it.n_units = n_work;
+    it.kb_units = k_blocks;
+    it.sk = sk != 0;
+    return it;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -349,11 +425,14 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       uint32_t it = 0;
-      for (int w = cluster; w < n_work; w += n_clusters) {
-        const int mp = w % m_pairs, nb = w / m_pairs;
+      SegIter sg = segs();
+      int w, kbs, kbe;
+      while (sg.next(w, kbs, kbe)) {
+        int mp, nb;
+        coords(w, mp, nb);
         const int arow = mp * 2 * TC_BM + rank * TC_BM;
         const int brow = nb * BN + rank * (BN / 2);
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        for (int kb = kbs; kb < kbe; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
           const uint32_t ph = (it / Cfg::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -370,12 +449,14 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
       constexpr uint32_t idesc = idesc_bf16_f32(2 * TC_BM, BN);
       uint32_t it = 0, t = 0;
-      for (int w = cluster; w < n_work; w += n_clusters, ++t) {
+      SegIter sg = segs();
+      int w, kbs, kbe;
+      for (; sg.next(w, kbs, kbe); ++t) {
         const int acc = t & 1;
         mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        for (int kb = kbs; kb < kbe; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
           const uint32_t ph = (it / Cfg::STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -384,7 +465,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           const uint64_t b0 = umma_desc_k_sw128(sB + s * Cfg::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk)
-            mma_bf16_pair(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            mma_bf16_pair(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
+                          (kb > kbs || kk) ? 1u : 0u);
           mma_commit_pair(&empty[s]);
         }
         mma_commit_pair(&tfull[acc]);
@@ -395,24 +477,76 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
     uint32_t t = 0;
-    for (int w = cluster; w < n_work; w += n_clusters, ++t) {
-      const int mp = w % m_pairs, nb = w / m_pairs;
+    SegIter sg = segs();
+    int w, kbs, kbe;
+    const int et = threadIdx.x - 64;  // 0..127 within the epilogue warps
+    for (; sg.next(w, kbs, kbe); ++t) {
+      int mp, nb;
+      coords(w, mp, nb);
       const int acc = t & 1;
-      const int row = mp * 2 * TC_BM + rank * TC_BM + g * 32 + lane;
+      const int rt = g * 32 + lane;  // row within this CTA's 128
+      const int row = mp * 2 * TC_BM + rank * TC_BM + rt;
       const bool row_ok = row < M;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
+      if (kbs != 0) {
+        // ---- a later piece of a split unit: spill the fp32 partial, raise the flag
+        float* dst = sk_part + ((int64_t)(cluster * 2 + rank) * TC_BM + rt) * BN;
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(g * 32) << 16), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(reinterpret_cast<float4*>(dst + cc * 32 + j),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) st_release(&sk_flags[cluster * 2 + rank], 1);
+        continue;
+      }
+      // ---- owner (or whole unit): gather the later pieces of this unit, if any
+      int c_last = cluster;
+      if (kbe != k_blocks) {
+        const int64_t unit_end = (int64_t)(w + 1) * k_blocks;
+        while (c_last + 1 < n_clusters && sk_start(c_last + 1) < unit_end) ++c_last;
+        if (et == 0)
+          for (int c2 = cluster + 1; c2 <= c_last; ++c2)
+            while (ld_acquire(&sk_flags[c2 * 2 + rank]) == 0) {}
+        named_bar_sync(1, 128);
+      }
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
         uint32_t r[32];
         tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(g * 32) << 16), r);
         tmem_ld_wait();
+        for (int c2 = cluster + 1; c2 <= c_last; ++c2) {
+          const float* src = sk_part + ((int64_t)(c2 * 2 + rank) * TC_BM + rt) * BN + cc * 32;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 p4 = __ldcg(reinterpret_cast<const float4*>(src + j));
+            r[j] = __float_as_uint(__uint_as_float(r[j]) + p4.x);
+            r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) + p4.y);
+            r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) + p4.z);
+            r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + p4.w);
+          }
+        }
         const int col0 = nb * BN + cc * 32;
         if (!row_ok || col0 >= N) continue;
         epilogue_row32(C, ldc, row, col0, N, r, ea);
       }
       tc_fence_before();
       mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      if (c_last > cluster) {  // every thread is done with the pieces: re-arm the flags
+        named_bar_sync(1, 128);
+        if (et == 0)
+          for (int c2 = cluster + 1; c2 <= c_last; ++c2) sk_flags[c2 * 2 + rank] = 0;
+      }
     }
   }
   tc_fence_before();
@@ -588,9 +722,13 @@ static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c,
   return QCF_OK;
 }
 
+// stream-K workspace: [flags: 4 KB][fp32 partial 128x256 per CTA of the grid]
+static size_t sk_bytes() { return 4096 + (size_t)(sm_count() & ~1) * TC_BM * 256 * sizeof(float); }
+
 template <int BN>
 static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                       int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+                       int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, void* ws = nullptr,
+                       size_t ws_bytes = 0) {
   CUtensorMap mb;
   int st = make_b_map(&mb, b, n, k, ldb, BN / 2, ea.b_tiled);
   if (st != QCF_OK) return st;
@@ -601,8 +739,19 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc2 attr");
     attr_set = true;
   }
+  if (g_group_m < 0) {
+    const char* e = getenv("QCF_GEMM_GROUP");
+    g_group_m = e ? atoi(e) : 0;
+  }
   const int64_t work = ((m + 2 * TC_BM - 1) / (2 * TC_BM)) * ((n + BN - 1) / BN);
-  const int clusters = (int)std::min<int64_t>(work, sm_count() / 2);
+  const int64_t iters = work * ((k + TC_BK - 1) / TC_BK);
+  // stream-K when the caller's workspace holds the flags + partials and the unit
+  // count does not fill whole waves of clusters
+  const int sk = (ws && ws_bytes >= sk_bytes() && g_streamk && (work % (sm_count() / 2)) != 0 &&
+                  iters >= 8 * (sm_count() / 2)) ? 1 : 0;
+  const int clusters = sk ? sm_count() / 2 : (int)std::min<int64_t>(work, sm_count() / 2);
+  int* sk_flags = sk ? reinterpret_cast<int*>(ws) : nullptr;
+  float* sk_part = sk ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + 4096) : nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(TC_THREADS);
@@ -617,7 +766,11 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea);
+  // raster band of m pairs (QCF_GEMM_GROUP); default = all m pairs (m fastest). Bands
+  // of 4-12 were within run-to-run noise at the fused-path shapes (tools/group_sweep.sh)
+  const int group_m = g_group_m > 0 ? g_group_m : (int)((m + 2 * TC_BM - 1) / (2 * TC_BM));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea, sk, sk_flags,
+                                     sk_part, group_m);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 pair)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 pair)");
   return QCF_OK;
@@ -626,7 +779,11 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 static int g_pair_mode = -1;  // QCF_GEMM_PAIR env: 0 off, 1 on (default on)
 static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64
 
-void set_gemm_plan(int p) { g_gemm_plan = (p >= 0 && p <= 4) ? p : 0; }
+void set_gemm_plan(int p) {
+  g_streamk = (p & 8) ? 1 : 0;  // +8: stream-K on (measurement)
+  p &= 7;
+  g_gemm_plan = (p >= 0 && p <= 4) ? p : 0;
+}
 
 // Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
 // weights; A box trimmed to the live rows. Returns splits (1 = no workspace).
@@ -638,9 +795,10 @@ static int skinny_splits(int64_t m, int64_t n, int64_t k) {
   return sp;
 }
 
+// [stream-K flags + partials][skinny split-K partials]
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   const int sp = skinny_splits(m, n, k);
-  return sp > 1 ? (size_t)sp * m * n * sizeof(float) : 0;
+  return sk_bytes() + (sp > 1 ? (size_t)sp * m * n * sizeof(float) : 0);
 }
 
 int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
@@ -655,31 +813,34 @@ int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void*
   int st = make_kmajor_map(&ma, a, m, k, lda, box);
   if (st != QCF_OK) return st;
   return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s, sp, box,
-                             (float*)ws);
+                             reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + sk_bytes()));
 }
 
 static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
-                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s);
+                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, void* ws,
+                             size_t ws_bytes);
 
 int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                   int64_t n, int64_t k, int epilogue, int out_dtype, cudaStream_t s, int b_layout) {
-  return gemm_tc_launch_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s);
+                   int64_t n, int64_t k, int epilogue, int out_dtype, cudaStream_t s, int b_layout, void* ws,
+                   size_t ws_bytes) {
+  return gemm_tc_launch_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s, ws, ws_bytes);
 }
 
 int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k, int h,
                          int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
                          const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
-                         int b_layout) {
+                         int b_layout, void* ws, size_t ws_bytes) {
   if (d % 32 || m <= 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
   if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab) & 15) return QCF_EUNSUPPORTED;
   EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
-  return gemm_tc_launch_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, s);
+  return gemm_tc_launch_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, s, ws, ws_bytes);
 }
 
 static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
-                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+                             int64_t m, int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, void* ws,
+                             size_t ws_bytes) {
   const int out_dtype = ea.out_dtype;
   // TMA: 16-byte aligned bases and row strides; vector epilogue alignment
   if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
@@ -696,7 +857,7 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
   const int sms = sm_count();
   const int64_t mt = (m + TC_BM - 1) / TC_BM;
   switch (g_gemm_plan) {  // forced plan (tuning / measurement)
-    case 1: if (m >= 192 && n >= 256) return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
+    case 1: if (m >= 192 && n >= 256) return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes); break;
     case 2: if (n >= 256) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
     case 3: if (n >= 128) return launch_bn<128>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
     case 4: return launch_bn<64>(ma, b, ldb, c, ldc, m, n, k, ea, s);
@@ -712,7 +873,7 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
     const int64_t t1 = mt * ((n + 255) / 256);
     const double e_one = 0.85 * (double)t1 / (double)(((t1 + sms - 1) / sms) * sms) * (double)m / (double)(mt * 128);
     if (units >= clusters / 2 && e_pair >= e_one)
-      return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s);
+      return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes);
   }
   // tile width: enough tiles to cover the SMs, widest tile otherwise
   if (n >= 256 && mt * ((n + 255) / 256) >= sms) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, ea, s);

@@ -31,7 +31,7 @@ class Scratch:
     q: torch.Tensor      # dt  [cap, H, D] rotated queries
     o: torch.Tensor      # dt  [cap, H*D] attention output
     hid: torch.Tensor    # dt  [cap, F]   relu(W1 x)
-    ws: torch.Tensor     # u8  split-K workspace of the skinny-M GEMMs
+    ws: torch.Tensor     # u8  GEMM workspace: stream-K flags/partials + skinny split-K partials
     delta: torch.Tensor  # f32 [cap, d] projection output awaiting its residual add
     pending: bool = False  # delta not yet added into x (launch-sequencing state)
 
@@ -65,7 +65,8 @@ class Executor:
                         torch.empty(cap, H, D, dtype=dt, device=dev),
                         torch.empty(cap, H * D, dtype=dt, device=dev),
                         torch.empty(cap, cfg.d_ff, dtype=dt, device=dev),
-                        torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev),
+                        # zero-filled once: the stream-K flag words must start at 0 (qcf_gemm_ws)
+                        torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev),
                         torch.empty(cap, cfg.d_model, dtype=torch.float32, device=dev))
             self._scratch[k] = s
         return s
@@ -121,7 +122,7 @@ class Executor:
             # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue
             call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, self.w.b_layout, m, d, H, Hkv, D,
                  pos.data_ptr(), dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(),
-                 self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), s)
+                 self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), sc.ws.data_ptr(), sc.ws.numel(), s)
         else:
             self.gemm(sc, sc.a, d, lw.wqkv, d, sc.qkv, nq, m, nq, d, EPI_STORE, QCF_F32, s)
             call("qcf_rope_qkv_scatter", sc.qkv.data_ptr(), m, H, Hkv, D, pos.data_ptr(),

@@ -274,7 +274,7 @@ def test_gemm_skinny_splitk_deterministic(L, m, n, k, epi):
     b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
     out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
     c0 = torch.randn(m, n, device="cuda")
-    ws = torch.empty(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
     outs = []
     for _ in range(2):
         c = c0.clone() if epi == 2 else torch.empty(m, n, device="cuda",
@@ -308,7 +308,7 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads):
     k1 = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
     v1 = torch.zeros_like(k1)
     L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
-           rope.n_pos, p(q1), p(k1), p(v1), S())
+           rope.n_pos, p(q1), p(k1), p(v1), None, 0, S())
     qkv = torch.empty(m, N, device="cuda")
     L.call("qcf_gemm", L.QCF_BF16, p(a), K, p(w), K, p(qkv), N, m, N, K, 0, L.QCF_F32, S())
     q2, k2, v2 = torch.zeros_like(q1), torch.zeros_like(k1), torch.zeros_like(v1)
@@ -333,7 +333,7 @@ def test_gemm_tile_major_weights_match_row_major(L, m, n, k, epi):
     assert torch.equal(untile64(bt), b)
     out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
     tdt = torch.bfloat16 if epi == 1 else torch.float32
-    ws = torch.empty(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
     c1 = torch.empty(m, n, device="cuda", dtype=tdt)
     c2 = torch.empty(m, n, device="cuda", dtype=tdt)
     L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(b), k, p(c1), n, m, n, k, epi, out_dt, 0, p(ws), ws.numel(), S())
@@ -451,3 +451,40 @@ def test_attention_tc_batched_gqa_versions(L, version, m, n, H, Hkv, n_req, sort
         ref = _torch_attention_gqa(q[r], k[r], v[r], kmax[r].long())
         err = (out[r].float() - ref).abs().max().item()
         assert err < 2e-2, (r, err)
+
+
+@pytest.mark.parametrize("m,n,k,epi", [(800, 4096, 4096, 0), (800, 12288, 4096, 0), (800, 4096, 14336, 0),
+                                       (800, 14336, 4096, 1), (6400, 4096, 4096, 0), (1100, 2048, 1024, 1),
+                                       (300, 4096, 8192, 0)])
+def test_gemm_stream_k_matches_data_parallel(L, m, n, k, epi):
+    """2-CTA stream-K (equal k-block ranges per CTA pair, split tiles fixed up
+    through the zeroed workspace in cluster order) equals the data-parallel
+    schedule to fp32 rounding, matches an fp32 torch reference, is bit-identical
+    across repeated launches (flags re-armed), and leaves the flag words zero."""
+    from paper_2604_08585_b200.model import tile64
+    torch.manual_seed(m + n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bt = tile64(b)
+    out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
+    tdt = torch.bfloat16 if epi == 1 else torch.float32
+    ws = torch.zeros(int(L.lib.qcf_gemm_workspace(m, n, k)), dtype=torch.uint8, device="cuda")
+    outs = []
+    try:
+        for plan in (1 + 8, 1 + 8, 1 + 8, 1):   # forced 2-CTA plan; +8 = stream-K on
+            L.call("qcf_set_gemm_plan", plan)
+            c = torch.full((m, n), 7.0, device="cuda", dtype=tdt)
+            L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(bt), k, p(c), n, m, n, k, epi, out_dt, 1, p(ws), ws.numel(),
+                   S())
+            outs.append(c)
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_gemm_plan", 0)
+    ref = a.float() @ b.float().t()
+    if epi == 1:
+        ref = ref.relu()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    tol = 2e-2 if epi == 1 else 1e-3
+    assert (outs[0].float() - ref).abs().max().item() < tol * max(1.0, ref.abs().max().item())
+    assert (outs[0].float() - outs[3].float()).abs().max().item() < tol * max(1.0, ref.abs().max().item())
+    assert int(ws[:4096].view(torch.int32).abs().sum().item()) == 0

@@ -15,7 +15,7 @@ b = tile64(b) if LAY else b
 for m in (32, 128, 256, 384, 512, 800, 1024, 1536):
     a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
     c = torch.empty(m, n, device="cuda")
-    ws = torch.empty(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
     f = lambda: _lib.call("qcf_gemm_ws", 1, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, 0, 0, LAY,
                           ws.data_ptr(), ws.numel(), s)
     f(); torch.cuda.synchronize()

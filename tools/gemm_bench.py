@@ -23,7 +23,7 @@ for m, n, k, epi, name in SHAPES:
     b = tile64(b) if LAY else b
     out_dt = _lib.QCF_BF16 if epi == 1 else _lib.QCF_F32
     c = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16 if epi == 1 else torch.float32)
-    ws = torch.empty(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
     f = lambda: _lib.call("qcf_gemm_ws", _lib.QCF_BF16, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, epi, out_dt, LAY, ws.data_ptr(), ws.numel(), s)
     for _ in range(3): f()
     torch.cuda.synchronize()
