@@ -148,7 +148,9 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
 /* Fused QKV projection + RoPE + KV scatter (bf16, tcgen05): the projection
  * a[M,K] . w[(H+2Hkv)D, K]^T never touches HBM in fp32; its epilogue rotates
  * Q/K at pos[i] and writes q_out[i], k_tab[dst_rows[i]], v_tab[dst_rows[i]].
- * Returns QCF_EUNSUPPORTED when d % 32 != 0 or m <= 32 (callers then use
+ * M <= 32 (the probe's query rows) with a workspace (qcf_gemm_workspace, zeroed):
+ * split-K weight streaming, the rotation + scatter applied in the split-K
+ * reduction. Returns QCF_EUNSUPPORTED when d % 32 != 0 (callers then use
  * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478. */
 int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m, int64_t k,
                       int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,

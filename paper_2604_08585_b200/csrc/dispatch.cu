@@ -107,7 +107,7 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
   QCF_REQUIRE(qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_qkv_rope: needs an sm_100 device");
   const int st = qcf::gemm_qkv_rope_launch(a, lda, w, ldb, m, k, h, hkv, d, pos, dst_rows, cos_tbl, sin_tbl,
                                            q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout, ws, ws_bytes);
-  if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, m > 32, alignment)");
+  if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, alignment)");
   return st;
 }
 

@@ -557,11 +557,15 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   }
 }
 
-// deterministic split-K reduction: C = epi(sum_s partial[s]) in split order
+// deterministic split-K reduction: C = epi(sum_s partial[s]) in split order.
+// Epilogues: store / ReLU / residual add (f32 or bf16 C) and the fused QKV
+// RoPE + KV scatter (the probe's M <= 32 projection: the rotation happens here,
+// no separate rope kernel).
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M, int N,
-                                     void* __restrict__ C, int64_t ldc, int epi, int out_dtype) {
+                                     void* __restrict__ C, int64_t ldc, const EpiArgs ea) {
   pdl_wait();
   pdl_trigger();
+  const int epi = ea.kind, out_dtype = ea.out_dtype;
   const int64_t total4 = (int64_t)M * N / 4;
   const int64_t mn = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -572,6 +576,38 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     const int row = (int)(e / N), col = (int)(e - (int64_t)row * N);
+    if (epi == QCF_EPI_ROPE_QKV) {
+      // columns [Q | K | V] (h / hkv heads x d); 4 columns = 2 interleaved pairs of one head
+      const int qd = ea.h * ea.d, kd = ea.hkv * ea.d;
+      __nv_bfloat16* out;
+      int base;
+      bool rot = true;
+      if (col < qd) {
+        base = col;
+        out = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)row * qd + base;
+      } else {
+        const int64_t drow = ea.dst[row];
+        if (col < qd + kd) {
+          base = col - qd;
+          out = reinterpret_cast<__nv_bfloat16*>(ea.k_tab) + drow * kd + base;
+        } else {
+          base = col - qd - kd;
+          out = reinterpret_cast<__nv_bfloat16*>(ea.v_tab) + drow * kd + base;
+          rot = false;
+        }
+      }
+      if (rot) {
+        const int64_t t0 = (int64_t)ea.pos[row] * (ea.d >> 1) + ((base % ea.d) >> 1);
+        const float c0 = (float)ea.cos_tbl[t0], s0 = (float)ea.sin_tbl[t0];
+        const float c1 = (float)ea.cos_tbl[t0 + 1], s1 = (float)ea.sin_tbl[t0 + 1];
+        const float x = acc.x * c0 - acc.y * s0, y = acc.x * s0 + acc.y * c0;
+        const float z = acc.z * c1 - acc.w * s1, w = acc.z * s1 + acc.w * c1;
+        acc = make_float4(x, y, z, w);
+      }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(out) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      continue;
+    }
     if (out_dtype == QCF_F32) {
       float4* c = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)row * ldc + col);
       if (epi == QCF_EPI_ADD_F32) {
@@ -696,7 +732,6 @@ template <int BN, bool SKINNY = false>
 static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                      int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, int splits = 1,
                      int a_box_rows = TC_BM, float* partial = nullptr) {
-  const int epi = ea.kind, out_dtype = ea.out_dtype;
   using Cfg = TcCfg<BN, SKINNY>;
   CUtensorMap mb;
   int st = make_b_map(&mb, b, n, k, ldb, BN, ea.b_tiled);
@@ -716,7 +751,7 @@ static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c,
   if (splits > 1) {
     const int64_t total4 = m * n / 4;
     const int rg = (int)std::min<int64_t>((total4 + 255) / 256, 4 * sm_count());
-    QCF_LAUNCH("splitk_reduce_kernel", splitk_reduce_kernel, dim3(rg), dim3(256), 0, s, partial, splits, (int)m, (int)n, c, ldc, epi, out_dtype);
+    QCF_LAUNCH("splitk_reduce_kernel", splitk_reduce_kernel, dim3(rg), dim3(256), 0, s, partial, splits, (int)m, (int)n, c, ldc, ea);
     QCF_LAUNCH_CHECK("qcf_gemm(split-k reduce)");
   }
   return QCF_OK;
@@ -801,18 +836,26 @@ size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   return sk_bytes() + (sp > 1 ? (size_t)sp * m * n * sizeof(float) : 0);
 }
 
+static int gemm_tc_skinny_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                             int64_t n, int64_t k, const EpiArgs& ea, void* ws, size_t ws_bytes, cudaStream_t s);
+
 int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                    int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout, void* ws, size_t ws_bytes,
                    cudaStream_t s) {
+  return gemm_tc_skinny_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, ws, ws_bytes, s);
+}
+
+static int gemm_tc_skinny_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                             int64_t n, int64_t k, const EpiArgs& ea, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int sp = skinny_splits(m, n, k);
   if (sp <= 1 || ws_bytes < gemm_workspace_bytes(m, n, k) || (n % 4) || ((uintptr_t)ws & 15)) return QCF_EUNSUPPORTED;
   if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
-  if ((ldc % 4) || ((uintptr_t)c & 15)) return QCF_EUNSUPPORTED;
+  if (ea.kind != QCF_EPI_ROPE_QKV && ((ldc % 4) || ((uintptr_t)c & 15))) return QCF_EUNSUPPORTED;
   const int box = (int)((m + 15) / 16 * 16);
   CUtensorMap ma;
   int st = make_kmajor_map(&ma, a, m, k, lda, box);
   if (st != QCF_OK) return st;
-  return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, s, sp, box,
+  return launch_bn<64, true>(ma, b, ldb, c, ldc, m, n, k, ea, s, sp, box,
                              reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + sk_bytes()));
 }
 
@@ -830,11 +873,15 @@ int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb,
                          int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
                          const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
                          int b_layout, void* ws, size_t ws_bytes) {
-  if (d % 32 || m <= 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
+  if (d % 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
   if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab) & 15) return QCF_EUNSUPPORTED;
   EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
+  if (m <= 32 && ws) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction
+    const int st = gemm_tc_skinny_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, ws, ws_bytes, s);
+    if (st != QCF_EUNSUPPORTED) return st;
+  }
   return gemm_tc_launch_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, s, ws, ws_bytes);
 }
 

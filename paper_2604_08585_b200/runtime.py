@@ -118,8 +118,9 @@ class Executor:
         nq = (H + 2 * Hkv) * D
         self._norm(sc, m, lw.ln1_g, lw.ln1_b, s)
         qdst = q_out if q_out is not None else sc.q
-        if self.fused_qkv and m > 32:
-            # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue
+        if self.fused_qkv:
+            # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue (M <= 32:
+            # split-K weight streaming with the rotation applied in the split-K reduction)
             call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, self.w.b_layout, m, d, H, Hkv, D,
                  pos.data_ptr(), dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(),
                  self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), sc.ws.data_ptr(), sc.ws.numel(), s)

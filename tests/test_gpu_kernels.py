@@ -292,12 +292,13 @@ def test_gemm_skinny_splitk_deterministic(L, m, n, k, epi):
     assert torch.equal(outs[0], outs[1])          # fixed-order split-K reduction
 
 
-@pytest.mark.parametrize("m,heads", [(800, 4), (33, 2), (5153, 2)])
-def test_fused_qkv_rope_matches_two_step(L, m, heads):
+@pytest.mark.parametrize("m,heads,kdim", [(800, 4, 512), (33, 2, 512), (5153, 2, 512), (32, 32, 4096), (7, 4, 2048),
+                                          (32, 2, 512)])
+def test_fused_qkv_rope_matches_two_step(L, m, heads, kdim):
     """qcf_gemm_qkv_rope == qcf_gemm (f32 QKV) + qcf_rope_qkv_scatter (bf16 table)."""
     from paper_2604_08585_b200.model import RopeTable
     torch.manual_seed(m)
-    D, K = 128, 512
+    D, K = 128, kdim
     N = 3 * heads * D
     a = (torch.randn(m, K, device="cuda") * 0.5).bfloat16()
     w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
@@ -307,8 +308,10 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads):
     q1 = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
     k1 = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
     v1 = torch.zeros_like(k1)
+    ws = torch.zeros(int(L.lib.qcf_gemm_workspace(m, N, K)), dtype=torch.uint8, device="cuda")
+    # M <= 32 with a workspace: split-K streaming + RoPE in the reduction (or the 1-CTA fallback)
     L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
-           rope.n_pos, p(q1), p(k1), p(v1), None, 0, S())
+           rope.n_pos, p(q1), p(k1), p(v1), p(ws), ws.numel(), S())
     qkv = torch.empty(m, N, device="cuda")
     L.call("qcf_gemm", L.QCF_BF16, p(a), K, p(w), K, p(qkv), N, m, N, K, 0, L.QCF_F32, S())
     q2, k2, v2 = torch.zeros_like(q1), torch.zeros_like(k1), torch.zeros_like(v1)
@@ -316,7 +319,8 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads):
            p(q2), p(k2), p(v2), L.QCF_BF16, S())
     for x, y in ((q1, q2), (k1, k2), (v1, v2)):
         assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
-    assert torch.equal(v1, v2)
+    if m > 32:  # same single-pass accumulation -> V bit-identical (split-K sums in another order)
+        assert torch.equal(v1, v2)
 
 
 @pytest.mark.parametrize("m,n,k,epi", [(800, 12288, 4096, 0), (800, 4096, 14336, 0), (800, 14336, 4096, 1),
