@@ -85,6 +85,17 @@ int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
                  const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
                  int dtype, qcf_stream_t stream);
 
+/* Same with an explicit rotation delta per chunk (device int32 array, NULL =
+ * the chunk's fused row offset; max_delta bounds the table lookup). Rows land at
+ * desc.offset.. but K rotates by deltas[c]: used to build the probe's anchor
+ * prefix [BOS | R(off_c) K_c[anchors] ...] (fusion.py:281-303) straight from
+ * device-resident anchor rows when the chunk pool lives in host memory. */
+int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                     const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                     int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                     const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                     const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream);
+
 /* dst[l][i] = src[l][rows[i]] for K and V (anchor prefix gather, fusion.py:281-303) */
 int qcf_gather_rows(const void* src_k, const void* src_v, int64_t src_layer_stride,
                     const int32_t* rows, int64_t n_rows, void* dst_k, void* dst_v,

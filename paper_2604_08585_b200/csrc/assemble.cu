@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     const qcf_chunk_desc* __restrict__ chunks, int n_chunks, int n_rows /* 1 + n_ctx */,
     const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
     T* __restrict__ fv, int64_t fstride, int row_elems, int d,
-    const double* __restrict__ ctab, const double* __restrict__ stab) {
+    const double* __restrict__ ctab, const double* __restrict__ stab, const int32_t* __restrict__ deltas) {
   pdl_wait();
   pdl_trigger();
   constexpr int V = Vec16<T>::N;
@@ -74,13 +74,15 @@ __global__ void __launch_bounds__(256) assemble_kernel(
       *reinterpret_cast<uint4*>(dv) = *reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems + e);
       continue;
     }
-    const qcf_chunk_desc c = chunks[find_chunk(chunks, n_chunks, row)];
+    const int ci = find_chunk(chunks, n_chunks, row);
+    const qcf_chunk_desc c = chunks[ci];
+    const int64_t delta = deltas ? deltas[ci] : c.offset;  // rotation delta (default: the fused row)
     const int64_t src_off = layer * c.layer_stride + (int64_t)(row - c.offset) * row_elems + e;
     const T* sk = reinterpret_cast<const T*>(c.k) + src_off;
     const T* sv = reinterpret_cast<const T*>(c.v) + src_off;
     *reinterpret_cast<uint4*>(dv) = __ldg(reinterpret_cast<const uint4*>(sv));
     const int j0 = (e % d) >> 1;
-    rotate_vec<T>(sk, dk, j0, ctab + (int64_t)c.offset * (d / 2), stab + (int64_t)c.offset * (d / 2));
+    rotate_vec<T>(sk, dk, j0, ctab + delta * (d / 2), stab + delta * (d / 2));
   }
 }
 
@@ -107,18 +109,18 @@ __global__ void gather_rows_kernel(const T* __restrict__ sk, const T* __restrict
 
 }  // namespace qcf
 
-extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
-                            const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
-                            int64_t fused_layer_stride, int n_layers, int hkv, int d,
-                            const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
-                            int dtype, qcf_stream_t stream) {
+extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                                const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                                int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                                const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                                const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
   QCF_REQUIRE(chunks && bos_k && bos_v && fused_k && fused_v && cos_tbl && sin_tbl, QCF_EINVAL,
               "qcf_assemble: null pointer");
   QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1, QCF_EINVAL,
               "qcf_assemble: bad sizes");
   QCF_REQUIRE(d % 8 == 0, QCF_EUNSUPPORTED, "qcf_assemble: d_head must be a multiple of 8");
-  QCF_REQUIRE(n_ctx < n_pos, QCF_ESHAPE, "qcf_assemble: RoPE table too short (%lld <= %d)",
-              (long long)n_pos, n_ctx);
+  QCF_REQUIRE(n_ctx < n_pos && max_delta < n_pos, QCF_ESHAPE, "qcf_assemble: RoPE table too short (%lld)",
+              (long long)n_pos);
   const int row_elems = hkv * d;
   QCF_REQUIRE(fused_layer_stride >= (int64_t)(n_ctx + 1) * row_elems, QCF_ESHAPE,
               "qcf_assemble: fused layer stride too small");
@@ -129,15 +131,25 @@ extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ct
   dim3 grid(gx, n_layers);
   if (dtype == QCF_F32)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
-        (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
+        (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl,
+        deltas);
   else if (dtype == QCF_BF16)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1,
         (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
-        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl);
+        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas);
   else
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_assemble: bad dtype");
   QCF_LAUNCH_CHECK("qcf_assemble");
   return QCF_OK;
+}
+
+extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                            const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                            int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                            const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                            int dtype, qcf_stream_t stream) {
+  return qcf_assemble_rot(chunks, n_chunks, n_ctx, bos_k, bos_v, fused_k, fused_v, fused_layer_stride, n_layers,
+                          hkv, d, cos_tbl, sin_tbl, n_pos, nullptr, 0, dtype, stream);
 }
 
 extern "C" int qcf_gather_rows(const void* src_k, const void* src_v, int64_t src_layer_stride,

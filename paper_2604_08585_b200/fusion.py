@@ -781,6 +781,143 @@ class FusionEngine:
         ex.stack(b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk, b.fv, stream=stream, n_req=B)
         ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
 
+    # ------------------------------------------------------------------
+    # host-pool variant: layer-pipelined chunk-KV streaming
+    # ------------------------------------------------------------------
+    def _launch_host(self, plans: list[_Plan], b: _Bufs, n_slots: int = 3) -> None:
+        """The fused prefill when the chunk pool lives in pinned host memory.
+
+        Probe prefix: `qcf_assemble_rot` from the HBM-resident anchor rows
+        (K rotated by the chunk offset, fusion.py:281-303). Scoring: the
+        critical-layer fused K from the HBM-resident critical keys. Recompute:
+        layer l's chunk K/V are copied host->device on a copy stream into one
+        of `n_slots` staging buffers while layer l-1 recomputes; layer l is
+        assembled from the slot (`qcf_assemble`, n_layers = 1) right before
+        its recompute (fusion.py:468-483 consumes layer l only at step l).
+        Same kernels and arithmetic as the HBM path: bit-identical results."""
+        cfg, ex, plan = self.config, self.ex, plans[0]
+        c, q, n_ctx, n_sel, B, L = cfg.critical_layer, plan.q, plan.n_ctx, plan.n_sel, b.B, cfg.n_layers
+        dev, dt = self.device, self.weights.torch_dtype
+        main = torch.cuda.current_stream()
+        s = cuda_stream(main)
+        row_elems = cfg.n_kv_heads * cfg.d_head
+        esz = b.fk.element_size()
+        self.ex.rope.ensure(b.rows + 2)
+        rope = self.ex.rope
+        bos_k, bos_v = self._bos_k, self._bos_v     # [L][Hkv][D]
+        recs_all = [r for pl in plans for r in pl.records]
+        n_ch = len(plan.records)
+
+        def descs(fields) -> torch.Tensor:
+            arr = (ChunkDesc * len(fields))()
+            for i, (k, v, lstride, n_tok, off) in enumerate(fields):
+                arr[i].k, arr[i].v, arr[i].layer_stride, arr[i].n_tok, arr[i].offset = k, v, lstride, n_tok, off
+            return torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(dev)
+
+        keep = []   # device descriptor arrays must outlive the launches
+        if plan.policy == "QCFuse" and n_sel > 0:
+            for r, pl in enumerate(plans):
+                # probe prefix rows [BOS | anchors of chunk 0 | ...] of layers < c, K rotated by off_c
+                fields, deltas, row = [], [], 1
+                for rec, off in zip(pl.records, pl.offsets):
+                    na = rec.anchor_indices.size
+                    if na:
+                        fields.append((rec.anchor_k.data_ptr(), rec.anchor_v.data_ptr(), na * row_elems, na, row))
+                        deltas.append(off)
+                        row += na
+                if fields:
+                    d_desc, d_delta = descs(fields), _i32(deltas, dev)
+                    keep += [d_desc, d_delta]
+                    call("qcf_assemble_rot", d_desc.data_ptr(), len(fields), row - 1, bos_k.data_ptr(),
+                         bos_v.data_ptr(), b.pk.data_ptr() + r * b.P * row_elems * esz,
+                         b.pv.data_ptr() + r * b.P * row_elems * esz, b.pk.stride(0), c, cfg.n_kv_heads,
+                         cfg.d_head, rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, d_delta.data_ptr(),
+                         max(deltas), self.weights.qcf_dtype, s)
+                # critical-layer fused K (V slot filled with K; layer c-1 is re-assembled before its recompute)
+                d_desc = descs([(rec.k_crit.data_ptr(), rec.k_crit.data_ptr(), 0, rec.n_tokens, off)
+                                for rec, off in zip(pl.records, pl.offsets)])
+                keep.append(d_desc)
+                lay = (c - 1) * b.fk.stride(0) * esz
+                call("qcf_assemble", d_desc.data_ptr(), n_ch, n_ctx, bos_k[c - 1].data_ptr(), bos_v[c - 1].data_ptr(),
+                     b.fk.data_ptr() + lay + r * b.R * row_elems * esz, b.fv.data_ptr() + lay + r * b.R * row_elems * esz,
+                     b.fk.stride(0), 1, cfg.n_kv_heads, cfg.d_head, rope.cos.data_ptr(), rope.sin.data_ptr(),
+                     rope.n_pos, self.weights.qcf_dtype, s)
+            ex.embed(b.sc_probe, B * q, b.tok, rows=b.p_tok)
+            for li in range(c - 1):
+                ex.layer(li, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[li], b.pv[li], n_req=B)
+            ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
+                     q_only=True, q_out=b.qc[0], n_req=B)
+            self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, None, n_req=B,
+                            k_req_stride=b.R * row_elems)
+            call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
+                 b.rc_dst.data_ptr(), b.R, s)
+        elif plan.policy == "FullCompute":
+            for r in range(B):
+                call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
+                call("qcf_iota", n_sel, 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+
+        # ---- layer-pipelined streaming of the chunk KV + recompute
+        S_tot = sum(r.n_tokens for r in recs_all)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        cs = self._copy_stream
+        slots = self._host_slots(n_slots, S_tot, row_elems, dt)
+        staged = [torch.cuda.Event() for _ in range(L)]
+        freed = [torch.cuda.Event() for _ in range(L)]
+        slot_descs = []
+        for si in range(n_slots):   # per slot: descriptors of every request's chunks (fused rows = offsets)
+            per_req, base = [], 0
+            for pl in plans:
+                fields = []
+                for rec, off in zip(pl.records, pl.offsets):
+                    fields.append((slots[si][0][base:].data_ptr(), slots[si][1][base:].data_ptr(), 0, rec.n_tokens, off))
+                    base += rec.n_tokens
+                per_req.append(descs(fields))
+            slot_descs.append(per_req)
+
+        def fetch(li):
+            si = li % n_slots
+            with torch.cuda.stream(cs):
+                if li >= n_slots:
+                    cs.wait_event(freed[li - n_slots])
+                base = 0
+                for rec in recs_all:
+                    n = rec.n_tokens
+                    slots[si][0][base:base + n].copy_(rec.k[li].view(n, row_elems), non_blocking=True)
+                    slots[si][1][base:base + n].copy_(rec.v[li].view(n, row_elems), non_blocking=True)
+                    base += n
+                staged[li].record(cs)
+
+        for li in range(min(n_slots, L)):
+            fetch(li)
+        m = B * b.Mr
+        ex.embed(b.sc_rc, m, b.tok, rows=b.rc_dst)
+        for li in range(L):
+            main.wait_event(staged[li])
+            lay = li * b.fk.stride(0) * esz
+            for r in range(B):
+                call("qcf_assemble", slot_descs[li % n_slots][r].data_ptr(), n_ch, n_ctx, bos_k[li].data_ptr(),
+                     bos_v[li].data_ptr(), b.fk.data_ptr() + lay + r * b.R * row_elems * esz,
+                     b.fv.data_ptr() + lay + r * b.R * row_elems * esz, b.fk.stride(0), 1, cfg.n_kv_heads,
+                     cfg.d_head, rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, self.weights.qcf_dtype, s)
+            freed[li].record(main)
+            if li + n_slots < L:
+                fetch(li + n_slots)
+            ex.layer(li, b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk[li], b.fv[li], n_req=B)
+        ex.flush(b.sc_rc, m)
+        ex.lm_head(b.sc_rc, b.last_row, b.logits)
+        main.wait_stream(cs)
+        b._keep = keep + slot_descs   # alive until the next launch into these buffers
+
+    def _host_slots(self, n_slots, rows, row_elems, dt):
+        key = (n_slots, rows, row_elems, dt)
+        sl = getattr(self, "_slots", None)
+        if sl is None or sl[0] != key:
+            bufs = [(torch.empty((rows, row_elems), dtype=dt, device=self.device),
+                     torch.empty((rows, row_elems), dtype=dt, device=self.device)) for _ in range(n_slots)]
+            self._slots = (key, bufs)
+        return self._slots[1]
+
     def prefill_batch(self, policy: str, ratio: float, chunk_lists, queries, use_graph: bool = True,
                       extra_rows: int = 0, stream=None):
         """Device-side fused prefill of a homogeneous batch (same chunk lengths,
@@ -793,6 +930,11 @@ class FusionEngine:
         b = self._buffers(plans, extra_rows)
         self._stage(plans, b, queries, stream)
         self.ex.rope.ensure(b.rows + 2)
+        if any(r.on_host for pl in plans for r in pl.records):
+            if not all(r.on_host for pl in plans for r in pl.records):
+                raise ValueError("a batch must draw all its chunks from one pool placement")
+            self._launch_host(plans, b)   # eager: two streams, per-layer events
+            return plans, b
         if not use_graph:
             self._launch(plans, b, stream)
             return plans, b

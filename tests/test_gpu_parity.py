@@ -402,10 +402,14 @@ def test_gqa_init_bit_exact(tmp_path):
 # ---------------------------------------------------------------- comparison policies
 @pytest.mark.parametrize("name", ["small", "small2", "tiny"])
 def test_baseline_policies_match_reference(tmp_path, name):
-    """CacheBlend / KVShare (layer-1 deviation pass on the GPU) and QCLast /
-    QCAll select exactly the reference's index sets in the f32 parity mode
-    (fixtures: tests/golden/make_golden.py baselines); deviation and received
-    attention within 1e-5 / 1e-6 of the reference's."""
+    """QCLast / QCAll select exactly the reference's index sets in the f32
+    parity mode; the layer-1 pass reproduces the reference's received attention
+    (1e-6) and its KV deviations to noise level. In the reference model layer-1
+    K/V do not depend on context (only on the token and a rotation), so an
+    untouched cache has deviations of pure rounding noise (~1e-7) and the
+    CacheBlend / KVShare ranking of such a cache is decided by BLAS rounding
+    order -- not reproducible across implementations; the perturbed-cache test
+    below pins those two policies where the deviation carries signal."""
     import json
     from pathlib import Path
     import paper_2604_08585_b200 as Q
@@ -423,15 +427,48 @@ def test_baseline_policies_match_reference(tmp_path, name):
     fused = eng.assemble_context(ids)
     k, v, received = eng._layer1_recompute_pass(fused, want_attention=True)
     dev = eng._kv_deviation(fused, k, v).cpu().numpy()
-    assert np.allclose(dev, z[f"{name}_deviation"], rtol=1e-5)
+    assert np.abs(dev - z[f"{name}_deviation"]).max() < 1e-5
     assert np.abs(received.cpu().numpy() - z[f"{name}_received"]).max() < 1e-6
     r = float(z[f"{name}_ratio"])
     q = z[f"{name}_query"].tolist()
-    for pol in ("CacheBlend", "KVShare", "QCLast", "QCAll"):
+    for pol in ("QCLast", "QCAll"):
         got = eng.select(pol, r, fused, q).indices
         assert np.array_equal(got, z[f"{name}_{pol}"]), pol
-    res = eng.run("KVShare", r, ids, q, max_new=1)
-    assert np.array_equal(res.selection.indices, z[f"{name}_KVShare"])
+    for pol in ("CacheBlend", "KVShare"):   # well-formed selections
+        got = eng.select(pol, r, fused, q).indices
+        assert got.size == math.ceil(r * fused.n_ctx) and np.all(np.diff(got) > 0)
+        assert got.min() >= 1 and got.max() <= fused.n_ctx
+
+
+def test_cacheblend_kvshare_on_stale_cache_match_oracle(tmp_path):
+    """A stale chunk cache (layer-1 K/V of 30% of the rows perturbed, as if
+    computed under another context): CacheBlend / KVShare on the GPU select
+    exactly the oracle's index sets (deviation and received attention carry
+    the signal), through select() and through run()."""
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    oc = O.Config(n_layers=4, n_heads=4, d_model=256, d_head=64, d_ff=1024, seed=1234)
+    ow = O.init_weights(oc)
+    rng = np.random.default_rng(7)
+    chunks = [O.precompute_chunk(ow, rng.integers(0, 256, 96), 0.1) for _ in range(3)]
+    for ch in chunks:
+        rows = rng.permutation(96)[:29]
+        ch.kv[0].keys[rows] += rng.normal(0, 0.5, ch.kv[0].keys[rows].shape).astype(np.float32)
+        ch.kv[0].values[rows] += rng.normal(0, 0.5, ch.kv[0].values[rows].shape).astype(np.float32)
+    fused_o = O.assemble(ow, chunks)
+    w = device_weights(ow, "f32")
+    store = Q.ChunkStore(tmp_path / "s", w.config, dtype="f32", persist=False)
+    ids = load_oracle_chunks(store, chunks)
+    eng = Q.FusionEngine(w, store)
+    fused = eng.assemble_context(ids)
+    q = rng.integers(0, 256, 8).tolist()
+    for ratio in (0.1, 0.25):
+        assert np.array_equal(eng.select("CacheBlend", ratio, fused, q).indices,
+                              O.select_topn(O.cacheblend_scores(ow, fused_o), ratio))
+        assert np.array_equal(eng.select("KVShare", ratio, fused, q).indices,
+                              O.select_topn(O.kvshare_scores(ow, fused_o), ratio))
+    res = eng.run("CacheBlend", 0.25, ids, q, max_new=1)
+    assert np.array_equal(res.selection.indices, O.select_topn(O.cacheblend_scores(ow, fused_o), 0.25))
 
 
 def test_received_attention_row_chunking(tmp_path):
@@ -458,3 +495,35 @@ def test_received_attention_row_chunking(tmp_path):
     ref = torch.softmax(s.masked_fill(~mask[None], float("-inf")), dim=-1).mean(dim=(0, 1)).cpu().numpy()
     assert np.abs(outs[0] - ref).max() < 1e-6
     assert np.abs(outs[1] - outs[0]).max() < 1e-7
+
+
+# ---------------------------------------------------------------- host-pool tier
+@pytest.mark.parametrize("dtype,policy", [("f32", "QCFuse"), ("bf16", "QCFuse"), ("bf16", "FullCompute")])
+def test_host_pool_pipelined_equals_hbm_pool(tmp_path, dtype, policy):
+    """Chunk KV in pinned host memory, streamed layer by layer while the
+    previous layer recomputes: selection and first-token logits bit-identical to
+    the HBM-resident pool (same kernels, same arithmetic), single and batched."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=21)
+    w = Q.init_weights(cfg, dtype=dtype)
+    hbm = Q.ChunkStore(tmp_path / "a", cfg, dtype=dtype, persist=False)
+    host = Q.ChunkStore(tmp_path / "b", cfg, dtype=dtype, persist=False, pool="host")
+    toks = [np.random.default_rng(40 + i).integers(0, 256, 96) for i in range(4)]
+    ids = [hbm.precompute(w, t, 0.05).chunk_id for t in toks]
+    for cid in ids:
+        r = hbm.get_record(cid)
+        host.add_record(r.token_ids, r.k, r.v, r.key_norms, r.anchor_indices)
+    assert host.get_record(ids[0]).on_host and host.get_record(ids[0]).anchor_k.is_cuda
+    e1, e2 = Q.FusionEngine(w, hbm), Q.FusionEngine(w, host)
+    rng = np.random.default_rng(5)
+    reqs = [[ids[j] for j in rng.permutation(4)[:3]] for _ in range(3)]   # equal chunk lengths: one batch shape
+    qs = [rng.integers(0, 256, 12).tolist() for _ in range(3)]
+    p1, b1 = e1.prefill_batch(policy, 0.2, reqs, qs, use_graph=False)
+    l1, s1 = b1.logits.cpu().numpy().copy(), b1.rc_pos.cpu().numpy().copy()
+    p2, b2 = e2.prefill_batch(policy, 0.2, reqs, qs)
+    torch.cuda.synchronize()
+    assert np.array_equal(b2.rc_pos.cpu().numpy(), s1)
+    assert np.array_equal(b2.logits.cpu().numpy(), l1)
+    lg, sel = e2.fuse(qs[0], reqs[0], 0.2)
+    lg1, sel1 = e1.fuse(qs[0], reqs[0], 0.2)
+    assert np.array_equal(sel, sel1) and np.array_equal(lg, lg1)
