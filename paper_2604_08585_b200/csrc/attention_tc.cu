@@ -337,7 +337,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
 // Pairing of query tiles: adjacent (2p, 2p+1) when the grid spans several
 // waves, mirrored (p, n-1-p) -- equal work per CTA -- when it fits in one.
 // ---------------------------------------------------------------------------
-constexpr int A2_THREADS = 576;
+// SPLIT = warps sharing one row (1: a thread owns a full 128-key row -- no
+// cross-warp max exchange; 2: half rows, 8 softmax warps per tile)
+template <int SPLIT>
+struct A2Cfg {
+  static constexpr int THREADS = 64 + 2 * 4 * SPLIT * 32;
+  static constexpr int W = 128 / SPLIT;  // keys / output dims per softmax thread
+};
 #ifndef A2_EMU16
 #define A2_EMU16 7  // of every 16 column pairs, this many take the FMA-pipe exp2 (balances MUFU vs FMA)
 #endif
@@ -425,7 +431,8 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
   return r;
 }
 
-__global__ void __launch_bounds__(A2_THREADS, 1)
+template <int SPLIT>
+__global__ void __launch_bounds__(A2Cfg<SPLIT>::THREADS, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
                 int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int mirrored) {
@@ -453,15 +460,19 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (M + AT_BM - 1) / AT_BM;
   const int n_pairs = (n_qt + 1) / 2;
-  const int pidx = n_pairs - 1 - (int)blockIdx.y;  // adjacent pairs: longest (latest rows) first
   int tile0, tile1;
   if (mirrored) {
+    const int pidx = n_pairs - 1 - (int)blockIdx.y;
     tile0 = pidx;
     tile1 = n_qt - 1 - pidx;
     if (tile1 == tile0) tile1 = -1;
   } else {
-    tile0 = 2 * pidx;
-    tile1 = 2 * pidx + 1 < n_qt ? 2 * pidx + 1 : -1;
+    // adjacent pairs counted from the LAST tile (longest key ranges first, LPT);
+    // an odd tile count leaves tile 0 -- the shortest -- without a partner
+    const int hi = n_qt - 1 - 2 * (int)blockIdx.y;
+    tile0 = hi - 1;
+    tile1 = hi;
+    if (tile0 < 0) { tile0 = hi; tile1 = -1; }
   }
   const int head = blockIdx.x;
   const int kvh = head / (H / Hkv);
@@ -477,7 +488,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 8);  // one elected arrive per softmax warp of the tile
+      mbar_init(&p_full[s], 4 * SPLIT);  // one elected arrive per softmax warp of the tile
       mbar_init(&o_full[s], 1);
     }
     fence_barrier_init();
@@ -568,7 +579,10 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {
           const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
-          const uint32_t pa = tmem + t * 128 + (kk >> 2) * 64 + (kk & 3) * 8;  // P cols of keys 16kk..16kk+15
+          // P (packed bf16) of keys 16kk..16kk+15: each softmax thread writes its W keys at the start
+          // of its own S columns -> col = ch*W + (16kk mod W)/2
+          constexpr int W = A2Cfg<SPLIT>::W;
+          const uint32_t pa = tmem + t * 128 + (kk * 16 / W) * W + ((kk * 16) % W) / 2;
           mma_bf16_ts(tmem + 256 + t * 128, pa, b, idesc_o, (j | kk) != 0);
         }
         const bool last_user = (t == 1) || (j >= nt1);
@@ -588,7 +602,134 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
         }
       }
     }
-  } else {  // ---------------- softmax / rescale / epilogue: warps 2..17
+  } else if (SPLIT == 1) {  // ---------------- softmax / rescale / epilogue: warps 2..9, one row per thread
+    const int t = (warp - 2) >> 2;        // query tile
+    const int g = warp & 3;               // TMEM lane quarter
+    const int r = g * 32 + lane;
+    const int n_my = t ? nt1 : nt0;
+    const int my_tile = t ? tile1 : tile0;
+    const int row = my_tile * AT_BM + r;
+    const int my_kmax = (my_tile >= 0 && row < M) ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const uint64_t sc2 = f2(scale_log2, scale_log2);
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_my; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const int lim = my_kmax - j * AT_BN;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= 127);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      uint32_t v0[32], v1[32], v2[32], v3[32];   // the whole S row stays in registers
+      tmem_ld32(tS + 0, v0);
+      tmem_ld32(tS + 32, v1);
+      tmem_ld32(tS + 64, v2);
+      tmem_ld32(tS + 96, v3);
+      tmem_ld_wait();
+#define SROW(i) __uint_as_float((i) < 32 ? v0[(i) & 31] : (i) < 64 ? v1[(i) & 31] : (i) < 96 ? v2[(i) & 31] : v3[(i) & 31])
+      float pmax = -INFINITY;
+      if (all_vis) {
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) pmax = fmax3(pmax, SROW(i), SROW(i + 1));
+      } else if (!none_vis) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) pmax = fmaxf(pmax, i <= lim ? SROW(i) : -INFINITY);
+      }
+      const float tmax = pmax * scale_log2;
+      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
+        m_ref = tmax;
+        l *= alpha;
+      }
+      const uint64_t nm2 = f2(-m_ref, -m_ref);
+      // P = exp2(s*scale - m_ref) as packed bf16 into S columns 0..63 (S is in registers)
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t pk[16];
+        if (none_vis) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        } else if (all_vis) {
+          uint64_t l2 = f2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t x2 = ffma2(f2(SROW(hh * 32 + i), SROW(hh * 32 + i + 1)), sc2, nm2);
+            uint64_t p2;
+            if (((i >> 1) & 15) < A2_EMU16) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float a, b;
+              f2_split(x2, a, b);
+              p2 = f2(ex2_approx(a), ex2_approx(b));
+            }
+            l2 = fadd2(l2, p2);
+            float p0, p1;
+            f2_split(p2, p0, p1);
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+          float la, lb;
+          f2_split(l2, la, lb);
+          l += la + lb;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const int c0 = hh * 32 + i;
+            float p0 = ex2_approx(fmaf(SROW(c0), scale_log2, -m_ref));
+            float p1 = ex2_approx(fmaf(SROW(c0 + 1), scale_log2, -m_ref));
+            p0 = (c0 <= lim) ? p0 : 0.f;
+            p1 = (c0 + 1 <= lim) ? p1 : 0.f;
+            l += p0 + p1;
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+        }
+        tmem_st16(tS + hh * 16, pk);
+      }
+#undef SROW
+      // lazy O rescale; PV(t, j-1) is complete (S(t, j) was issued after it, in order)
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          uint32_t o[32];
+          tmem_ld32(tO + hh * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tO + hh * 32, o);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    if (n_my > 0) {  // epilogue: O / l for the whole row
+      mbar_wait(&o_full[t], 0);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t o[32];
+        tmem_ld32(tO + hh * 32, o);
+        tmem_ld_wait();
+        if (row < M && my_kmax >= 0) {
+          __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + hh * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 pk4;
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv,
+                                            __uint_as_float(o[i + 2 * u + 1]) * inv);
+            *reinterpret_cast<uint4*>(dst + i) = pk4;
+          }
+        }
+      }
+    }
+  } else {  // ---------------- SPLIT == 2: softmax / rescale / epilogue: warps 2..17, half rows
     const int t = (warp - 2) >> 3;        // query tile
     const int ch = ((warp - 2) >> 2) & 1; // column half: keys / output dims 64ch..64ch+63
     const int g = warp & 3;               // TMEM lane quarter
@@ -741,7 +882,13 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
 
 static int g_attn_ver = -1;  // QCF_ATTN env / qcf_set_attention_kernel: 1 = single-tile, 2 = ping-pong (default)
 
-void set_attention_kernel(int v) { g_attn_ver = (v == 1 || v == 2) ? v : 0; }
+static int g_attn_split = 2;  // v2 softmax layout: 2 = half rows (default), 1 = full row per thread (knob 3)
+
+void set_attention_kernel(int v) {
+  g_attn_split = (v == 3) ? 1 : 2;
+  if (v == 3) v = 2;
+  g_attn_ver = (v == 1 || v == 2) ? v : 0;
+}
 
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
                         int hkv, int d, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
@@ -761,7 +908,9 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+      e = cudaFuncSetAttribute(attn_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
     if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
     attr = true;
   }
@@ -778,10 +927,19 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   const int ver = g_attn_ver ? g_attn_ver : (one_wave ? 1 : 2);
   if (ver == 2) {
     // one wave or less: mirrored pairs balance the per-CTA key ranges
-    const int mirrored = one_wave ? 1 : 0;
+    static int pair_mode = -1;  // QCF_ATTN_PAIR: 0 adjacent, 1 mirrored, unset = mirrored for one-wave grids
+    if (pair_mode == -1) {
+      const char* e = getenv("QCF_ATTN_PAIR");
+      pair_mode = e ? atoi(e) : 2;
+    }
+    const int mirrored = pair_mode == 2 ? (one_wave ? 1 : 0) : pair_mode;
     dim3 grid((unsigned)h, (unsigned)n_pairs, (unsigned)n_req);
-    QCF_LAUNCH("attn_tc2_kernel", attn_tc2_kernel, dim3(grid), dim3(A2_THREADS), A2_SMEM, s, mq, mk, mv, kmax, (int)m,
-               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
+    if (g_attn_split == 2)
+      QCF_LAUNCH("attn_tc2_kernel<2>", attn_tc2_kernel<2>, dim3(grid), dim3(A2Cfg<2>::THREADS), A2_SMEM, s, mq, mk, mv,
+                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
+    else
+      QCF_LAUNCH("attn_tc2_kernel<1>", attn_tc2_kernel<1>, dim3(grid), dim3(A2Cfg<1>::THREADS), A2_SMEM, s, mq, mk, mv,
+                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
   } else {
     dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
     QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m,

@@ -1,4 +1,6 @@
-"""tcgen05 attention kernels 1 vs 2 at the fused-path shapes (CUDA events).
+"""tcgen05 attention kernels at the fused-path shapes (CUDA events): 1 = one
+tile per CTA, 2 = ping-pong pairs with half-row softmax threads, 3 = ping-pong
+with full-row threads. QCF_ATTN_PAIR=0/1 forces adjacent/mirrored pairing.
 FLOPs counted on the exact visible keys: 4*H*D*sum(kmax+1)."""
 import sys
 from pathlib import Path
@@ -18,7 +20,7 @@ def bench(m, n_keys, H, Hkv, n_req, kmax, it=20):
     out = torch.empty_like(q)
     flops = 4.0 * H * D * float((kmax.long() + 1).sum())
     res = {}
-    for ver in (1, 2):
+    for ver in (1, 2, 3):
         _lib.call("qcf_set_attention_kernel", ver)
         f = lambda: _lib.call("qcf_attention_batched", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(), kmax.data_ptr(),
                               m, n_req, H, Hkv, D, n_keys, out.data_ptr(), S)
