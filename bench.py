@@ -189,6 +189,7 @@ def phase_profile(eng, chunk_lists, queries, policy, ratio):
     from paper_2604_08585_b200 import _lib
     plans, b = eng.prefill_batch(policy, ratio, chunk_lists, queries, use_graph=False)
     torch.cuda.synchronize()
+    conc, eng.concurrent = eng.concurrent, False   # per-launch events on one stream
     _lib.profiler = _lib.Profiler()
     try:
         # park the GPU on a spin kernel so every launch below is queued before it
@@ -199,6 +200,7 @@ def phase_profile(eng, chunk_lists, queries, policy, ratio):
         recs = _lib.profiler.summary()
     finally:
         _lib.profiler = None
+        eng.concurrent = conc
     return plans, b, recs
 
 
@@ -271,14 +273,12 @@ def main():
     for bt in batches:
         pl = [eng._plan("QCFuse", ratio, c, t) for c, t in bt]
         eng._stage(pl, bb, [t for _, t in bt])
-        staged.append((bb.desc.clone(), bb.tok.clone(), bb.anchor_rows.clone()))
+        staged.append([t.clone() for t in bb.staged()])
     torch.cuda.synchronize()
 
     def batch_step(i):
-        d, t, a = staged[i % len(staged)]
-        bb.desc.copy_(d, non_blocking=True)
-        bb.tok.copy_(t, non_blocking=True)
-        bb.anchor_rows.copy_(a, non_blocking=True)
+        for dst, src in zip(bb.staged(), staged[i % len(staged)]):
+            dst.copy_(src, non_blocking=True)
         bb.graph.replay()
         if world > 1:
             res = torch.cat([bb.logits, bb.rc_pos.view(B, bb.Mr)[:, :plans[0].n_sel].float()], dim=1)
@@ -321,7 +321,7 @@ def main():
         if i >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), device)
-    h2d = B * (cfgd["n_chunks"] * 32 + 4 * bb.R + 4 * plans[0].anchor_rows.size)
+    h2d = sum(t.numel() * t.element_size() for t in bb.staged())
     d2h = B * (4 * cfg.vocab_size + 4 * n_sel)
 
     # ---- instrumented pass: per-phase + dominant kernel (GEMM family) roofline

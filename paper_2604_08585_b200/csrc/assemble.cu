@@ -20,24 +20,22 @@ __device__ __forceinline__ int find_chunk(const qcf_chunk_desc* ch, int n_chunks
   return lo;
 }
 
+// rotate the interleaved pairs of one 16-byte vector (value in, value out)
 template <typename T>
-__device__ __forceinline__ void rotate_vec(const T* src, T* dst, int j0, const double* ctab,
-                                           const double* stab);
+__device__ __forceinline__ uint4 rotate_vec(uint4 raw, int j0, const double* ctab, const double* stab);
 
 template <>
-__device__ __forceinline__ void rotate_vec<float>(const float* src, float* dst, int j0,
-                                                  const double* ctab, const double* stab) {
-  float4 x = *reinterpret_cast<const float4*>(src);
+__device__ __forceinline__ uint4 rotate_vec<float>(uint4 raw, int j0, const double* ctab, const double* stab) {
+  float4 x = *reinterpret_cast<float4*>(&raw);
   float4 y;
   rotate_pair_exact(x.x, x.y, ctab[j0], stab[j0], y.x, y.y);
   rotate_pair_exact(x.z, x.w, ctab[j0 + 1], stab[j0 + 1], y.z, y.w);
-  *reinterpret_cast<float4*>(dst) = y;
+  return *reinterpret_cast<uint4*>(&y);
 }
 
 template <>
-__device__ __forceinline__ void rotate_vec<__nv_bfloat16>(const __nv_bfloat16* src, __nv_bfloat16* dst,
-                                                          int j0, const double* ctab, const double* stab) {
-  uint4 raw = *reinterpret_cast<const uint4*>(src);
+__device__ __forceinline__ uint4 rotate_vec<__nv_bfloat16>(uint4 raw, int j0, const double* ctab,
+                                                           const double* stab) {
   const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&raw);
   uint4 outr;
   __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(&outr);
@@ -48,11 +46,16 @@ __device__ __forceinline__ void rotate_vec<__nv_bfloat16>(const __nv_bfloat16* s
     rotate_pair_fast(f.x, f.y, (float)ctab[j0 + t], (float)stab[j0 + t], oe, oo);
     q[t] = __floats2bfloat162_rn(oe, oo);
   }
-  *reinterpret_cast<uint4*>(dst) = outr;
+  return outr;
 }
 
+// One CTA per (fused row, layer): the chunk lookup happens once per row, and
+// every thread moves ASM_UNROLL 16-byte vectors of K and of V with all loads
+// issued before the stores (more bytes in flight per thread; HBM-bound).
+constexpr int ASM_THREADS = 128, ASM_UNROLL = 4;
+
 template <typename T>
-__global__ void __launch_bounds__(256) assemble_kernel(
+__global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
     const qcf_chunk_desc* __restrict__ chunks, int n_chunks, int n_rows /* 1 + n_ctx */,
     const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
     T* __restrict__ fv, int64_t fstride, int row_elems, int d,
@@ -62,27 +65,50 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   constexpr int V = Vec16<T>::N;
   const int layer = blockIdx.y;
   const int vpr = row_elems / V;
-  const int64_t total = (int64_t)n_rows * vpr;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(idx / vpr);
-    const int e = (int)(idx - (int64_t)row * vpr) * V;  // element within the row
-    T* dk = fk + layer * fstride + (int64_t)row * row_elems + e;
-    T* dv = fv + layer * fstride + (int64_t)row * row_elems + e;
+  __shared__ qcf_chunk_desc sc;
+  __shared__ int64_t s_delta;
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    T* dk = fk + layer * fstride + (int64_t)row * row_elems;
+    T* dv = fv + layer * fstride + (int64_t)row * row_elems;
     if (row == 0) {
-      *reinterpret_cast<uint4*>(dk) = *reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems + e);
-      *reinterpret_cast<uint4*>(dv) = *reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems + e);
+      for (int i = threadIdx.x; i < vpr; i += blockDim.x) {
+        reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems)[i];
+        reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems)[i];
+      }
       continue;
     }
-    const int ci = find_chunk(chunks, n_chunks, row);
-    const qcf_chunk_desc c = chunks[ci];
-    const int64_t delta = deltas ? deltas[ci] : c.offset;  // rotation delta (default: the fused row)
-    const int64_t src_off = layer * c.layer_stride + (int64_t)(row - c.offset) * row_elems + e;
-    const T* sk = reinterpret_cast<const T*>(c.k) + src_off;
-    const T* sv = reinterpret_cast<const T*>(c.v) + src_off;
-    *reinterpret_cast<uint4*>(dv) = __ldg(reinterpret_cast<const uint4*>(sv));
-    const int j0 = (e % d) >> 1;
-    rotate_vec<T>(sk, dk, j0, ctab + delta * (d / 2), stab + delta * (d / 2));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int ci = find_chunk(chunks, n_chunks, row);
+      sc = chunks[ci];
+      s_delta = deltas ? deltas[ci] : sc.offset;  // rotation delta (default: the fused row)
+    }
+    __syncthreads();
+    const int64_t src_off = layer * sc.layer_stride + (int64_t)(row - sc.offset) * row_elems;
+    const uint4* sk = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.k) + src_off);
+    const uint4* sv = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.v) + src_off);
+    const double* ct = ctab + s_delta * (d / 2);
+    const double* st = stab + s_delta * (d / 2);
+    for (int i0 = threadIdx.x; i0 < vpr; i0 += blockDim.x * ASM_UNROLL) {
+      uint4 kv[ASM_UNROLL], vv[ASM_UNROLL];
+#pragma unroll
+      for (int u = 0; u < ASM_UNROLL; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < vpr) {
+          kv[u] = __ldg(sk + i);
+          vv[u] = __ldg(sv + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < ASM_UNROLL; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < vpr) {
+          reinterpret_cast<uint4*>(dv)[i] = vv[u];
+          const int j0 = ((i * V) % d) >> 1;
+          reinterpret_cast<uint4*>(dk)[i] = rotate_vec<T>(kv[u], j0, ct, st);
+        }
+      }
+    }
   }
 }
 
@@ -125,16 +151,15 @@ extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int 
   QCF_REQUIRE(fused_layer_stride >= (int64_t)(n_ctx + 1) * row_elems, QCF_ESHAPE,
               "qcf_assemble: fused layer stride too small");
   auto s = qcf::as_stream(stream);
-  const int vec = dtype == QCF_F32 ? 4 : 8;
-  const int64_t per_layer = (int64_t)(n_ctx + 1) * (row_elems / vec);
-  int gx = (int)std::min<int64_t>((per_layer + 255) / 256, 65535 * 4);
-  dim3 grid(gx, n_layers);
+  QCF_REQUIRE(row_elems % (dtype == QCF_F32 ? 4 : 8) == 0, QCF_EUNSUPPORTED, "qcf_assemble: row not 16B multiple");
+  dim3 grid((unsigned)std::min<int64_t>(n_ctx + 1, 65535), n_layers);
+  const dim3 block(qcf::ASM_THREADS);
   if (dtype == QCF_F32)
-    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
+    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
         (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl,
         deltas);
   else if (dtype == QCF_BF16)
-    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, chunks, n_chunks, n_ctx + 1,
+    QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1,
         (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
         (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas);
   else

@@ -5,7 +5,10 @@ Hot path (`FusionEngine.fuse` / `run("QCFuse", …)`), all on one CUDA stream,
 no host synchronisation between kernels:
 
   K1 qcf_assemble          fused table = [BOS | R(off_c)·K_c …], V copied     fusion.py:234-263
-  K2 qcf_gather_rows       probe past = [BOS | anchor rows] for layers < c     fusion.py:281-303
+  K2 qcf_assemble_rot      probe past = [BOS | R(off_c)·anchor rows] for layers < c, from the
+                           chunks' HBM-resident anchor copies; K1 runs concurrently on a
+                           forked stream (both are HBM-bound, no data dependence) and joins
+                           before K4                                           fusion.py:281-303
   K3 layer stack (q rows)  LN→QKV→RoPE→attn→Wo→LN→FFN for layers 1..c-1, then
                            layer c's LN→Wq→RoPE = Q_c                          fusion.py:305-311
   K4 qcf_score             softmax over context keys, mean over (h,t)         fusion.py:313-326
@@ -370,6 +373,10 @@ class _Bufs:
         self.desc = torch.empty(B * len(plan.records) * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
         self.tok = torch.empty(B * R, dtype=torch.int32, device=dev)
         self.anchor_rows = torch.empty(B * max(n_pre, 1), dtype=torch.int32, device=dev)
+        # probe prefix straight from each chunk's anchor rows (K rotated by the chunk offset)
+        self.adesc = torch.empty(B * len(plan.records) * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
+        self.adelta = torch.empty(B * len(plan.records), dtype=torch.int32, device=dev)
+        self.max_delta = n_ctx
         self.pk = torch.empty((c, B * P, Hkv, D), dtype=dt, device=dev)
         self.pv = torch.empty_like(self.pk)
         ar = torch.arange(q, dtype=torch.int32, device=dev)
@@ -392,6 +399,11 @@ class _Bufs:
         self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
 
+    def staged(self) -> list[torch.Tensor]:
+        """The device tensors a batch's host inputs are staged into (swapped
+        between graph replays)."""
+        return [self.desc, self.tok, self.anchor_rows, self.adesc, self.adelta]
+
 
 class FusionEngine:
     """B200 engine with the reference's FusionEngine surface (fusion.py:211-563)."""
@@ -413,6 +425,10 @@ class FusionEngine:
         self._bos_k, self._bos_v = bk[:, 0].contiguous(), bv[:, 0].contiguous()
         self._bufs: dict[tuple, _Bufs] = {}
         self._oracle_cache: dict = {}
+        # assembly || probe on two streams (see _launch); measured neutral on B200 at the
+        # Llama-3-8B shape (tools/concurrency_check.py: both phases are HBM-bound), off by default
+        self.concurrent = False
+        self._aux: torch.cuda.Stream | None = None
 
     # ------------------------------------------------------------------
     # planning helpers
@@ -440,6 +456,22 @@ class FusionEngine:
             arr[i].layer_stride = r.k.stride(0)
             arr[i].n_tok = r.n_tokens
             arr[i].offset = o
+        return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
+
+    def _anchor_desc_bytes(self, recs, offs) -> torch.Tensor:
+        """Descriptors of each chunk's HBM-resident anchor rows, landing at
+        consecutive probe-prefix rows after BOS (zero-anchor chunks occupy no rows)."""
+        arr = (ChunkDesc * len(recs))()
+        row = 1
+        for i, r in enumerate(recs):
+            ak, av = self.store.anchor_kv(r)
+            na = int(r.anchor_indices.size)
+            arr[i].k = ak.data_ptr()
+            arr[i].v = av.data_ptr()
+            arr[i].layer_stride = ak.stride(0) if na else 0
+            arr[i].n_tok = na
+            arr[i].offset = row
+            row += na
         return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
 
     def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None, layer_stride=None):
@@ -722,9 +754,11 @@ class FusionEngine:
     def _stage(self, plans: list[_Plan], b: _Bufs, queries, stream=None) -> dict:
         """Host -> device copies of the batch's inputs (chunk descriptors,
         token tables, probe rows). Returns the byte counts."""
-        descs, toks, rows = [], [], []
+        descs, toks, rows, adescs, adeltas = [], [], [], [], []
         for plan, qt in zip(plans, queries):
             descs.append(self._desc_bytes(plan.records, plan.offsets))
+            adescs.append(self._anchor_desc_bytes(plan.records, plan.offsets))
+            adeltas.append(np.asarray(plan.offsets, np.int32))
             t = np.zeros(b.R, np.int32)
             body = np.concatenate([[BOS_ID], *[r.token_ids for r in plan.records], np.asarray(qt, np.int64)])
             t[:body.size] = body
@@ -733,12 +767,16 @@ class FusionEngine:
         desc = torch.cat(descs)
         tok = np.concatenate(toks)
         rows = np.concatenate(rows)
+        adesc = torch.cat(adescs)
+        adelta = np.concatenate(adeltas)
         s = stream or torch.cuda.current_stream()
         with torch.cuda.stream(s):
+            b.adesc.copy_(adesc.pin_memory(), non_blocking=True)
+            b.adelta.copy_(torch.from_numpy(adelta).pin_memory(), non_blocking=True)
             b.desc.copy_(desc.pin_memory(), non_blocking=True)
             b.tok.copy_(torch.from_numpy(tok).pin_memory(), non_blocking=True)
             b.anchor_rows[:rows.size].copy_(torch.from_numpy(rows).pin_memory(), non_blocking=True)
-        return {"h2d": desc.numel() + tok.nbytes + rows.nbytes}
+        return {"h2d": desc.numel() + tok.nbytes + rows.nbytes + adesc.numel() + adelta.nbytes}
 
     def _launch(self, plans: list[_Plan], b: _Bufs, stream=None) -> None:
         """Every kernel of one (batched) fused prefill, in order (module docstring)."""
@@ -748,17 +786,35 @@ class FusionEngine:
         row_elems = cfg.n_kv_heads * cfg.d_head
         esz = b.fk.element_size()
         nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
+        n_ch = len(plan.records)
+        probe = plan.policy == "QCFuse" and n_sel > 0
+        # K1 (assembly, HBM-bound on the chunk pool) and K2+K3 (probe, HBM-bound on the
+        # weights) are independent: with `concurrent` the assembly runs on a forked
+        # stream and joins before scoring (graph capture records the fork/join)
+        fork = probe and self.concurrent and B * n_ch > 0
+        main = stream or torch.cuda.current_stream()
+        asm_stream = main
+        if fork:
+            if self._aux is None:
+                self._aux = torch.cuda.Stream(device=self.device)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self._aux.wait_event(ev)
+            asm_stream = self._aux
         for r in range(B):   # K1: assembly into request r's slice of the batch table
             self._assemble_into(plan.records, plan.offsets, n_ctx,
                                 _view_rows(b.fk, r * b.R), _view_rows(b.fv, r * b.R),
-                                _DescView(b.desc, r * nd), stream, layer_stride=b.fk.stride(0))
-        if plan.policy == "QCFuse" and n_sel > 0:
-            for r in range(B):   # K2: probe prefix rows of request r
-                call("qcf_gather_rows", b.fk.data_ptr() + r * b.R * row_elems * esz,
-                     b.fv.data_ptr() + r * b.R * row_elems * esz, b.fk.stride(0),
-                     b.anchor_rows.data_ptr() + r * b.n_pre * 4, b.n_pre,
-                     b.pk.data_ptr() + r * b.P * row_elems * esz, b.pv.data_ptr() + r * b.P * row_elems * esz,
-                     b.pk.stride(0), c, row_elems, self.weights.qcf_dtype, s)
+                                _DescView(b.desc, r * nd), asm_stream, layer_stride=b.fk.stride(0))
+        if fork:
+            joined = torch.cuda.Event()
+            joined.record(asm_stream)
+        if probe:
+            for r in range(B):   # K2: probe prefix rows of request r from the chunks' anchor rows
+                call("qcf_assemble_rot", b.adesc.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k.data_ptr(),
+                     self._bos_v.data_ptr(), b.pk.data_ptr() + r * b.P * row_elems * esz,
+                     b.pv.data_ptr() + r * b.P * row_elems * esz, b.pk.stride(0), c, cfg.n_kv_heads, cfg.d_head,
+                     self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(), self.ex.rope.n_pos,
+                     b.adelta.data_ptr() + r * n_ch * 4, b.max_delta, self.weights.qcf_dtype, s)
             # K3: probe layers 1..c-1 + layer c's Q, all B*q rows at once
             ex.embed(b.sc_probe, B * q, b.tok, rows=b.p_tok, stream=stream)
             for li in range(c - 1):
@@ -766,6 +822,8 @@ class FusionEngine:
                          n_req=B)
             ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
                      q_only=True, q_out=b.qc[0], stream=stream, n_req=B)
+            if fork:
+                main.wait_event(joined)
             # K4: scoring of the whole batch (request r's keys at rows r*R+1.. of layer c)
             self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream, n_req=B,
                             k_req_stride=b.R * row_elems)
