@@ -179,6 +179,18 @@ int qcf_attention(int dtype, const void* q, const void* k, const void* v,
 int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
                           const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
                           int64_t n_keys, void* out, qcf_stream_t stream);
+/* Same with a caller-owned workspace (>= qcf_attention_workspace bytes): with
+ * qcf_set_attention_split(n > 1) and tile pairs that fit in one wave of CTAs,
+ * every pair's key range is split into n chunks (split-KV) whose pieces a
+ * second kernel combines. Off by default: slower than single tiles at the
+ * one-request fused shape on B200 (tools/attn_bench.py). */
+size_t qcf_attention_workspace(int64_t m, int n_req, int h);   /* 0 when no split applies */
+int qcf_attention_split(int64_t m, int n_req, int h);          /* the split-KV factor (1 = none) */
+int qcf_set_attention_split(int n_split);                       /* 0 = off (default), 2..16 */
+int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void* v,
+                             const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
+                             int64_t n_keys, void* out, void* ws, size_t ws_bytes,
+                             qcf_stream_t stream);
 /* Tuning knob (process-wide): tcgen05 attention kernel 1 = one 128-row query
  * tile per CTA, P staged through shared memory; 2 = two query tiles per CTA
  * ping-ponging on the tensor core, P kept in TMEM; 0 (default) = 2 when the

@@ -63,7 +63,11 @@ SIGNATURES: dict[str, tuple] = {
                                _SZ, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_attention_batched": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P]),
+    "qcf_attention_workspace": (_SZ, [_I64, _I, _I]),
+    "qcf_attention_split": (_I, [_I64, _I, _I]),
+    "qcf_attention_batched_ws": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P, _SZ, _P]),
     "qcf_set_attention_kernel": (_I, [_I]),
+    "qcf_set_attention_split": (_I, [_I]),
     "qcf_set_gemm_plan": (_I, [_I]),
     "qcf_score_workspace": (_SZ, [_I64, _I, _I]),
     "qcf_score": (_I, [_I, _P, _P, _I64, _I, _I, _I, _I, _D, _I, _I, _P, _P, _SZ, _P]),
@@ -114,7 +118,7 @@ def check(status: int, what: str = "") -> None:
 # kernels launched per successful call (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {"qcf_score": 3}
 _NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
-               "qcf_score_batched_workspace", "qcf_set_attention_kernel", "qcf_set_gemm_plan",
+               "qcf_score_batched_workspace", "qcf_attention_workspace", "qcf_attention_split", "qcf_set_attention_kernel", "qcf_set_gemm_plan", "qcf_set_attention_split",
                "qcf_topn_workspace", "qcf_gemm_workspace"}
 launch_count = 0
 
@@ -163,6 +167,9 @@ def _kernels_per_call(name: str, args: tuple) -> int:
         per_row = 8 * (h * n_keys + 2 * h)
         chunk = max(1, min(n_rows, (ws_bytes - 8 * n_keys - 256) // per_row))
         return 3 * ((n_rows + chunk - 1) // chunk)
+    if name == "qcf_attention_batched_ws" and args[12] and args[0] == QCF_BF16:
+        # split-KV adds the combine kernel
+        return 2 if lib.qcf_attention_split(args[5], args[6], args[7]) > 1 else 1
     if name == "qcf_score_batched":
         # tensor-core path: 3 kernels for the whole batch; SIMT path: 3 per request
         dtype, n_req, precise = args[0], args[6], args[12]

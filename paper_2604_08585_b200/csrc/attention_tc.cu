@@ -435,8 +435,13 @@ template <int SPLIT>
 __global__ void __launch_bounds__(A2Cfg<SPLIT>::THREADS, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
-                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int mirrored) {
+                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int mirrored,
+                int n_split, float* __restrict__ ws_o, float2* __restrict__ ws_ml) {
+  // split-KV (n_split > 1, one-wave grids): CTA (pair, chunk) covers key tiles
+  // [chunk*n/n_split, (chunk+1)*n/n_split) of the pair's range and leaves an
+  // unnormalised fp32 O + (max, sum) per row for attn_combine_kernel
   const int req = blockIdx.z;
+  const int pair_y = (int)blockIdx.y / n_split, chunk = (int)blockIdx.y % n_split;
   kmax += (int64_t)req * M;
   out += (int64_t)req * M * H * AT_D;
   extern __shared__ uint8_t smem_raw[];
@@ -462,14 +467,14 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
   const int n_pairs = (n_qt + 1) / 2;
   int tile0, tile1;
   if (mirrored) {
-    const int pidx = n_pairs - 1 - (int)blockIdx.y;
+    const int pidx = n_pairs - 1 - pair_y;
     tile0 = pidx;
     tile1 = n_qt - 1 - pidx;
     if (tile1 == tile0) tile1 = -1;
   } else {
     // adjacent pairs counted from the LAST tile (longest key ranges first, LPT);
     // an odd tile count leaves tile 0 -- the shortest -- without a partner
-    const int hi = n_qt - 1 - 2 * (int)blockIdx.y;
+    const int hi = n_qt - 1 - 2 * pair_y;
     tile0 = hi - 1;
     tile1 = hi;
     if (tile0 < 0) { tile0 = hi; tile1 = -1; }
@@ -514,8 +519,12 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nt0 = (s_kend[0] + AT_BN - 1) / AT_BN;
-  const int nt1 = (s_kend[1] + AT_BN - 1) / AT_BN;
+  const int nt0_full = (s_kend[0] + AT_BN - 1) / AT_BN;
+  const int nt1_full = (s_kend[1] + AT_BN - 1) / AT_BN;
+  const int nfull = max(nt0_full, nt1_full);
+  const int jb = chunk * nfull / n_split, je = (chunk + 1) * nfull / n_split;  // key tiles of this CTA
+  const int nt0 = max(0, min(nt0_full, je) - jb);
+  const int nt1 = max(0, min(nt1_full, je) - jb);
   const int nmax = max(nt0, nt1);
 
   if (warp == 0) {
@@ -532,16 +541,16 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
         mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
         uint8_t* k = sK + st * AT_TILE_BYTES;
-        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
-        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, (jb + j) * AT_BN, req);
+        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, (jb + j) * AT_BN, req);
       };
       auto load_v = [&](int j) {
         const int st = j & 1;
         mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
         uint8_t* v = sV + st * AT_TILE_BYTES;
-        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
-        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, (jb + j) * AT_BN, req);
+        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, (jb + j) * AT_BN, req);
       };
       load_k(0);
       for (int j = 0; j < nmax; ++j) {
@@ -618,7 +627,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
     for (int j = 0; j < n_my; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const int lim = my_kmax - j * AT_BN;  // columns <= lim are visible
+      const int lim = my_kmax - (jb + j) * AT_BN;  // columns <= lim are visible
       const bool all_vis = __all_sync(0xffffffffu, lim >= 127);
       const bool none_vis = __all_sync(0xffffffffu, lim < 0);
       uint32_t v0[32], v1[32], v2[32], v3[32];   // the whole S row stays in registers
@@ -746,7 +755,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
     for (int j = 0; j < n_my; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const int lim = my_kmax - j * AT_BN - ch * 64;  // columns <= lim are visible
+      const int lim = my_kmax - (jb + j) * AT_BN - ch * 64;  // columns <= lim are visible
       const bool all_vis = __all_sync(0xffffffffu, lim >= 63);
       const bool none_vis = __all_sync(0xffffffffu, lim < 0);
       float pmax = -INFINITY;
@@ -842,8 +851,32 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    // epilogue: combine the two half-row sums, then O / l for this warp's 64 output dims
-    if (n_my > 0) {
+    // split-KV: this CTA's piece of the row -> (max, sum) + unnormalised fp32 O
+    if (n_split > 1 && my_tile >= 0) {
+      const int64_t base = (((int64_t)req * H + head) * n_qt + my_tile) * n_split + chunk;
+      float lt = 0.f;
+      if (n_my > 0) {
+        named_bar(bar_id, 64);
+        red[t][0][ch][r] = l;
+        named_bar(bar_id, 64);
+        lt = red[t][0][0][r] + red[t][0][1][r];
+        mbar_wait(&o_full[t], 0);
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t o[32];
+          tmem_ld32(tO + ch * 64 + hh * 32, o);
+          tmem_ld_wait();
+          float* dst = ws_o + (base * AT_BM + r) * AT_D + ch * 64 + hh * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(o[i]), __uint_as_float(o[i + 1]),
+                                                              __uint_as_float(o[i + 2]), __uint_as_float(o[i + 3]));
+        }
+      }
+      if (ch == 0) ws_ml[base * AT_BM + r] = make_float2(n_my > 0 ? m_ref : -INFINITY, lt);
+    } else if (n_my > 0) {
+      // epilogue: combine the two half-row sums, then O / l for this warp's 64 output dims
       named_bar(bar_id, 64);
       red[t][0][ch][r] = l;
       named_bar(bar_id, 64);
@@ -880,6 +913,45 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
   }
 }
 
+// split-KV combine: out[row, head] = sum_c 2^(m_c - M) O_c / sum_c 2^(m_c - M) l_c
+// (m in the log2 domain of the kernel's lazy reference max). One warp per
+// (row, head), 4 output dims per lane.
+__global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restrict__ ws_o,
+                                                           const float2* __restrict__ ws_ml, int M, int H,
+                                                           int n_split, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.x * 4 + warp;
+  const int row = blockIdx.y, req = blockIdx.z;
+  if (head >= H) return;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int tile = row / AT_BM, r = row % AT_BM;
+  const int64_t base0 = (((int64_t)req * H + head) * n_qt + tile) * n_split;
+  float mx = -INFINITY;
+  for (int c = 0; c < n_split; ++c) mx = fmaxf(mx, ws_ml[(base0 + c) * AT_BM + r].x);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float L = 0.f;
+  for (int c = 0; c < n_split; ++c) {
+    const float2 ml = ws_ml[(base0 + c) * AT_BM + r];
+    if (ml.x == -INFINITY) continue;
+    const float w = ex2_approx(ml.x - mx);
+    const float4 o = *reinterpret_cast<const float4*>(ws_o + ((base0 + c) * AT_BM + r) * AT_D + lane * 4);
+    acc.x += w * o.x; acc.y += w * o.y; acc.z += w * o.z; acc.w += w * o.w;
+    L += w * ml.y;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  *reinterpret_cast<uint2*>(out + (((int64_t)req * M + row) * H + head) * AT_D + lane * 4) =
+      make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+size_t attention_workspace(int64_t m, int n_req, int h, int n_split) {
+  if (n_split <= 1) return 0;
+  const int64_t n_qt = (m + AT_BM - 1) / AT_BM;
+  return (size_t)n_req * h * n_qt * n_split * AT_BM * (AT_D * sizeof(float) + sizeof(float2)) + 256;
+}
+
 static int g_attn_ver = -1;  // QCF_ATTN env / qcf_set_attention_kernel: 1 = single-tile, 2 = ping-pong (default)
 
 static int g_attn_split = 2;  // v2 softmax layout: 2 = half rows (default), 1 = full row per thread (knob 3)
@@ -890,8 +962,32 @@ void set_attention_kernel(int v) {
   g_attn_ver = (v == 1 || v == 2) ? v : 0;
 }
 
+static int g_attn_nsplit = -1;  // QCF_ATTN_SPLIT env / qcf_set_attention_split: split-KV factor (one-wave grids)
+
+void set_attention_split(int n) { g_attn_nsplit = n > 0 ? n : 0; }
+
+// split-KV factor for a one-wave grid: ~2 waves of CTAs, at most 8 chunks
+int attention_auto_split(int64_t m, int n_req, int h) {
+  if (g_attn_nsplit < 0) {
+    const char* e = getenv("QCF_ATTN_SPLIT");
+    g_attn_nsplit = e ? std::max(1, atoi(e)) : 0;
+  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  const int64_t n_pairs = ((m + AT_BM - 1) / AT_BM + 1) / 2;
+  const int64_t grid = (int64_t)h * n_pairs * n_req;
+  if (grid > sms) return 1;
+  // measured on B200 (tools/attn_bench.py): the split pieces pay the per-CTA
+  // prologue/epilogue and the combine pass, and the one-request shape ran 88-120 us
+  // split vs 70 us with single tiles -> opt-in only
+  return g_attn_nsplit > 0 ? g_attn_nsplit : 1;
+}
+
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
-                        int hkv, int d, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
+                        int hkv, int d, int64_t n_keys, void* out, cudaStream_t s, int n_req, void* ws,
+                        size_t ws_bytes) {
   if (d != AT_D || m > INT32_MAX || n_keys > INT32_MAX || n_req > 65535) return QCF_EUNSUPPORTED;
   if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) return QCF_EUNSUPPORTED;
   CUtensorMap mq, mk, mv;
@@ -917,29 +1013,43 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
   const int n_qt = (int)((m + AT_BM - 1) / AT_BM);
   const int n_pairs = (n_qt + 1) / 2;
+  // auto: tile pairs when they span more than one wave; a one-wave grid either
+  // splits every pair's key range (split-KV + combine; needs the workspace and
+  // QCF_ATTN_SPLIT) or runs single tiles (default: measured faster on B200)
+  int n_split = 1;
+  if (g_attn_ver == 0 && g_attn_split == 2 && ws) {
+    n_split = attention_auto_split(m, n_req, h);
+    if (n_split > 1 && ws_bytes < attention_workspace(m, n_req, h, n_split)) n_split = 1;
+  }
+  const int64_t grid_pairs = (int64_t)h * n_pairs * n_req;
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  const bool one_wave = (int64_t)h * n_pairs * n_req <= sms;
-  // auto: tile pairs need more than one wave of CTAs to beat single tiles (a lone
-  // long tile per CTA cannot ping-pong); measured in tools/attn_bench.py
-  const int ver = g_attn_ver ? g_attn_ver : (one_wave ? 1 : 2);
+  const int ver = g_attn_ver ? g_attn_ver : ((grid_pairs > sms || n_split > 1) ? 2 : 1);
   if (ver == 2) {
-    // one wave or less: mirrored pairs balance the per-CTA key ranges
-    static int pair_mode = -1;  // QCF_ATTN_PAIR: 0 adjacent, 1 mirrored, unset = mirrored for one-wave grids
+    static int pair_mode = -1;  // QCF_ATTN_PAIR: 0 adjacent (default), 1 mirrored
     if (pair_mode == -1) {
       const char* e = getenv("QCF_ATTN_PAIR");
-      pair_mode = e ? atoi(e) : 2;
+      pair_mode = e ? atoi(e) : 0;
     }
-    const int mirrored = pair_mode == 2 ? (one_wave ? 1 : 0) : pair_mode;
-    dim3 grid((unsigned)h, (unsigned)n_pairs, (unsigned)n_req);
+    float* ws_o = n_split > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    float2* ws_ml = n_split > 1 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws) +
+                                                            (size_t)n_req * h * n_qt * n_split * AT_BM * AT_D * 4)
+                                : nullptr;
+    dim3 grid((unsigned)h, (unsigned)(n_pairs * n_split), (unsigned)n_req);
     if (g_attn_split == 2)
       QCF_LAUNCH("attn_tc2_kernel<2>", attn_tc2_kernel<2>, dim3(grid), dim3(A2Cfg<2>::THREADS), A2_SMEM, s, mq, mk, mv,
-                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
+                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, pair_mode, n_split, ws_o, ws_ml);
     else
       QCF_LAUNCH("attn_tc2_kernel<1>", attn_tc2_kernel<1>, dim3(grid), dim3(A2Cfg<1>::THREADS), A2_SMEM, s, mq, mk, mv,
-                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, mirrored);
+                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, pair_mode, 1,
+                 (float*)nullptr, (float2*)nullptr);
+    QCF_LAUNCH_CHECK("qcf_attention(tcgen05 pairs)");
+    if (n_split > 1) {
+      QCF_LAUNCH("attn_combine_kernel", attn_combine_kernel, dim3((unsigned)((h + 3) / 4), (unsigned)m, (unsigned)n_req),
+                 dim3(128), 0, s, (const float*)ws_o, (const float2*)ws_ml, (int)m, h, n_split, (__nv_bfloat16*)out);
+    }
   } else {
     dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
     QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m,

@@ -44,9 +44,16 @@ extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, in
   return qcf::gemm_simt_launch(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
 }
 
-extern "C" int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
-                                     const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
-                                     int64_t n_keys, void* out, qcf_stream_t stream) {
+extern "C" int qcf_attention_split(int64_t m, int n_req, int h) { return qcf::attention_auto_split(m, n_req, h); }
+
+extern "C" size_t qcf_attention_workspace(int64_t m, int n_req, int h) {
+  return qcf::attention_workspace(m, n_req, h, qcf::attention_auto_split(m, n_req, h));
+}
+
+extern "C" int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void* v,
+                                        const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
+                                        int64_t n_keys, void* out, void* ws, size_t ws_bytes,
+                                        qcf_stream_t stream) {
   QCF_REQUIRE(q && k && v && kmax && out, QCF_EINVAL, "qcf_attention: null pointer");
   QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && n_keys > 0 && n_req >= 1, QCF_EINVAL,
               "qcf_attention: bad shape");
@@ -55,10 +62,16 @@ extern "C" int qcf_attention_batched(int dtype, const void* q, const void* k, co
   if (m == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
   if (dtype == QCF_BF16 && qcf::tc_ok()) {
-    int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req);
+    int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req, ws, ws_bytes);
     if (st != QCF_EUNSUPPORTED) return st;
   }
   return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req);
+}
+
+extern "C" int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v,
+                                     const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,
+                                     int64_t n_keys, void* out, qcf_stream_t stream) {
+  return qcf_attention_batched_ws(dtype, q, k, v, kmax, m, n_req, h, hkv, d, n_keys, out, nullptr, 0, stream);
 }
 
 extern "C" int qcf_attention(int dtype, const void* q, const void* k, const void* v,
@@ -120,5 +133,11 @@ extern "C" int qcf_set_attention_kernel(int version) {
 extern "C" int qcf_set_gemm_plan(int plan) {
   QCF_REQUIRE((plan & 7) <= 4 && plan >= 0 && plan < 16, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 4, +8 = stream-K on");
   qcf::set_gemm_plan(plan);
+  return QCF_OK;
+}
+
+extern "C" int qcf_set_attention_split(int n_split) {
+  QCF_REQUIRE(n_split >= 0 && n_split <= 16, QCF_EINVAL, "qcf_set_attention_split: 0 (off) .. 16");
+  qcf::set_attention_split(n_split);
   return QCF_OK;
 }

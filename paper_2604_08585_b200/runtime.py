@@ -42,6 +42,7 @@ class Executor:
         self.cfg = weights.config
         self.rope = rope or RopeTable(self.cfg.d_head, self.cfg.rope_theta, weights.device)
         self._scratch: dict[int, Scratch] = {}
+        self._aws: dict[tuple, torch.Tensor] = {}
         # fused QKV+RoPE epilogue: bf16 on a tcgen05 device, head dim a multiple of 32
         self.fused_qkv = (weights.dtype == "bf16" and self.cfg.d_head % 32 == 0
                           and torch.cuda.is_available() and bool(_lib.lib.qcf_tc_available()))
@@ -70,6 +71,19 @@ class Executor:
                         torch.empty(cap, cfg.d_model, dtype=torch.float32, device=dev))
             self._scratch[k] = s
         return s
+
+    def _attn_ws(self, m_per_req: int, n_req: int) -> torch.Tensor | None:
+        """Split-KV workspace of the attention (only when the grid is one wave)."""
+        if self.w.dtype != "bf16":
+            return None
+        n = int(_lib.lib.qcf_attention_workspace(m_per_req, n_req, self.cfg.n_heads))
+        if n == 0:
+            return None
+        t = self._aws.get((m_per_req, n_req))
+        if t is None:
+            t = torch.empty(n, dtype=torch.uint8, device=self.w.device)
+            self._aws[(m_per_req, n_req)] = t
+        return t
 
     # ------------------------------------------------------------------
     def embed(self, sc: Scratch, m: int, tokens: torch.Tensor, rows: torch.Tensor | None = None,
@@ -131,8 +145,10 @@ class Executor:
                  qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
         if q_only:
             return
-        call("qcf_attention_batched", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
-             kmax.data_ptr(), m // n_req, n_req, H, Hkv, D, tab_k.shape[0] // n_req, sc.o.data_ptr(), s)
+        aws = self._attn_ws(m // n_req, n_req)
+        call("qcf_attention_batched_ws", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
+             kmax.data_ptr(), m // n_req, n_req, H, Hkv, D, tab_k.shape[0] // n_req, sc.o.data_ptr(),
+             aws.data_ptr() if aws is not None else None, aws.numel() if aws is not None else 0, s)
         self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.delta, d, m, d, H * D, EPI_STORE, QCF_F32, s)
         sc.pending = True
         self._norm(sc, m, lw.ln2_g, lw.ln2_b, s)

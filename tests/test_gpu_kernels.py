@@ -427,7 +427,7 @@ def _torch_attention_gqa(q, k, v, kmax):
     return torch_attention(q, k.repeat_interleave(H // Hkv, dim=1), v.repeat_interleave(H // Hkv, dim=1), kmax)
 
 
-@pytest.mark.parametrize("version", [1, 2, 3])
+@pytest.mark.parametrize("version", [1, 2, 3, "auto+ws", "split3"])
 @pytest.mark.parametrize("m,n,H,Hkv,n_req,sort", [
     (800, 5153, 4, 4, 3, True), (130, 1000, 8, 2, 2, True), (64, 300, 2, 1, 1, True),
     (1000, 1200, 32, 8, 8, True), (256, 700, 2, 2, 1, False), (383, 900, 4, 4, 2, False)])
@@ -446,12 +446,21 @@ def test_attention_tc_batched_gqa_versions(L, version, m, n, H, Hkv, n_req, sort
         kmax = torch.sort(kmax, dim=1).values
     kmax = kmax.int().contiguous()
     out = torch.empty_like(q)
-    L.call("qcf_set_attention_kernel", version)
+    L.call("qcf_set_attention_kernel", 0 if isinstance(version, str) else version)
+    L.call("qcf_set_attention_split", 3 if version == "split3" else 0)
     try:
-        L.call("qcf_attention_batched", L.QCF_BF16, p(q), p(k), p(v), p(kmax), m, n_req, H, Hkv, D, n, p(out), S())
+        if isinstance(version, str):   # split3: one-wave grids -> tile pairs with split-KV + combine
+            nb = int(L.lib.qcf_attention_workspace(m, n_req, H))
+            ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+            L.call("qcf_attention_batched_ws", L.QCF_BF16, p(q), p(k), p(v), p(kmax), m, n_req, H, Hkv, D, n, p(out),
+                   p(ws), nb, S())
+        else:
+            L.call("qcf_attention_batched", L.QCF_BF16, p(q), p(k), p(v), p(kmax), m, n_req, H, Hkv, D, n, p(out),
+                   S())
         torch.cuda.synchronize()
     finally:
         L.call("qcf_set_attention_kernel", 0)
+        L.call("qcf_set_attention_split", 0)
     for r in range(n_req):
         ref = _torch_attention_gqa(q[r], k[r], v[r], kmax[r].long())
         err = (out[r].float() - ref).abs().max().item()

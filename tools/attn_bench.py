@@ -20,10 +20,14 @@ def bench(m, n_keys, H, Hkv, n_req, kmax, it=20):
     out = torch.empty_like(q)
     flops = 4.0 * H * D * float((kmax.long() + 1).sum())
     res = {}
-    for ver in (1, 2, 3):
+    nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H))
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+    res["auto_split"] = int(_lib.lib.qcf_attention_split(m, n_req, H))
+    for ver in (1, 2, 3, 0):   # 0 = auto with workspace (split-KV for one-wave grids)
         _lib.call("qcf_set_attention_kernel", ver)
-        f = lambda: _lib.call("qcf_attention_batched", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(), kmax.data_ptr(),
-                              m, n_req, H, Hkv, D, n_keys, out.data_ptr(), S)
+        f = lambda: _lib.call("qcf_attention_batched_ws", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                              kmax.data_ptr(), m, n_req, H, Hkv, D, n_keys, out.data_ptr(),
+                              ws.data_ptr() if ver == 0 else None, nb if ver == 0 else 0, S)
         for _ in range(3):
             f()
         torch.cuda.synchronize()
