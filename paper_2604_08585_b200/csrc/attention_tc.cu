@@ -31,7 +31,7 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
 constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
 constexpr int AT_THREADS = 576;  // 2 control warps + 16 softmax warps
 constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
-constexpr int AT_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q, K[2], V[2], P
+constexpr int AT_SMEM = AT_TILE_BYTES * 5 + 1024 + 256;  // Q, K[2], V[2] (P lives in TMEM)
 
 // MN-major SW128 descriptor (B = V: N = head dim contiguous, K = keys):
 // 8-key groups 1024 B apart (SBO), 64-column atoms 16 KB apart (LBO).
@@ -56,327 +56,9 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(AT_THREADS, 1)
-attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-               const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
-               int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out) {
-  // request (batch) index: q/out/kmax are [req][M]..., the K/V tables [req][n_keys]...
-  const int req = blockIdx.z;
-  kmax += (int64_t)req * M;
-  out += (int64_t)req * M * H * AT_D;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + AT_TILE_BYTES;          // [2]
-  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [2]
-  uint8_t* sP = smem + 5 * AT_TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * AT_TILE_BYTES);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [2]  K ring: freed as soon as S_j is computed
-  uint64_t* k_empty = bars + 3;    // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* s_free = bars + 7;     // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint64_t* v_full = bars + 11;    // [2]  V ring: freed when P_j.V_j is done
-  uint64_t* v_empty = bars + 13;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
-  __shared__ int s_kend;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_qt = (M + AT_BM - 1) / AT_BM;
-  const int qt = n_qt - 1 - blockIdx.y;  // longest tiles (largest positions) launch first
-  const int head = blockIdx.x;
-  const int kvh = head / (H / Hkv);
-  const int m0 = qt * AT_BM;
-  constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
-
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&map_q);
-    tma_prefetch_desc(&map_k);
-    tma_prefetch_desc(&map_v);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], N_SOFT);
-    }
-    mbar_init(p_full, N_SOFT);
-    mbar_init(pv_done, 1);
-    fence_barrier_init();
-    s_kend = 0;
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  __syncthreads();
-  pdl_wait();  // barrier init + TMEM alloc overlap the previous kernel's tail
-  pdl_trigger();
-  // key range of this tile = 1 + max kmax over its rows (rows are normally
-  // sorted by position, but the kernel does not rely on it)
-  if (threadIdx.x < AT_BM) {
-    int v = (m0 + (int)threadIdx.x < M) ? kmax[m0 + threadIdx.x] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
-  const uint32_t tS0 = tmem, tO = tmem + 256;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      mbar_expect_tx(q_full, AT_TILE_BYTES);
-      tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
-      tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
-      // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
-      // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
-      auto load_k = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
-        uint8_t* k = sK + st * AT_TILE_BYTES;
-        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
-        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
-      };
-      auto load_v = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
-        uint8_t* v = sV + st * AT_TILE_BYTES;
-        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
-        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
-      };
-      load_k(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) load_k(j + 1);
-        load_v(j);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A, K-major B
-      constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      auto issue_pv = [&](int jj) {
-        const int st = jj & 1;
-        mbar_wait(p_full, jj & 1);
-        mbar_wait(&v_full[st], (jj >> 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < AT_BN / 16; ++kk) {
-          const uint64_t a = umma_desc_k_sw128(sP + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
-          const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
-          mma_bf16(tO, a, b, idesc_o, (jj | kk) != 0);
-        }
-        mma_commit(&v_empty[st]);
-        mma_commit(pv_done);
-      };
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1, sb = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        mbar_wait(&s_free[sb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk) {
-          const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
-          const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
-                             (uint64_t)((kk & 3) * 2);
-          mma_bf16(tS0 + sb * 128, a, b, idesc_s, kk != 0);
-        }
-        mma_commit(&s_full[sb]);
-        mma_commit(&k_empty[st]);
-        if (j > 0) issue_pv(j - 1);
-      }
-      issue_pv(n_tiles - 1);
-    }
-  } else {  // ---------------- softmax / correction / epilogue (warps 2..17)
-    const int g = warp & 3;               // TMEM lane quarter -> rows 32g..32g+31
-    const int cg = (warp - 2) >> 2;       // column group: S keys / O dims 32cg..32cg+31
-    const int r = g * 32 + lane;          // row within the tile == TMEM lane
-    const int row = m0 + r;
-    const int my_kmax = row < M ? kmax[row] : -1;
-    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
-    const int bar_id = 1 + g;             // named barrier of the 4 warps sharing these rows
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tS0 + sb * 128 + cg * 32 + lane_off, v);
-      tmem_ld_wait();
-      const int lim = my_kmax - j * AT_BN - cg * 32;  // columns <= lim are visible
-      const bool all_vis = __all_sync(0xffffffffu, lim >= 31);
-      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
-      float pmax = -INFINITY;
-      if (all_vis) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, __uint_as_float(v[i]));
-      } else if (!none_vis) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
-      }
-      red[sb][cg][r] = pmax * scale_log2;
-      named_bar(bar_id, 128);
-      const float tmax = fmaxf(fmaxf(red[sb][0][r], red[sb][1][r]), fmaxf(red[sb][2][r], red[sb][3][r]));
-      // the previous P.V must be done before P is overwritten or O rescaled
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);
-        tc_fence_after();
-      }
-      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
-      float alpha = 1.f;
-      if (need) {
-        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
-        m_ref = tmax;
-        l *= alpha;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's O slice in TMEM
-        uint32_t o[32];
-        tmem_ld32(tO + cg * 32 + lane_off, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tO + cg * 32 + lane_off),
-            "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
-            "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
-            "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
-            "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
-      // P = exp2(s*scale - m_ref) -> bf16, columns 32cg..32cg+31 of the SW128 K-major P tile
-      uint32_t pk[16];
-      float psum = 0.f;
-      if (none_vis) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = 0u;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
-          float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
-          if (!all_vis) {
-            p0 = (i <= lim) ? p0 : 0.f;
-            p1 = (i + 1 <= lim) ? p1 : 0.f;
-          }
-          psum += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-      }
-      l += psum;
-      const uint32_t atom = smem_u32(sP + (cg >> 1) * (AT_TILE_BYTES / 2) + r * 128);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int chunk = ((cg & 1) * 4 + q) ^ (r & 7);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(atom + chunk * 16), "r"(pk[4 * q]),
-                     "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3]) : "memory");
-      }
-      tc_fence_before();
-      mbar_arrive(&s_free[sb]);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
-      mbar_arrive(p_full);
-    }
-    // epilogue: combine the 4 partial row sums, then O / l for this warp's 32 columns
-    named_bar(bar_id, 128);
-    red[0][cg][r] = l;
-    named_bar(bar_id, 128);
-    const float lt = (red[0][0][r] + red[0][1][r]) + (red[0][2][r] + red[0][3][r]);
-    mbar_wait(pv_done, (n_tiles - 1) & 1);
-    tc_fence_after();
-    const float inv = lt > 0.f ? 1.f / lt : 0.f;
-    uint32_t o[32];
-    tmem_ld32(tO + cg * 32 + lane_off, o);
-    tmem_ld_wait();
-    if (row < M) {
-      __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cg * 32;
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk4;
-        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv, __uint_as_float(o[i + 2 * u + 1]) * inv);
-        *reinterpret_cast<uint4*>(dst + i) = pk4;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// v2: two query tiles per CTA (ping-pong) with P kept in tensor memory.
-//
-// One CTA = (two 128-row query tiles, one head). TMEM: S_t / P_t (cols 128t..)
-// and O_t (cols 256+128t..) for t = 0, 1. Per key tile j the MMA thread issues,
-// in order,  PV(0,j-1)? .. : S(0,j) S(1,j) PV(0,j) S(0,j+1) PV(1,j) S(1,j+1) ...
-// so the tensor core computes one tile's QK^T / PV while the other tile's
-// softmax warps run. P_t,j is written as packed bf16 over the first 64 columns
-// of S_t,j (tcgen05.st) and consumed straight from TMEM as the A operand of
-// O_t += P_t,j . V_j (the .kind::f16 [a-tmem] form) -- no shared-memory round
-// trip. tcgen05 ops of one thread complete in order, so S_t,j+1 (issued after
-// PV_t,j) cannot overwrite P_t,j early, and "S_t,j+1 complete" also means
-// "PV_t,j complete": the lazy O rescale needs no extra barrier.
-// Softmax: 8 warps per tile = 4 TMEM lane quarters x 2 column halves (64 keys /
-// 64 output dims each); the two halves of a row exchange their max via smem.
-// Pairing of query tiles: adjacent (2p, 2p+1) when the grid spans several
-// waves, mirrored (p, n-1-p) -- equal work per CTA -- when it fits in one.
-// ---------------------------------------------------------------------------
-// SPLIT = warps sharing one row (1: a thread owns a full 128-key row -- no
-// cross-warp max exchange; 2: half rows, 8 softmax warps per tile)
-template <int SPLIT>
-struct A2Cfg {
-  static constexpr int THREADS = 64 + 2 * 4 * SPLIT * 32;
-  static constexpr int W = 128 / SPLIT;  // keys / output dims per softmax thread
-};
 #ifndef A2_EMU16
 #define A2_EMU16 7  // of every 16 column pairs, this many take the FMA-pipe exp2 (balances MUFU vs FMA)
 #endif
-constexpr int A2_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q[2], K[2], V[2]
-
-__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&o)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
-      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
-      "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
-      "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
-}
-
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
-      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]));
-}
-
 // ---- softmax arithmetic helpers (packed f32x2 FFMA2/FADD2, 3-input max, exp2
 // emulated on the FMA pipe for part of the columns: B200's MUFU ex2 rate (16/clk/SM)
 // would otherwise bound the softmax below the tensor core's rate)
@@ -430,6 +112,343 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&o)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
+      "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
+      "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+      "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]));
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+               const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
+               int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  // request (batch) index: q/out/kmax are [req][M]..., the K/V tables [req][n_keys]...
+  const int req = blockIdx.z;
+  kmax += (int64_t)req * M;
+  out += (int64_t)req * M * H * AT_D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + AT_TILE_BYTES;          // [2]
+  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * AT_TILE_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;     // [2]  K ring: freed as soon as S_j is computed
+  uint64_t* k_empty = bars + 3;    // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* s_free = bars + 7;     // [2]
+  uint64_t* p_full = bars + 9;     // [2]  per TMEM P buffer (one phase per use: no parity aliasing)
+  uint64_t* pv_done = bars + 11;   // [2]
+  uint64_t* v_full = bars + 13;    // [2]  V ring: freed when P_j.V_j is done
+  uint64_t* v_empty = bars + 15;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
+  __shared__ int s_kend;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int qt = n_qt - 1 - blockIdx.y;  // longest tiles (largest positions) launch first
+  const int head = blockIdx.x;
+  const int kvh = head / (H / Hkv);
+  const int m0 = qt * AT_BM;
+  constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], N_SOFT);
+      mbar_init(&p_full[s], N_SOFT);
+      mbar_init(&pv_done[s], 1);
+    }
+    fence_barrier_init();
+    s_kend = 0;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  __syncthreads();
+  pdl_wait();  // barrier init + TMEM alloc overlap the previous kernel's tail
+  pdl_trigger();
+  // key range of this tile = 1 + max kmax over its rows (rows are normally
+  // sorted by position, but the kernel does not rely on it)
+  if (threadIdx.x < AT_BM) {
+    int v = (m0 + (int)threadIdx.x < M) ? kmax[m0 + threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
+  const uint32_t tS0 = tmem, tO = tmem + 256, tP0 = tmem + 384;  // S[2] | O | P[2] (64 cols each)
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      mbar_expect_tx(q_full, AT_TILE_BYTES);
+      tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
+      tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
+      // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
+      // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
+      auto load_k = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
+        uint8_t* k = sK + st * AT_TILE_BYTES;
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      };
+      auto load_v = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
+        uint8_t* v = sV + st * AT_TILE_BYTES;
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      };
+      load_k(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) load_k(j + 1);
+        load_v(j);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A, K-major B
+      constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_pv = [&](int jj) {
+        const int st = jj & 1;
+        mbar_wait(&p_full[st], (jj >> 1) & 1);
+        mbar_wait(&v_full[st], (jj >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk) {   // A = P_jj straight from TMEM (packed bf16)
+          const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
+          mma_bf16_ts(tO, tP0 + st * 64 + kk * 8, b, idesc_o, (jj | kk) != 0);
+        }
+        mma_commit(&v_empty[st]);
+        mma_commit(&pv_done[st]);
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1, sb = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        mbar_wait(&s_free[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk) {
+          const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+          const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
+                             (uint64_t)((kk & 3) * 2);
+          mma_bf16(tS0 + sb * 128, a, b, idesc_s, kk != 0);
+        }
+        mma_commit(&s_full[sb]);
+        mma_commit(&k_empty[st]);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_tiles - 1);
+    }
+  } else {  // ---------------- softmax / correction / epilogue (warps 2..17)
+    const int g = warp & 3;               // TMEM lane quarter -> rows 32g..32g+31
+    const int cg = (warp - 2) >> 2;       // column group: S keys / O dims 32cg..32cg+31
+    const int r = g * 32 + lane;          // row within the tile == TMEM lane
+    const int row = m0 + r;
+    const int my_kmax = row < M ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const int bar_id = 1 + g;             // named barrier of the 4 warps sharing these rows
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tS0 + sb * 128 + cg * 32 + lane_off, v);
+      tmem_ld_wait();
+      const int lim = my_kmax - j * AT_BN - cg * 32;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= 31);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      float pmax = -INFINITY;
+      if (all_vis) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, __uint_as_float(v[i]));
+      } else if (!none_vis) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
+      }
+      red[sb][cg][r] = pmax * scale_log2;
+      named_bar(bar_id, 128);
+      const float tmax = fmaxf(fmaxf(red[sb][0][r], red[sb][1][r]), fmaxf(red[sb][2][r], red[sb][3][r]));
+      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
+        m_ref = tmax;
+        l *= alpha;
+      }
+      // P buffer j&1 was read by P_{j-2}.V_{j-2}; the O rescale needs P_{j-1}.V_{j-1}
+      if (j >= 2) {
+        mbar_wait(&pv_done[j & 1], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      const bool rescale = j > 0 && __any_sync(0xffffffffu, need);
+      if (rescale) {
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+      }
+      if (rescale) {  // rescale this warp's O slice in TMEM
+        uint32_t o[32];
+        tmem_ld32(tO + cg * 32 + lane_off, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tO + cg * 32 + lane_off),
+            "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]),
+            "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
+            "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
+            "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      // P = exp2(s*scale - m_ref) -> packed bf16 for keys 32cg..32cg+31 (TMEM P buffer j&1)
+      uint32_t pk[16];
+      float psum = 0.f;
+      if (none_vis) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = 0u;
+      } else {
+        if (all_vis) {  // packed f32x2 math, part of the exp2 on the FMA pipe
+          const uint64_t sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_ref, -m_ref);
+          uint64_t l2 = f2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
+            uint64_t p2;
+            if (((i >> 1) & 15) < A2_EMU16) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float a, b;
+              f2_split(x2, a, b);
+              p2 = f2(ex2_approx(a), ex2_approx(b));
+            }
+            l2 = fadd2(l2, p2);
+            float p0, p1;
+            f2_split(p2, p0, p1);
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+          float la, lb;
+          f2_split(l2, la, lb);
+          psum = la + lb;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
+            float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
+            p0 = (i <= lim) ? p0 : 0.f;
+            p1 = (i + 1 <= lim) ? p1 : 0.f;
+            psum += p0 + p1;
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+        }
+      }
+      l += psum;
+      tmem_st16(tP0 + (j & 1) * 64 + cg * 16 + lane_off, pk);  // keys 32cg.. -> P cols 16cg..
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&s_free[sb]);
+      mbar_arrive(&p_full[j & 1]);
+    }
+    // epilogue: combine the 4 partial row sums, then O / l for this warp's 32 columns
+    named_bar(bar_id, 128);
+    red[0][cg][r] = l;
+    named_bar(bar_id, 128);
+    const float lt = (red[0][0][r] + red[0][1][r]) + (red[0][2][r] + red[0][3][r]);
+    mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    uint32_t o[32];
+    tmem_ld32(tO + cg * 32 + lane_off, o);
+    tmem_ld_wait();
+    if (row < M) {
+      __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cg * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk4;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv, __uint_as_float(o[i + 2 * u + 1]) * inv);
+        *reinterpret_cast<uint4*>(dst + i) = pk4;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v2: two query tiles per CTA (ping-pong) with P kept in tensor memory.
+//
+// One CTA = (two 128-row query tiles, one head). TMEM: S_t / P_t (cols 128t..)
+// and O_t (cols 256+128t..) for t = 0, 1. Per key tile j the MMA thread issues,
+// in order,  PV(0,j-1)? .. : S(0,j) S(1,j) PV(0,j) S(0,j+1) PV(1,j) S(1,j+1) ...
+// so the tensor core computes one tile's QK^T / PV while the other tile's
+// softmax warps run. P_t,j is written as packed bf16 over the first 64 columns
+// of S_t,j (tcgen05.st) and consumed straight from TMEM as the A operand of
+// O_t += P_t,j . V_j (the .kind::f16 [a-tmem] form) -- no shared-memory round
+// trip. tcgen05 ops of one thread complete in order, so S_t,j+1 (issued after
+// PV_t,j) cannot overwrite P_t,j early, and "S_t,j+1 complete" also means
+// "PV_t,j complete": the lazy O rescale needs no extra barrier.
+// Softmax: 8 warps per tile = 4 TMEM lane quarters x 2 column halves (64 keys /
+// 64 output dims each); the two halves of a row exchange their max via smem.
+// Pairing of query tiles: adjacent (2p, 2p+1) when the grid spans several
+// waves, mirrored (p, n-1-p) -- equal work per CTA -- when it fits in one.
+// ---------------------------------------------------------------------------
+// SPLIT = warps sharing one row (1: a thread owns a full 128-key row -- no
+// cross-warp max exchange; 2: half rows, 8 softmax warps per tile)
+template <int SPLIT>
+struct A2Cfg {
+  static constexpr int THREADS = 64 + 2 * 4 * SPLIT * 32;
+  static constexpr int W = 128 / SPLIT;  // keys / output dims per softmax thread
+};
+constexpr int A2_SMEM = AT_TILE_BYTES * 6 + 1024 + 256;  // Q[2], K[2], V[2]
+
 
 template <int SPLIT>
 __global__ void __launch_bounds__(A2Cfg<SPLIT>::THREADS, 1)
