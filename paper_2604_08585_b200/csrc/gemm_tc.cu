@@ -822,12 +822,28 @@ void set_gemm_plan(int p) {
 
 // Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
 // weights; A box trimmed to the live rows. Returns splits (1 = no workspace).
+// Split count: the one whose unit count (tiles x splits) fills whole waves of
+// SMs best (each unit streams >= 2 stages of weights); ties -> fewer splits.
+// (An in-kernel "last split reduces" variant measured slower than the separate
+// deterministic reduce kernel: the last CTA's serial partial reads stall its
+// epilogue warps.)
 static int skinny_splits(int64_t m, int64_t n, int64_t k) {
   if (m > 32) return 1;
   const int64_t tiles = (n + 63) / 64, kb = (k + 4 * TC_BK - 1) / (4 * TC_BK);
-  int sp = 1;
-  while (tiles * sp < 2 * sm_count() && kb / (sp * 2) >= 4 && sp < 16) sp *= 2;
-  return sp;
+  const int64_t sms = sm_count();
+  int best = 1;
+  double best_eff = -1.0;
+  for (int sp = 1; sp <= 16; ++sp) {
+    const int64_t kb_per = (kb + sp - 1) / sp;
+    if (kb_per < 2 || (sp - 1) * kb_per >= kb) continue;  // every split gets >= 1 k block
+    const int64_t units = tiles * sp;
+    const double eff = (double)units / (double)(((units + sms - 1) / sms) * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
 }
 
 // [stream-K flags + partials][skinny split-K partials]

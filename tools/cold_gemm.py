@@ -8,11 +8,14 @@ from paper_2604_08585_b200 import _lib
 from paper_2604_08585_b200.model import tile64
 LAY = int(os.environ.get("QCF_TILED", "1"))  # 1 = tile-major weights (production layout)
 n, k = int(sys.argv[1]), int(sys.argv[2])
+if len(sys.argv) > 3:
+    os.environ.setdefault("QCF_MS", sys.argv[3])
 s = torch.cuda.current_stream().cuda_stream
 flush = torch.empty(512 * 1024 * 1024 // 4, device="cuda")
 b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
 b = tile64(b) if LAY else b
-for m in (32, 128, 256, 384, 512, 800, 1024, 1536):
+MS = [int(x) for x in os.environ.get("QCF_MS", "32,128,256,384,512,800,1024,1536").split(",")]
+for m in MS:
     a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
     c = torch.empty(m, n, device="cuda")
     ws = torch.zeros(max(int(_lib.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
