@@ -213,7 +213,7 @@ int qcf_score(int dtype, const void* q, const void* k, int64_t n_ctx, int nq, in
 /* Homogeneous request batch: q [n_req*nq][H][D]; request r's context keys start
  * at k + r*k_req_stride elements (rows of Hkv*D); scores [n_req][n_ctx].
  * bf16 with precise=0 runs on the tensor cores (tcgen05 QK^T in TMEM fused with
- * the row max/sum and the per-key (h,t) mean: 3 launches for the whole batch);
+ * the row max/sum and the per-key (h,t) mean: 4 launches for the whole batch);
  * precise=1 / f32 run the SIMT kernels per request (float64 when precise).
  * workspace >= qcf_score_batched_workspace(...) bytes. */
 size_t qcf_score_batched_workspace(int64_t n_ctx, int nq, int n_req, int h, int hkv);

@@ -173,5 +173,5 @@ def _kernels_per_call(name: str, args: tuple) -> int:
     if name == "qcf_score_batched":
         # tensor-core path: 3 kernels for the whole batch; SIMT path: 3 per request
         dtype, n_req, precise = args[0], args[6], args[12]
-        return 3 if (dtype == QCF_BF16 and not precise and lib.qcf_tc_available()) else 3 * n_req
+        return 4 if (dtype == QCF_BF16 and not precise and lib.qcf_tc_available()) else 3 * n_req
     return KERNELS_PER_CALL.get(name, 1)

@@ -18,6 +18,7 @@
 //   pass 2  every thread owns one key (one TMEM lane): it folds the global
 //           (max, sum) of each column into sum_c exp(s - M_c) / L_c over its G*nt
 //           columns, in registers -> partial[kv head][key].
+//   stats   per (h,t) row: fold the tile partials into (max, 1/sum) once.
 //   final   score[n] = sum over kv heads (fixed order) / (H * nt).
 // Deterministic (no atomics). Work per request: 2 x 2*n_ctx*H*nt*D flop and
 // 2 x n_ctx*Hkv*D*2 bytes of K.
@@ -123,16 +124,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_k, const __grid_constant
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
 
   if (PASS2) {
-    // global (max, 1/sum) of every column from the per-tile partials of pass 1
+    // global (max, 1/sum) of every column, reduced once by score_tc_stats_kernel
     for (int c = threadIdx.x; c < N; c += ST_THREADS) {
       const int head = kvh * G + c % G, t = c / G;
-      const float2* p = stats + ((int64_t)req * H * nt + (int64_t)head * nt + t) * n_kt;
-      float m = -INFINITY;
-      for (int j = 0; j < n_kt; ++j) m = fmaxf(m, p[j].x);
-      float l = 0.f;
-      for (int j = 0; j < n_kt; ++j) l += p[j].y * st_ex2(p[j].x - m);
-      sM[c] = m;
-      sInv[c] = 1.f / l;
+      const float2 ms = stats[((int64_t)req * H * nt + (int64_t)head * nt + t) * n_kt];
+      sM[c] = ms.x;
+      sInv[c] = ms.y;
     }
     __syncthreads();
   }
@@ -184,6 +181,21 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_k, const __grid_constant
     tc_fence_after();
     tmem_dealloc(tmem, cols);
   }
+}
+
+// between the passes: per (h, t) row, fold the per-key-tile (max, sum) partials
+// into (max, 1/sum), stored in the row's first slot (deterministic order)
+__global__ void score_tc_stats_kernel(float2* __restrict__ stats, int64_t n_rows, int n_kt) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= n_rows) return;
+  float2* p = stats + row * n_kt;
+  float m = -INFINITY;
+  for (int j = 0; j < n_kt; ++j) m = fmaxf(m, p[j].x);
+  float l = 0.f;
+  for (int j = 0; j < n_kt; ++j) l += p[j].y * st_ex2(p[j].x - m);
+  p[0] = make_float2(m, 1.f / l);
 }
 
 __global__ void score_tc_final_kernel(const float* __restrict__ partial, int n_ctx, int Hkv, float inv_rows,
@@ -248,6 +260,10 @@ int score_tc_launch(const void* q, const void* k, int64_t k_req_stride, int64_t 
   QCF_LAUNCH("score_tc_kernel<1>", score_tc_kernel<false>, grid, dim3(ST_THREADS), smem, s, mk, mq, (int)n_ctx, nq,
              t0, nt, h, hkv, d, n_pad, sl2, stats, partial);
   QCF_LAUNCH_CHECK("qcf_score(tcgen05) pass 1");
+  const int64_t n_rows = (int64_t)n_req * h * nt;
+  QCF_LAUNCH("score_tc_stats_kernel", score_tc_stats_kernel, dim3(ceil_div(n_rows, 128)), dim3(128), 0, s, stats, n_rows,
+             n_kt);
+  QCF_LAUNCH_CHECK("qcf_score(tcgen05) stats");
   QCF_LAUNCH("score_tc_kernel<2>", score_tc_kernel<true>, grid, dim3(ST_THREADS), smem, s, mk, mq, (int)n_ctx, nq,
              t0, nt, h, hkv, d, n_pad, sl2, stats, partial);
   QCF_LAUNCH_CHECK("qcf_score(tcgen05) pass 2");
