@@ -17,7 +17,12 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const int32_t* 
   const int tok = rows ? tokens[rows[i] - row_base] : tokens[i];
   const float* src = emb + (int64_t)tok * d;
   float* dst = x + i * d;
-  for (int e = threadIdx.x; e < d; e += blockDim.x) dst[e] = src[e];
+  if ((d & 3) == 0 && !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)) {
+    for (int e = threadIdx.x; e < (d >> 2); e += blockDim.x)
+      reinterpret_cast<float4*>(dst)[e] = __ldg(reinterpret_cast<const float4*>(src) + e);
+  } else {
+    for (int e = threadIdx.x; e < d; e += blockDim.x) dst[e] = src[e];
+  }
 }
 
 __device__ __forceinline__ void row_stats(const float* __restrict__ xr, int d, int lane,
@@ -179,10 +184,12 @@ __global__ void add_rows_kernel(float* __restrict__ x, const float* __restrict__
   }
 }
 
-// lm-head: grid (vocab tiles of 32, rows). Every CTA recomputes LN_f of its
-// row into shared memory (d floats), then each of 8 warps dots 4 vocab rows.
-constexpr int LM_THREADS = 256, LM_VT = 32;
+// lm-head: grid (vocab tiles of LM_VT, rows). Every CTA recomputes LN_f of its
+// row into shared memory (d floats), then each warp dots one vocab row at a
+// time with float4 loads, LM_UNROLL of them in flight per lane.
+constexpr int LM_THREADS = 256, LM_VT = 16, LM_UNROLL = 8;
 
+template <bool VEC>
 __global__ void __launch_bounds__(LM_THREADS) lm_head_kernel(const float* __restrict__ x,
                                                              const int32_t* __restrict__ rows, int d,
                                                              const float* __restrict__ g,
@@ -217,20 +224,40 @@ __global__ void __launch_bounds__(LM_THREADS) lm_head_kernel(const float* __rest
   const float sd = sqrtf(var / d + eps);
   for (int e = threadIdx.x; e < d; e += LM_THREADS) xs[e] = ((xs[e] - mean) / sd) * g[e] + b[e];
   __syncthreads();
+  const int d4 = d >> 2;
   for (int vv = warp; vv < LM_VT; vv += 8) {
     const int v = blockIdx.x * LM_VT + vv;
     if (v >= vocab) break;
-    const float* er = emb + (int64_t)v * d;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    int e = lane;
-    for (; e + 96 < d; e += 128) {
-      a0 = fmaf(xs[e], er[e], a0);
-      a1 = fmaf(xs[e + 32], er[e + 32], a1);
-      a2 = fmaf(xs[e + 64], er[e + 64], a2);
-      a3 = fmaf(xs[e + 96], er[e + 96], a3);
+    float acc = 0.f;
+    if (!VEC) {  // d % 4 != 0 (toy widths): scalar dot
+      const float* er = emb + (int64_t)v * d;
+      for (int e = lane; e < d; e += 32) acc = fmaf(xs[e], er[e], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
+      continue;
     }
-    for (; e < d; e += 32) a0 = fmaf(xs[e], er[e], a0);
-    const float acc = warp_sum((a0 + a1) + (a2 + a3));
+    const float4* er = reinterpret_cast<const float4*>(emb + (int64_t)v * d);
+    const float4* xs4 = reinterpret_cast<const float4*>(xs);
+    for (int e0 = lane; e0 < d4; e0 += 32 * LM_UNROLL) {
+      float4 w[LM_UNROLL];
+#pragma unroll
+      for (int u = 0; u < LM_UNROLL; ++u) {
+        const int e = e0 + u * 32;
+        w[u] = e < d4 ? __ldg(er + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < LM_UNROLL; ++u) {
+        const int e = e0 + u * 32;
+        if (e < d4) {
+          const float4 xv = xs4[e];
+          acc = fmaf(xv.x, w[u].x, acc);
+          acc = fmaf(xv.y, w[u].y, acc);
+          acc = fmaf(xv.z, w[u].z, acc);
+          acc = fmaf(xv.w, w[u].w, acc);
+        }
+      }
+    }
+    acc = warp_sum(acc);
     if (lane == 0) logits[(int64_t)r * vocab + v] = acc;
   }
 }
@@ -322,14 +349,20 @@ int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d, cons
                 qcf_stream_t stream) {
   QCF_REQUIRE(x && g && b && emb && logits && d > 0 && vocab > 0, QCF_EINVAL, "qcf_lm_head: bad args");
   QCF_REQUIRE(d * 4 <= 200 * 1024, QCF_EUNSUPPORTED, "qcf_lm_head: d_model too large");
+  const bool vec = d % 4 == 0 && !(((uintptr_t)emb) & 15);
   if (n_rows == 0) return QCF_OK;
   const size_t smem = (size_t)d * sizeof(float);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(qcf::lm_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(qcf::lm_head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(qcf::lm_head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return qcf::cuda_status(e, "qcf_lm_head attr");
   }
   dim3 grid((unsigned)((vocab + qcf::LM_VT - 1) / qcf::LM_VT), (unsigned)n_rows);
-  QCF_LAUNCH("lm_head_kernel", qcf::lm_head_kernel, dim3(grid), dim3(qcf::LM_THREADS), smem, qcf::as_stream(stream), x, rows, d, g, b, eps, emb, vocab, logits);
+  if (vec)
+    QCF_LAUNCH("lm_head_kernel", qcf::lm_head_kernel<true>, dim3(grid), dim3(qcf::LM_THREADS), smem, qcf::as_stream(stream), x, rows, d, g, b, eps, emb, vocab, logits);
+  else
+    QCF_LAUNCH("lm_head_kernel", qcf::lm_head_kernel<false>, dim3(grid), dim3(qcf::LM_THREADS), smem, qcf::as_stream(stream), x, rows, d, g, b, eps, emb, vocab, logits);
   QCF_LAUNCH_CHECK("qcf_lm_head");
   return QCF_OK;
 }
