@@ -527,3 +527,29 @@ def test_host_pool_pipelined_equals_hbm_pool(tmp_path, dtype, policy):
     lg, sel = e2.fuse(qs[0], reqs[0], 0.2)
     lg1, sel1 = e1.fuse(qs[0], reqs[0], 0.2)
     assert np.array_equal(sel, sel1) and np.array_equal(lg, lg1)
+
+
+def test_llama_width_bf16_against_oracle(tmp_path):
+    """Full Llama-3-8B WIDTH (d 4096, H 32, D 128, F 14336) at the reference's
+    minimum depth (L 4), 2 x 512-token chunks, q 32, r .15: the bf16 speed
+    path (tcgen05 GEMMs / attention / scoring) against the f32 oracle on the
+    same splitmix64 weights and the same chunk KV. Bounds: Top-N overlap >= 0.9,
+    relative first-token logit error < 5e-2, same top-1 token."""
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    oc = O.Config(n_layers=4, n_heads=32, d_model=4096, d_head=128, d_ff=14336, seed=1234)
+    ow = O.init_weights(oc)
+    rng = np.random.default_rng(2024)
+    chunks = [O.precompute_chunk(ow, rng.integers(0, 256, 512), 0.05) for _ in range(2)]
+    query = rng.integers(0, 256, 32).tolist()
+    ref = O.run(ow, chunks, query, 0.15)
+    w = device_weights(ow, "bf16")
+    store = Q.ChunkStore(tmp_path / "s", w.config, dtype="bf16", persist=False)
+    ids = load_oracle_chunks(store, chunks)
+    eng = Q.FusionEngine(w, store)
+    logits, sel = eng.fuse(query, ids, 0.15)
+    overlap = len(set(sel.tolist()) & set(ref.selection.tolist())) / len(sel)
+    err = np.abs(logits - ref.first_logits).max() / np.abs(ref.first_logits).max()
+    print(f"Llama width L4: overlap {overlap:.3f} rel logit err {err:.3e}")
+    assert overlap >= 0.9 and err < 5e-2
+    assert int(np.argmax(logits)) == int(np.argmax(ref.first_logits))
