@@ -998,10 +998,12 @@ int attention_auto_split(int64_t m, int n_req, int h) {
   const int64_t n_pairs = ((m + AT_BM - 1) / AT_BM + 1) / 2;
   const int64_t grid = (int64_t)h * n_pairs * n_req;
   if (grid > sms) return 1;
-  // measured on B200 (tools/attn_bench.py): the split pieces pay the per-CTA
-  // prologue/epilogue and the combine pass, and the one-request shape ran 88-120 us
-  // split vs 70 us with single tiles -> opt-in only
-  return g_attn_nsplit > 0 ? g_attn_nsplit : 1;
+  if (g_attn_nsplit > 0) return g_attn_nsplit;
+  // auto only for grids far below one wave (query-only / decode-like shapes: a few
+  // tiles over a long key range); at the one-request recompute shape (128 pairs)
+  // single tiles measured faster (tools/attn_bench.py)
+  if (grid * 4 > sms) return 1;
+  return (int)std::min<int64_t>(8, std::max<int64_t>(2, (2 * sms + grid - 1) / grid));
 }
 
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,

@@ -58,6 +58,9 @@ for name, n_req, H, Hkv in [("llama batch8", 8, 32, 32), ("llama single", 1, 32,
     print(json.dumps({"shape": name, "m": 800, "keys": 5153, **bench(800, 5153, H, Hkv, n_req, km)}), flush=True)
 km = torch.arange(5152, dtype=torch.int32, device="cuda")[None].contiguous()
 print(json.dumps({"shape": "full prefill causal", "m": 5152, "keys": 5153, **bench(5152, 5153, 32, 32, 1, km)}), flush=True)
+km = (torch.arange(32, dtype=torch.int32) + 5121)[None].cuda().contiguous()
+print(json.dumps({"shape": "query rows only (FullReuse)", "m": 32, "keys": 5153, **bench(32, 5153, 32, 32, 1, km)}),
+      flush=True)
 km = sel_kmax(32768, 4916, 32, 1)
 print(json.dumps({"shape": "mistral 32k single", "m": 4948, "keys": 32801, **bench(4948, 32801, 32, 8, 1, km, it=5)}),
       flush=True)
