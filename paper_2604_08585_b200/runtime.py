@@ -181,6 +181,24 @@ class Executor:
         return (torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device),
                 torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device))
 
+    def forward_full_batch(self, tokens: torch.Tensor, stream=None):
+        """forward_full of B equal-length sequences at once: tokens [B][m] ->
+        tables [L][B*m][Hkv][D] (sequence b owns rows b*m..), one layer stack
+        with the batched attention (n_req = B). Every row's arithmetic is the
+        one forward_full does for it alone (per-row GEMM accumulation order and
+        attention are independent of the batch)."""
+        B, m = tokens.shape
+        self.rope.ensure(m + 1)
+        dev = self.w.device
+        tk, tv = self.new_table(B * m)
+        ar = torch.arange(m, dtype=torch.int32, device=dev)
+        pos = ar.repeat(B)
+        dst = torch.arange(B * m, dtype=torch.int32, device=dev)
+        sc = self.scratch(B * m, key=("full_batch", B * m))
+        self.embed(sc, B * m, tokens.reshape(-1), stream=stream)
+        self.stack(sc, B * m, pos, dst, pos, tk, tv, stream=stream, n_req=B)
+        return tk, tv
+
     def forward_full(self, tokens: torch.Tensor, start: int = 0, tab=None, want_logits_rows=None,
                      stream=None):
         """Full causal forward of `tokens` at positions start.. (model.py:391-400).

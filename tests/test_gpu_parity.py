@@ -553,3 +553,26 @@ def test_llama_width_bf16_against_oracle(tmp_path):
     print(f"Llama width L4: overlap {overlap:.3f} rel logit err {err:.3e}")
     assert overlap >= 0.9 and err < 5e-2
     assert int(np.argmax(logits)) == int(np.argmax(ref.first_logits))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_precompute_batch_equals_precompute(tmp_path, dtype):
+    """Batched chunk precompute (one layer stack over B equal-length chunks)
+    produces the same records as one-at-a-time precompute: K/V bit-identical,
+    same anchors, cache hits for known chunks, mixed lengths grouped."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=5)
+    w = Q.init_weights(cfg, dtype=dtype)
+    rng = np.random.default_rng(1)
+    toks = [rng.integers(0, 256, n) for n in (96, 96, 64, 96, 64)]
+    s1 = Q.ChunkStore(tmp_path / "a", cfg, dtype=dtype, persist=False)
+    s2 = Q.ChunkStore(tmp_path / "b", cfg, dtype=dtype, persist=False)
+    r1 = [s1.precompute(w, t, 0.1) for t in toks]
+    s2.precompute(w, toks[1], 0.1)                    # one already cached
+    r2 = s2.precompute_batch(w, toks + [toks[0]], 0.1)
+    assert s2.manifest.cache_hits == 2                # the cached chunk + the in-call duplicate
+    for a, b in zip(r1, r2):
+        assert a.chunk_id == b.chunk_id
+        assert np.array_equal(a.anchor_indices, b.anchor_indices)
+        assert torch.equal(a.k, b.k) and torch.equal(a.v, b.v)
+    assert r2[-1].chunk_id == r1[0].chunk_id
