@@ -26,6 +26,7 @@ lazily, only when a caller reads them.
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import time
 import weakref
@@ -56,6 +57,15 @@ def _executor_for(weights: ModelWeights) -> Executor:
         ex = Executor(weights)
         _EXECUTORS[weights] = ex
     return ex
+
+
+def _serialized(fn):
+    """Run an engine method under its executor's lock (shared device buffers)."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with self.ex.lock:
+            return fn(self, *args, **kwargs)
+    return wrapper
 
 
 class _DescView:
@@ -499,6 +509,7 @@ class FusionEngine:
     # ------------------------------------------------------------------
     # context assembly (fusion.py:234-263)
     # ------------------------------------------------------------------
+    @_serialized
     def assemble_context(self, chunk_ids: list[str], extra_rows: int = 0) -> FusedContext:
         recs, offs, n_ctx = self._records(chunk_ids)
         cfg = self.config
@@ -514,6 +525,7 @@ class FusionEngine:
     # ------------------------------------------------------------------
     # probing and scoring (fusion.py:269-329)
     # ------------------------------------------------------------------
+    @_serialized
     def probe_query(self, query_tokens, fused: FusedContext, mode: str = PROBE_ANCHORS,
                     layers: int | None = None) -> QueryProbe:
         toks = np.asarray(query_tokens, dtype=np.int64)
@@ -564,6 +576,7 @@ class FusionEngine:
              1 if self.options.query_agg == "last" else 0, 1 if self.score_precise else 0,
              out.data_ptr(), ws.data_ptr(), ws.numel(), cuda_stream(stream))
 
+    @_serialized
     def score_against_keys(self, probe: QueryProbe, fused: FusedContext, layer: int) -> np.ndarray:
         if self.options.query_agg not in ("mean", "last"):
             raise ValueError(f"unknown query_agg: {self.options.query_agg}")
@@ -580,11 +593,13 @@ class FusionEngine:
     def score_critical(self, probe: QueryProbe, fused: FusedContext) -> np.ndarray:
         return self.score_against_keys(probe, fused, self.config.critical_layer)
 
+    @_serialized
     def oracle_importance(self, context_tokens, query_tokens) -> np.ndarray:
         """Critical-layer importance from a full GPU forward over
         [BOS | context | query] (fusion.py:331-346)."""
         return self.importance_at(context_tokens, query_tokens, self.config.critical_layer)
 
+    @_serialized
     def importance_at(self, context_tokens, query_tokens, layer: int) -> np.ndarray:
         """oracle_importance at any layer (the full forward runs layers 1..layer)."""
         ctx = np.asarray(context_tokens, np.int64)
@@ -628,6 +643,7 @@ class FusionEngine:
             scores = self.score_critical(probe, fused)
         return select_topn(scores, ratio, "QCAll")
 
+    @_serialized
     def select(self, policy: str, ratio: float, fused: FusedContext, query_tokens) -> SelectionResult:
         if policy not in POLICIES:
             raise ValueError(f"unknown policy: {policy}")
@@ -654,6 +670,7 @@ class FusionEngine:
         return self.qcfuse_select(query_tokens, fused, ratio)
 
     # ---- layer-1 deviation baselines (fusion.py:352-392) on the device
+    @_serialized
     def _layer1_recompute_pass(self, fused: FusedContext, want_attention: bool = False):
         """Layer 1 recomputed for every context token from raw embeddings
         (fusion.py:352-373): returns (new K [n][Hkv][D], new V, received
@@ -706,6 +723,7 @@ class FusionEngine:
     # ------------------------------------------------------------------
     # recomputation (fusion.py:446-490)
     # ------------------------------------------------------------------
+    @_serialized
     def recompute_selected(self, fused: FusedContext, selection: SelectionResult):
         cfg = self.config
         sel = np.asarray(selection.indices, dtype=np.int64)
@@ -976,6 +994,7 @@ class FusionEngine:
             self._slots = (key, bufs)
         return self._slots[1]
 
+    @_serialized
     def prefill_batch(self, policy: str, ratio: float, chunk_lists, queries, use_graph: bool = True,
                       extra_rows: int = 0, stream=None):
         """Device-side fused prefill of a homogeneous batch (same chunk lengths,
@@ -1018,6 +1037,7 @@ class FusionEngine:
         plans, b = self.prefill_batch(policy, ratio, [chunk_ids], [query_tokens], use_graph, extra_rows, stream)
         return plans[0], b
 
+    @_serialized
     def fuse_batch(self, queries, chunk_lists, ratio: float = 0.15):
         """Batched north-star entry (BASELINE config 3): one fused prefill for
         a homogeneous batch of RAG requests. Returns (logits [B][V] numpy,
@@ -1030,6 +1050,7 @@ class FusionEngine:
         sel = b.rc_pos.view(b.B, b.Mr)[:, :n].cpu().numpy().astype(np.int64)
         return b.logits.cpu().numpy(), [sel[r] for r in range(b.B)]
 
+    @_serialized
     def fuse(self, query, chunk_ids, ratio: float = 0.15):
         """North-star entry: fuse(query, chunks) → (first-token logits [V] f32
         numpy, ascending selected positions). QCFuse policy."""
@@ -1070,6 +1091,7 @@ class FusionEngine:
     # ------------------------------------------------------------------
     # end to end (fusion.py:496-563)
     # ------------------------------------------------------------------
+    @_serialized
     def oracle_run(self, context_tokens, query_tokens, max_new: int | None = None) -> dict:
         """Full-computation reference on the GPU (fusion.py:496-517): a full
         prefill over [BOS | context | query], greedy decode, importance."""
@@ -1093,6 +1115,7 @@ class FusionEngine:
         self._oracle_cache[key] = res
         return res
 
+    @_serialized
     def run(self, policy: str, ratio: float, chunk_ids: list[str], query,
             compare_oracle: bool = False, max_new: int | None = None) -> RunResult:
         if policy not in POLICIES:

@@ -12,6 +12,7 @@ can be captured into a CUDA graph.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -43,6 +44,10 @@ class Executor:
         self.rope = rope or RopeTable(self.cfg.d_head, self.cfg.rope_theta, weights.device)
         self._scratch: dict[int, Scratch] = {}
         self._aws: dict[tuple, torch.Tensor] = {}
+        # the scratch / workspaces are shared by every engine on these weights: one
+        # request at a time runs through them (the reference engine is re-entrant,
+        # fusion.py:211-216, so concurrent Python threads must be safe)
+        self.lock = threading.RLock()
         # fused QKV+RoPE epilogue: bf16 on a tcgen05 device, head dim a multiple of 32
         self.fused_qkv = (weights.dtype == "bf16" and self.cfg.d_head % 32 == 0
                           and torch.cuda.is_available() and bool(_lib.lib.qcf_tc_available()))

@@ -576,3 +576,29 @@ def test_precompute_batch_equals_precompute(tmp_path, dtype):
         assert np.array_equal(a.anchor_indices, b.anchor_indices)
         assert torch.equal(a.k, b.k) and torch.equal(a.v, b.v)
     assert r2[-1].chunk_id == r1[0].chunk_id
+
+
+def test_engine_is_reentrant_across_threads(tmp_path):
+    """The reference engine may be shared by threads (fusion.py:211-216, the
+    FastAPI threadpool): concurrent fuse() calls give the sequential results."""
+    import threading
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=8)
+    w = Q.init_weights(cfg, dtype="bf16")
+    store = Q.ChunkStore(tmp_path / "s", cfg, dtype="bf16", persist=False)
+    ids = [store.precompute(w, np.random.default_rng(i).integers(0, 256, 80), 0.05).chunk_id for i in range(3)]
+    eng = Q.FusionEngine(w, store)
+    qs = [np.random.default_rng(100 + i).integers(0, 256, 8).tolist() for i in range(6)]
+    ref = [eng.fuse(q, ids, 0.2) for q in qs]
+    got = [None] * len(qs)
+
+    def work(i):
+        got[i] = eng.fuse(qs[i], ids, 0.2)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(qs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (l1, s1), (l2, s2) in zip(ref, got):
+        assert np.array_equal(s1, s2) and np.array_equal(l1, l2)
