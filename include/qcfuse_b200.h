@@ -198,7 +198,8 @@ int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void
 int qcf_set_attention_kernel(int version);
 /* Tuning knob (process-wide): tcgen05 GEMM tile plan for M > 32. 0 (default) =
  * wave-quantisation model; 1 = 2-CTA 256x256; 2 = 1-CTA 128x256; 3 = 128x128;
- * 4 = 128x64 (falls back to auto when the shape does not fit the plan);
+ * 4 = 128x64; 5 = 2-CTA 128x256 (64 rows per CTA) (falls back to auto when the
+ * shape does not fit the plan);
  * +8 = stream-K schedule for the 2-CTA kernel (off by default: slower here). */
 int qcf_set_gemm_plan(int plan);
 

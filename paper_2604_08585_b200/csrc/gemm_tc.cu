@@ -305,13 +305,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // CTA r holds A rows [128r, 128r+128) and B rows [r*BN/2, (r+1)*BN/2) of the tile,
 // the leader (rank 0) issues the MMAs, each CTA's TMEM holds its 128 output rows.
 // Per SM this halves the B bytes per MMA cycle, doubling the TMA lookahead.
-template <int BN>
+// PM = the pair's M: 256 (each CTA 128 rows, one TMEM lane per row) or 128
+// (each CTA 64 rows; the accumulator uses the "2x2" TMEM layout: lanes 0-63 hold
+// columns [0, BN/2) of rows 0-63, lanes 64-127 columns [BN/2, BN) of the same
+// rows -- BN/2 TMEM columns per accumulator). PM = 128 halves the row padding
+// and doubles the unit count of small-M GEMMs (one request: M = 800).
+template <int BN, int PM = 256>
 struct Tc2Cfg {
-  static constexpr int STAGES = 6;
-  static constexpr int A_BYTES = TC_BM * TC_BK * 2;          // 16 KB (this CTA's 128 rows)
-  static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;       // this CTA's half of B
+  static constexpr int ROWS = PM / 2;                         // A rows per CTA
+  static constexpr int STAGES = PM == 256 ? 6 : 8;
+  static constexpr int A_BYTES = ROWS * TC_BK * 2;            // this CTA's rows
+  static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;        // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int ACC_COLS = PM == 256 ? BN : BN / 2;    // TMEM columns per accumulator
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
@@ -358,12 +365,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN>
+template <int BN, int PM = 256>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int sk,
                 int* __restrict__ sk_flags, float* __restrict__ sk_part, int group_m) {
-  using Cfg = Tc2Cfg<BN>;
+  using Cfg = Tc2Cfg<BN, PM>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -377,7 +384,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const int m_pairs = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+  const int m_pairs = (M + PM - 1) / PM;
   const int n_tiles = (N + BN - 1) / BN;
   const int n_work = m_pairs * n_tiles;
   const int k_blocks = (K + TC_BK - 1) / TC_BK;
@@ -430,7 +437,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       while (sg.next(w, kbs, kbe)) {
         int mp, nb;
         coords(w, mp, nb);
-        const int arow = mp * 2 * TC_BM + rank * TC_BM;
+        const int arow = mp * PM + rank * Cfg::ROWS;
         const int brow = nb * BN + rank * (BN / 2);
         for (int kb = kbs; kb < kbe; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
@@ -447,7 +454,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
-      constexpr uint32_t idesc = idesc_bf16_f32(2 * TC_BM, BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(PM, BN);
       uint32_t it = 0, t = 0;
       SegIter sg = segs();
       int w, kbs, kbe;
@@ -455,7 +462,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const int acc = t & 1;
         mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_COLS;
         for (int kb = kbs; kb < kbe; ++kb, ++it) {
           const int s = it % Cfg::STAGES;
           const uint32_t ph = (it / Cfg::STAGES) & 1;
@@ -484,18 +491,20 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       int mp, nb;
       coords(w, mp, nb);
       const int acc = t & 1;
-      const int rt = g * 32 + lane;  // row within this CTA's 128
-      const int row = mp * 2 * TC_BM + rank * TC_BM + rt;
+      // row within this CTA's rows and first output column of this warp's TMEM half
+      const int rt = PM == 256 ? g * 32 + lane : (g & 1) * 32 + lane;
+      const int cbase = PM == 256 ? 0 : (g >> 1) * (BN / 2);
+      const int row = mp * PM + rank * Cfg::ROWS + rt;
       const bool row_ok = row < M;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
       if (kbs != 0) {
         // ---- a later piece of a split unit: spill the fp32 partial, raise the flag
-        float* dst = sk_part + ((int64_t)(cluster * 2 + rank) * TC_BM + rt) * BN;
+        float* dst = sk_part + ((int64_t)(cluster * 2 + rank) * TC_BM + rt) * BN + cbase;
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        for (int cc = 0; cc < Cfg::ACC_COLS / 32; ++cc) {
           uint32_t r[32];
-          tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(g * 32) << 16), r);
+          tmem_ld32(tmem_base + acc * Cfg::ACC_COLS + cc * 32 + ((uint32_t)(g * 32) << 16), r);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
@@ -521,12 +530,12 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         named_bar_sync(1, 128);
       }
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
+      for (int cc = 0; cc < Cfg::ACC_COLS / 32; ++cc) {
         uint32_t r[32];
-        tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(g * 32) << 16), r);
+        tmem_ld32(tmem_base + acc * Cfg::ACC_COLS + cc * 32 + ((uint32_t)(g * 32) << 16), r);
         tmem_ld_wait();
         for (int c2 = cluster + 1; c2 <= c_last; ++c2) {
-          const float* src = sk_part + ((int64_t)(c2 * 2 + rank) * TC_BM + rt) * BN + cc * 32;
+          const float* src = sk_part + ((int64_t)(c2 * 2 + rank) * TC_BM + rt) * BN + cbase + cc * 32;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 p4 = __ldcg(reinterpret_cast<const float4*>(src + j));
@@ -536,7 +545,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + p4.w);
           }
         }
-        const int col0 = nb * BN + cc * 32;
+        const int col0 = nb * BN + cbase + cc * 32;
         if (!row_ok || col0 >= N) continue;
         epilogue_row32(C, ldc, row, col0, N, r, ea);
       }
@@ -760,17 +769,19 @@ static int launch_bn(const CUtensorMap& ma, const void* b, int64_t ldb, void* c,
 // stream-K workspace: [flags: 4 KB][fp32 partial 128x256 per CTA of the grid]
 static size_t sk_bytes() { return 4096 + (size_t)(sm_count() & ~1) * TC_BM * 256 * sizeof(float); }
 
-template <int BN>
+template <int BN, int PM = 256>
 static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                        int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, void* ws = nullptr,
                        size_t ws_bytes = 0) {
   CUtensorMap mb;
   int st = make_b_map(&mb, b, n, k, ldb, BN / 2, ea.b_tiled);
   if (st != QCF_OK) return st;
+  // the caller's A map has a box of Tc2Cfg<BN, PM>::ROWS rows (this CTA's rows of the tile)
+  const CUtensorMap& ma_pair = ma;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Tc2Cfg<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<BN, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Tc2Cfg<BN, PM>::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc2 attr");
     attr_set = true;
   }
@@ -778,7 +789,7 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
     const char* e = getenv("QCF_GEMM_GROUP");
     g_group_m = e ? atoi(e) : 0;
   }
-  const int64_t work = ((m + 2 * TC_BM - 1) / (2 * TC_BM)) * ((n + BN - 1) / BN);
+  const int64_t work = ((m + PM - 1) / PM) * ((n + BN - 1) / BN);
   const int64_t iters = work * ((k + TC_BK - 1) / TC_BK);
   // stream-K when the caller's workspace holds the flags + partials and the unit
   // count does not fill whole waves of clusters
@@ -790,7 +801,7 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = Tc2Cfg<BN>::SMEM;
+  cfg.dynamicSmemBytes = Tc2Cfg<BN, PM>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -803,8 +814,8 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   // raster band of m pairs (QCF_GEMM_GROUP); default = all m pairs (m fastest). Bands
   // of 4-12 were within run-to-run noise at the fused-path shapes (tools/group_sweep.sh)
-  const int group_m = g_group_m > 0 ? g_group_m : (int)((m + 2 * TC_BM - 1) / (2 * TC_BM));
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, ma, mb, c, ldc, (int)m, (int)n, (int)k, ea, sk, sk_flags,
+  const int group_m = g_group_m > 0 ? g_group_m : (int)((m + PM - 1) / PM);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, PM>, ma_pair, mb, c, ldc, (int)m, (int)n, (int)k, ea, sk, sk_flags,
                                      sk_part, group_m);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 pair)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 pair)");
@@ -812,12 +823,12 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 }
 
 static int g_pair_mode = -1;  // QCF_GEMM_PAIR env: 0 off, 1 on (default on)
-static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64
+static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64, 5 pair-128-rows
 
 void set_gemm_plan(int p) {
   g_streamk = (p & 8) ? 1 : 0;  // +8: stream-K on (measurement)
   p &= 7;
-  g_gemm_plan = (p >= 0 && p <= 4) ? p : 0;
+  g_gemm_plan = (p >= 0 && p <= 5) ? p : 0;
 }
 
 // Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
@@ -924,18 +935,34 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
     case 2: if (n >= 256) return launch_bn<256>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
     case 3: if (n >= 128) return launch_bn<128>(ma, b, ldb, c, ldc, m, n, k, ea, s); break;
     case 4: return launch_bn<64>(ma, b, ldb, c, ldc, m, n, k, ea, s);
+    case 5:
+      if (m >= 96 && n >= 256) {
+        CUtensorMap ma64;
+        st = make_kmajor_map(&ma64, a, m, k, lda, 64);
+        if (st != QCF_OK) return st;
+        return launch_pair<256, 128>(ma64, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes);
+      }
+      break;
     default: break;
   }
   // 2-CTA 256-row tiles vs 1-CTA 128-row tiles: estimate each one's useful
   // fraction (wave quantisation x row padding; 1-CTA pays ~15% for its
   // shallower TMA lookahead) and take the better one
+  // (2-CTA pairs of 128 rows -- plan 5 -- halve the row padding of small M and double
+  // the unit count, but each SM then streams 1.5x the operand bytes per flop: measured
+  // 10-20% slower than the 256-row pairs at M = 800 (tools/gemm_plans.py), so the
+  // automatic choice is between 256-row pairs and 1-CTA tiles)
   if (g_pair_mode && m >= 192 && n >= 256) {
-    const int64_t mps = (m + 255) / 256, units = mps * ((n + 255) / 256), clusters = sms / 2;
-    const double e_pair = (double)units / (double)(((units + clusters - 1) / clusters) * clusters) *
-                          (double)m / (double)(mps * 256);
-    const int64_t t1 = mt * ((n + 255) / 256);
+    const int64_t clusters = sms / 2, nt = (n + 255) / 256;
+    auto eff = [&](int64_t units, int64_t rows_padded) {
+      return (double)units / (double)(((units + clusters - 1) / clusters) * clusters) * (double)m /
+             (double)rows_padded;
+    };
+    const int64_t mps = (m + 255) / 256;
+    const double e_pair = eff(mps * nt, mps * 256);
+    const int64_t t1 = mt * nt;
     const double e_one = 0.85 * (double)t1 / (double)(((t1 + sms - 1) / sms) * sms) * (double)m / (double)(mt * 128);
-    if (units >= clusters / 2 && e_pair >= e_one)
+    if (mps * nt >= clusters / 2 && e_pair >= e_one)
       return launch_pair<256>(ma, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes);
   }
   // tile width: enough tiles to cover the SMs, widest tile otherwise

@@ -502,3 +502,67 @@ def test_gemm_stream_k_matches_data_parallel(L, m, n, k, epi):
     assert (outs[0].float() - ref).abs().max().item() < tol * max(1.0, ref.abs().max().item())
     assert (outs[0].float() - outs[3].float()).abs().max().item() < tol * max(1.0, ref.abs().max().item())
     assert int(ws[:4096].view(torch.int32).abs().sum().item()) == 0
+
+
+@pytest.mark.parametrize("m,n,k,epi", [(800, 4096, 4096, 0), (800, 12288, 1024, 1), (300, 2048, 2048, 0),
+                                       (1100, 4096, 14336, 0), (96, 512, 256, 1), (6400, 1024, 512, 0)])
+def test_gemm_pair_128_rows(L, m, n, k, epi):
+    """2-CTA tiles of 128 rows (64 per CTA, the "2x2" TMEM accumulator layout:
+    lanes 64-127 hold the second half of the columns) vs an fp32 torch
+    reference and vs the 256-row pair plan; tile-major weights."""
+    from paper_2604_08585_b200.model import tile64
+    torch.manual_seed(m + n)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bt = tile64(b)
+    out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
+    tdt = torch.bfloat16 if epi == 1 else torch.float32
+    ws = torch.zeros(int(L.lib.qcf_gemm_workspace(m, n, k)), dtype=torch.uint8, device="cuda")
+    outs = []
+    try:
+        for plan in (5, 1, 5):
+            L.call("qcf_set_gemm_plan", plan)
+            c = torch.full((m, n), 3.0, device="cuda", dtype=tdt)
+            L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(bt), k, p(c), n, m, n, k, epi, out_dt, 1, p(ws), ws.numel(),
+                   S())
+            outs.append(c)
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_gemm_plan", 0)
+    ref = a.float() @ b.float().t()
+    if epi == 1:
+        ref = ref.relu()
+    tol = 2e-2 if epi == 1 else 1e-3
+    scale = max(1.0, ref.abs().max().item())
+    assert (outs[0].float() - ref).abs().max().item() < tol * scale
+    assert torch.equal(outs[0], outs[2])
+    assert (outs[0].float() - outs[1].float()).abs().max().item() < tol * scale
+
+
+def test_fused_qkv_rope_pair_128_rows(L):
+    """The fused QKV + RoPE + KV-scatter epilogue on the 128-row pair plan
+    equals the 256-row pair plan."""
+    from paper_2604_08585_b200.model import RopeTable
+    torch.manual_seed(3)
+    m, heads, D, K = 800, 8, 128, 1024
+    N = 3 * heads * D
+    a = (torch.randn(m, K, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    pos = torch.sort(torch.randperm(6000, device="cuda")[:m]).values.int()
+    dst = torch.randperm(m + 7, device="cuda")[:m].int()
+    rope = RopeTable(D, 10000.0, "cuda", 8192)
+    res = []
+    try:
+        for plan in (5, 1):
+            L.call("qcf_set_gemm_plan", plan)
+            q = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
+            kt = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
+            vt = torch.zeros_like(kt)
+            L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos),
+                   p(rope.sin), rope.n_pos, p(q), p(kt), p(vt), None, 0, S())
+            res.append((q, kt, vt))
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_gemm_plan", 0)
+    for x, y in zip(res[0], res[1]):
+        assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
