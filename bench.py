@@ -246,10 +246,19 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # QCF_BENCH_DEVICES (testing only): GPUs available to the job; ranks share them
+    # round-robin (e.g. 2 ranks on a 1-GPU box with QCF_BENCH_BACKEND=gloo, since NCCL
+    # refuses two ranks on one device). Default: one rank per GPU, NCCL.
+    n_dev = int(os.environ.get("QCF_BENCH_DEVICES", "0")) or torch.cuda.device_count()
+    local = local % max(n_dev, 1)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("QCF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     from paper_2604_08585_b200 import _lib
     from paper_2604_08585_b200.dist import gather_rows, max_over_ranks
 

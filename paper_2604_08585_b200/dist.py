@@ -41,10 +41,11 @@ def gather_rows(local: torch.Tensor, n_total: int, world: int, rank: int,
     pad = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[:local.shape[0]] = local
     out = torch.empty((per * world,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    if dist.get_backend(group) == "gloo":
-        parts = list(out.chunk(world))
-        dist.all_gather(parts, pad, group=group)
-        out = torch.cat(parts)
+    if dist.get_backend(group) == "gloo":   # CPU tests / single-GPU multi-rank testing
+        pad_h = pad.cpu()
+        parts = [torch.empty_like(pad_h) for _ in range(world)]
+        dist.all_gather(parts, pad_h, group=group)
+        out = torch.cat(parts).to(local.device)
     else:
         dist.all_gather_into_tensor(out, pad, group=group)
     if rank != 0:
@@ -57,6 +58,7 @@ def max_over_ranks(value: float, device, group=None) -> float:
     """Max of a scalar over ranks (multi-GPU times are max-over-ranks)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    on_gloo = dist.get_backend(group) == "gloo"
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if on_gloo else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
