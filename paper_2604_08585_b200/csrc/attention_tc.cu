@@ -301,7 +301,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       float pmax = -INFINITY;
       if (all_vis) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, __uint_as_float(v[i]));
+        for (int i = 0; i < 32; i += 2) pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
       } else if (!none_vis) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
@@ -1040,6 +1040,8 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   int n_split = 1;
   if (g_attn_ver == 0 && g_attn_split == 2 && ws) {
     n_split = attention_auto_split(m, n_req, h);
+    // at least two key tiles per chunk (the probe's short anchor prefix stays whole)
+    n_split = (int)std::min<int64_t>(n_split, std::max<int64_t>(1, (n_keys + 2 * AT_BN - 1) / (2 * AT_BN)));
     if (n_split > 1 && ws_bytes < attention_workspace(m, n_req, h, n_split)) n_split = 1;
   }
   const int64_t grid_pairs = (int64_t)h * n_pairs * n_req;
