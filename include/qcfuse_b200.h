@@ -184,8 +184,8 @@ int qcf_attention_batched(int dtype, const void* q, const void* k, const void* v
  * every pair's key range is split into n chunks (split-KV) whose pieces a
  * second kernel combines. Off by default: slower than single tiles at the
  * one-request fused shape on B200 (tools/attn_bench.py). */
-size_t qcf_attention_workspace(int64_t m, int n_req, int h);   /* 0 when no split applies */
-int qcf_attention_split(int64_t m, int n_req, int h);          /* the split-KV factor (1 = none) */
+size_t qcf_attention_workspace(int64_t m, int n_req, int h, int64_t n_keys);  /* 0: no split applies */
+int qcf_attention_split(int64_t m, int n_req, int h, int64_t n_keys);         /* split-KV factor (1 = none) */
 int qcf_set_attention_split(int n_split);                       /* 0 = off (default), 2..16 */
 int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void* v,
                              const int32_t* kmax, int64_t m, int n_req, int h, int hkv, int d,

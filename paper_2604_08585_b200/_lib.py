@@ -63,8 +63,8 @@ SIGNATURES: dict[str, tuple] = {
                                _SZ, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_attention_batched": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P]),
-    "qcf_attention_workspace": (_SZ, [_I64, _I, _I]),
-    "qcf_attention_split": (_I, [_I64, _I, _I]),
+    "qcf_attention_workspace": (_SZ, [_I64, _I, _I, _I64]),
+    "qcf_attention_split": (_I, [_I64, _I, _I, _I64]),
     "qcf_attention_batched_ws": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P, _SZ, _P]),
     "qcf_set_attention_kernel": (_I, [_I]),
     "qcf_set_attention_split": (_I, [_I]),
@@ -169,7 +169,7 @@ def _kernels_per_call(name: str, args: tuple) -> int:
         return 3 * ((n_rows + chunk - 1) // chunk)
     if name == "qcf_attention_batched_ws" and args[12] and args[0] == QCF_BF16:
         # split-KV adds the combine kernel
-        return 2 if lib.qcf_attention_split(args[5], args[6], args[7]) > 1 else 1
+        return 2 if lib.qcf_attention_split(args[5], args[6], args[7], args[10]) > 1 else 1
     if name == "qcf_score_batched":
         # tensor-core path: 3 kernels for the whole batch; SIMT path: 3 per request
         dtype, n_req, precise = args[0], args[6], args[12]

@@ -986,7 +986,7 @@ static int g_attn_nsplit = -1;  // QCF_ATTN_SPLIT env / qcf_set_attention_split:
 void set_attention_split(int n) { g_attn_nsplit = n > 0 ? n : 0; }
 
 // split-KV factor for a one-wave grid: ~2 waves of CTAs, at most 8 chunks
-int attention_auto_split(int64_t m, int n_req, int h) {
+int attention_auto_split(int64_t m, int n_req, int h, int64_t n_keys) {
   if (g_attn_nsplit < 0) {
     const char* e = getenv("QCF_ATTN_SPLIT");
     g_attn_nsplit = e ? std::max(1, atoi(e)) : 0;
@@ -1003,7 +1003,9 @@ int attention_auto_split(int64_t m, int n_req, int h) {
   // tiles over a long key range); at the one-request recompute shape (128 pairs)
   // single tiles measured faster (tools/attn_bench.py)
   if (grid * 4 > sms) return 1;
-  return (int)std::min<int64_t>(8, std::max<int64_t>(2, (2 * sms + grid - 1) / grid));
+  const int64_t sp = std::min<int64_t>(8, std::max<int64_t>(2, (2 * sms + grid - 1) / grid));
+  // at least two key tiles per chunk (the probe's short anchor prefix stays whole)
+  return (int)std::min<int64_t>(sp, std::max<int64_t>(1, (n_keys + 2 * AT_BN - 1) / (2 * AT_BN)));
 }
 
 int attention_tc_launch(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m, int h,
@@ -1039,9 +1041,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   // QCF_ATTN_SPLIT) or runs single tiles (default: measured faster on B200)
   int n_split = 1;
   if (g_attn_ver == 0 && g_attn_split == 2 && ws) {
-    n_split = attention_auto_split(m, n_req, h);
-    // at least two key tiles per chunk (the probe's short anchor prefix stays whole)
-    n_split = (int)std::min<int64_t>(n_split, std::max<int64_t>(1, (n_keys + 2 * AT_BN - 1) / (2 * AT_BN)));
+    n_split = attention_auto_split(m, n_req, h, n_keys);
     if (n_split > 1 && ws_bytes < attention_workspace(m, n_req, h, n_split)) n_split = 1;
   }
   const int64_t grid_pairs = (int64_t)h * n_pairs * n_req;

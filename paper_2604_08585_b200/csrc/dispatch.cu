@@ -44,10 +44,12 @@ extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, in
   return qcf::gemm_simt_launch(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
 }
 
-extern "C" int qcf_attention_split(int64_t m, int n_req, int h) { return qcf::attention_auto_split(m, n_req, h); }
+extern "C" int qcf_attention_split(int64_t m, int n_req, int h, int64_t n_keys) {
+  return qcf::attention_auto_split(m, n_req, h, n_keys);
+}
 
-extern "C" size_t qcf_attention_workspace(int64_t m, int n_req, int h) {
-  return qcf::attention_workspace(m, n_req, h, qcf::attention_auto_split(m, n_req, h));
+extern "C" size_t qcf_attention_workspace(int64_t m, int n_req, int h, int64_t n_keys) {
+  return qcf::attention_workspace(m, n_req, h, qcf::attention_auto_split(m, n_req, h, n_keys));
 }
 
 extern "C" int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void* v,

@@ -77,17 +77,17 @@ class Executor:
             self._scratch[k] = s
         return s
 
-    def _attn_ws(self, m_per_req: int, n_req: int) -> torch.Tensor | None:
-        """Split-KV workspace of the attention (only when the grid is one wave)."""
+    def _attn_ws(self, m_per_req: int, n_req: int, n_keys: int) -> torch.Tensor | None:
+        """Split-KV workspace of the attention (only for grids far below one wave)."""
         if self.w.dtype != "bf16":
             return None
-        n = int(_lib.lib.qcf_attention_workspace(m_per_req, n_req, self.cfg.n_heads))
+        n = int(_lib.lib.qcf_attention_workspace(m_per_req, n_req, self.cfg.n_heads, n_keys))
         if n == 0:
             return None
-        t = self._aws.get((m_per_req, n_req))
+        t = self._aws.get((m_per_req, n_req, n_keys))
         if t is None:
             t = torch.empty(n, dtype=torch.uint8, device=self.w.device)
-            self._aws[(m_per_req, n_req)] = t
+            self._aws[(m_per_req, n_req, n_keys)] = t
         return t
 
     # ------------------------------------------------------------------
@@ -150,7 +150,7 @@ class Executor:
                  qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), dt, s)
         if q_only:
             return
-        aws = self._attn_ws(m // n_req, n_req)
+        aws = self._attn_ws(m // n_req, n_req, tab_k.shape[0] // n_req)
         call("qcf_attention_batched_ws", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
              kmax.data_ptr(), m // n_req, n_req, H, Hkv, D, tab_k.shape[0] // n_req, sc.o.data_ptr(),
              aws.data_ptr() if aws is not None else None, aws.numel() if aws is not None else 0, s)

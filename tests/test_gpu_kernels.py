@@ -450,7 +450,7 @@ def test_attention_tc_batched_gqa_versions(L, version, m, n, H, Hkv, n_req, sort
     L.call("qcf_set_attention_split", 3 if version == "split3" else 0)
     try:
         if isinstance(version, str):   # split3: one-wave grids -> tile pairs with split-KV + combine
-            nb = int(L.lib.qcf_attention_workspace(m, n_req, H))
+            nb = int(L.lib.qcf_attention_workspace(m, n_req, H, n))
             ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
             L.call("qcf_attention_batched_ws", L.QCF_BF16, p(q), p(k), p(v), p(kmax), m, n_req, H, Hkv, D, n, p(out),
                    p(ws), nb, S())

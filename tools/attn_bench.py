@@ -20,9 +20,9 @@ def bench(m, n_keys, H, Hkv, n_req, kmax, it=20):
     out = torch.empty_like(q)
     flops = 4.0 * H * D * float((kmax.long() + 1).sum())
     res = {}
-    nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H))
+    nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H, n_keys))
     ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
-    res["auto_split"] = int(_lib.lib.qcf_attention_split(m, n_req, H))
+    res["auto_split"] = int(_lib.lib.qcf_attention_split(m, n_req, H, n_keys))
     for ver in (1, 2, 3, 0):   # 0 = auto with workspace (split-KV for one-wave grids)
         _lib.call("qcf_set_attention_kernel", ver)
         f = lambda: _lib.call("qcf_attention_batched_ws", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(),

@@ -16,7 +16,7 @@ q = torch.randn(n_req, m, H, D, device="cuda").bfloat16()
 k = torch.randn(n_req, n_keys, H, D, device="cuda").bfloat16()
 v = torch.randn(n_req, n_keys, H, D, device="cuda").bfloat16()
 out = torch.empty_like(q)
-nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H))
+nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H, n_keys))
 ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
 _lib.call("qcf_set_attention_kernel", ver)
 S = torch.cuda.current_stream().cuda_stream
