@@ -602,3 +602,32 @@ def test_engine_is_reentrant_across_threads(tmp_path):
         t.join()
     for (l1, s1), (l2, s2) in zip(ref, got):
         assert np.array_equal(s1, s2) and np.array_equal(l1, l2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_long_context_16k_against_oracle(tmp_path, dtype):
+    """16 chunks x 1024 tokens (16k context, RoPE table growth, 129 key tiles,
+    16k-key Top-N and scoring) through the fast path vs the oracle. f32: the
+    selection is bit-exact and logits within 1e-4; bf16: overlap >= 0.9 and
+    relative logit error < 5e-2."""
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    oc = O.Config(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=31)
+    ow = O.init_weights(oc)
+    rng = np.random.default_rng(16)
+    chunks = [O.precompute_chunk(ow, rng.integers(0, 256, 1024), 0.05) for _ in range(16)]
+    query = rng.integers(0, 256, 24).tolist()
+    ref = O.run(ow, chunks, query, 0.15)
+    w = device_weights(ow, dtype)
+    store = Q.ChunkStore(tmp_path / "s", w.config, dtype=dtype, persist=False)
+    ids = load_oracle_chunks(store, chunks)
+    eng = Q.FusionEngine(w, store)
+    logits, sel = eng.fuse(query, ids, 0.15)
+    if dtype == "f32":
+        assert np.array_equal(sel, ref.selection)
+        assert np.abs(logits - ref.first_logits).max() < 1e-4
+    else:
+        overlap = len(set(sel.tolist()) & set(ref.selection.tolist())) / len(sel)
+        err = np.abs(logits - ref.first_logits).max() / np.abs(ref.first_logits).max()
+        print(f"16k bf16: overlap {overlap:.3f} rel logit err {err:.3e}")
+        assert overlap >= 0.9 and err < 5e-2
