@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
     }
     __syncthreads();
     if (tid < 32) {  // warp 0: find the digit holding the need-th largest key
-      int need = s_need;
+      const int need = s_need;
+      __syncwarp();    // every lane has read s_need before the owning lane rewrites it
       // suffix sums over the 256 bins, 8 per lane, highest bins in lane 31
       int cnt[8], tot = 0;
 #pragma unroll
