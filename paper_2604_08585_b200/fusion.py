@@ -408,6 +408,8 @@ class _Bufs:
         self.sc_probe = eng.ex.scratch(B * q, key=("probe", id(self)))
         self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
+        self.h_staged: list[torch.Tensor] | None = None   # pinned host mirrors of staged()
+        self.h_done: torch.cuda.Event | None = None
 
     def staged(self) -> list[torch.Tensor]:
         """The device tensors a batch's host inputs are staged into (swapped
@@ -787,14 +789,21 @@ class FusionEngine:
         rows = np.concatenate(rows)
         adesc = torch.cat(adescs)
         adelta = np.concatenate(adeltas)
+        host = [desc, torch.from_numpy(tok), torch.from_numpy(rows), adesc, torch.from_numpy(adelta)]
+        dev = [b.desc, b.tok, b.anchor_rows[:rows.size], b.adesc, b.adelta]
+        if b.h_staged is None:   # persistent pinned staging buffers (no per-call pinned allocation)
+            b.h_staged = [torch.empty(t.numel() * t.element_size(), dtype=torch.uint8, pin_memory=True)
+                          for t in host]
+            b.h_done = torch.cuda.Event()
+        b.h_done.synchronize()   # the previous batch's H2D copies out of these buffers have finished
         s = stream or torch.cuda.current_stream()
         with torch.cuda.stream(s):
-            b.adesc.copy_(adesc.pin_memory(), non_blocking=True)
-            b.adelta.copy_(torch.from_numpy(adelta).pin_memory(), non_blocking=True)
-            b.desc.copy_(desc.pin_memory(), non_blocking=True)
-            b.tok.copy_(torch.from_numpy(tok).pin_memory(), non_blocking=True)
-            b.anchor_rows[:rows.size].copy_(torch.from_numpy(rows).pin_memory(), non_blocking=True)
-        return {"h2d": desc.numel() + tok.nbytes + rows.nbytes + adesc.numel() + adelta.nbytes}
+            for h, pinned, d in zip(host, b.h_staged, dev):
+                view = pinned.view(h.dtype)[:h.numel()]
+                view.copy_(h.reshape(-1))
+                d.copy_(view, non_blocking=True)
+            b.h_done.record(s)
+        return {"h2d": sum(h.numel() * h.element_size() for h in host)}
 
     def _launch(self, plans: list[_Plan], b: _Bufs, stream=None) -> None:
         """Every kernel of one (batched) fused prefill, in order (module docstring)."""
