@@ -144,8 +144,10 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16
 __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
-               int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out) {
+               int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int rshift) {
   // request (batch) index: q/out/kmax are [req][M]..., the K/V tables [req][n_keys]...
+  // rshift: query tiles start at row t*128 - rshift (virtual rows < 0 are masked), so
+  // the partial tile is the FIRST one (fewest keys), not the last (longest key range)
   const int req = blockIdx.z;
   kmax += (int64_t)req * M;
   out += (int64_t)req * M * H * AT_D;
@@ -173,7 +175,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   const int qt = n_qt - 1 - blockIdx.y;  // longest tiles (largest positions) launch first
   const int head = blockIdx.x;
   const int kvh = head / (H / Hkv);
-  const int m0 = qt * AT_BM;
+  const int m0 = qt * AT_BM - rshift;
   constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
 
   if (threadIdx.x == 0) {
@@ -201,7 +203,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   // key range of this tile = 1 + max kmax over its rows (rows are normally
   // sorted by position, but the kernel does not rely on it)
   if (threadIdx.x < AT_BM) {
-    int v = (m0 + (int)threadIdx.x < M) ? kmax[m0 + threadIdx.x] : 0;
+    const int rr = m0 + (int)threadIdx.x;
+    int v = (rr >= 0 && rr < M) ? kmax[rr] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
     if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
@@ -284,7 +287,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     const int cg = (warp - 2) >> 2;       // column group: S keys / O dims 32cg..32cg+31
     const int r = g * 32 + lane;          // row within the tile == TMEM lane
     const int row = m0 + r;
-    const int my_kmax = row < M ? kmax[row] : -1;
+    const int my_kmax = (row >= 0 && row < M) ? kmax[row] : -1;
     const uint32_t lane_off = (uint32_t)(g * 32) << 16;
     const int bar_id = 1 + g;             // named barrier of the 4 warps sharing these rows
     float m_ref = -INFINITY, l = 0.f;
@@ -401,7 +404,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     uint32_t o[32];
     tmem_ld32(tO + cg * 32 + lane_off, o);
     tmem_ld_wait();
-    if (row < M) {
+    if (row >= 0 && row < M) {
       __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cg * 32;
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(A2Cfg<SPLIT>::THREADS, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
                 int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int mirrored,
-                int n_split, float* __restrict__ ws_o, float2* __restrict__ ws_ml) {
+                int n_split, float* __restrict__ ws_o, float2* __restrict__ ws_ml, int rshift) {
   // split-KV (n_split > 1, one-wave grids): CTA (pair, chunk) covers key tiles
   // [chunk*n/n_split, (chunk+1)*n/n_split) of the pair's range and leaves an
   // unnormalised fp32 O + (max, sum) per row for attn_combine_kernel
@@ -527,8 +530,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
     const int tl = t ? tile1 : tile0;
     int v = 0;
     if (tl >= 0) {
-      const int row = tl * AT_BM + (threadIdx.x % AT_BM);
-      v = row < M ? kmax[row] + 1 : 0;
+      const int row = tl * AT_BM - rshift + (threadIdx.x % AT_BM);
+      v = (row >= 0 && row < M) ? kmax[row] + 1 : 0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -552,8 +555,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
       for (int t = 0; t < 2; ++t) {
         const int n_t = t ? nt1 : nt0, tl = t ? tile1 : tile0;
         if (n_t == 0) continue;
-        tma_load_3d(sQ + t * AT_TILE_BYTES, &map_q, q_full, head * AT_D, tl * AT_BM, req);
-        tma_load_3d(sQ + t * AT_TILE_BYTES + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, tl * AT_BM, req);
+        tma_load_3d(sQ + t * AT_TILE_BYTES, &map_q, q_full, head * AT_D, tl * AT_BM - rshift, req);
+        tma_load_3d(sQ + t * AT_TILE_BYTES + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64,
+                    tl * AT_BM - rshift, req);
       }
       auto load_k = [&](int j) {
         const int st = j & 1;
@@ -636,8 +640,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
     const int r = g * 32 + lane;
     const int n_my = t ? nt1 : nt0;
     const int my_tile = t ? tile1 : tile0;
-    const int row = my_tile * AT_BM + r;
-    const int my_kmax = (my_tile >= 0 && row < M) ? kmax[row] : -1;
+    const int row = my_tile * AT_BM - rshift + r;
+    const int my_kmax = (my_tile >= 0 && row >= 0 && row < M) ? kmax[row] : -1;
     const uint32_t lane_off = (uint32_t)(g * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
     const uint32_t tO = tmem + 256 + t * 128 + lane_off;
@@ -764,8 +768,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
     const int r = g * 32 + lane;
     const int n_my = t ? nt1 : nt0;
     const int my_tile = t ? tile1 : tile0;
-    const int row = my_tile * AT_BM + r;
-    const int my_kmax = (my_tile >= 0 && row < M) ? kmax[row] : -1;
+    const int row = my_tile * AT_BM - rshift + r;
+    const int my_kmax = (my_tile >= 0 && row >= 0 && row < M) ? kmax[row] : -1;
     const uint32_t lane_off = (uint32_t)(g * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
     const uint32_t tO = tmem + 256 + t * 128 + lane_off;
@@ -937,7 +941,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
 // (row, head), 4 output dims per lane.
 __global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restrict__ ws_o,
                                                            const float2* __restrict__ ws_ml, int M, int H,
-                                                           int n_split, __nv_bfloat16* __restrict__ out) {
+                                                           int n_split, __nv_bfloat16* __restrict__ out,
+                                                           int rshift) {
   pdl_wait();
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -945,7 +950,7 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const float* __restri
   const int row = blockIdx.y, req = blockIdx.z;
   if (head >= H) return;
   const int n_qt = (M + AT_BM - 1) / AT_BM;
-  const int tile = row / AT_BM, r = row % AT_BM;
+  const int tile = (row + rshift) / AT_BM, r = (row + rshift) % AT_BM;
   const int64_t base0 = (((int64_t)req * H + head) * n_qt + tile) * n_split;
   float mx = -INFINITY;
   for (int c = 0; c < n_split; ++c) mx = fmaxf(mx, ws_ml[(base0 + c) * AT_BM + r].x);
@@ -1036,6 +1041,9 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)d);
   const int n_qt = (int)((m + AT_BM - 1) / AT_BM);
   const int n_pairs = (n_qt + 1) / 2;
+  // the partial query tile goes FIRST (rows sorted by position -> it is the one
+  // with the fewest keys); the query rows at the end then fill a whole tile
+  const int rshift = (int)((AT_BM - m % AT_BM) % AT_BM);
   // auto: tile pairs when they span more than one wave; a one-wave grid either
   // splits every pair's key range (split-KV + combine; needs the workspace and
   // QCF_ATTN_SPLIT) or runs single tiles (default: measured faster on B200)
@@ -1063,20 +1071,22 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
     dim3 grid((unsigned)h, (unsigned)(n_pairs * n_split), (unsigned)n_req);
     if (g_attn_split == 2)
       QCF_LAUNCH("attn_tc2_kernel<2>", attn_tc2_kernel<2>, dim3(grid), dim3(A2Cfg<2>::THREADS), A2_SMEM, s, mq, mk, mv,
-                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, pair_mode, n_split, ws_o, ws_ml);
+                 kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, pair_mode, n_split, ws_o, ws_ml,
+                 rshift);
     else
       QCF_LAUNCH("attn_tc2_kernel<1>", attn_tc2_kernel<1>, dim3(grid), dim3(A2Cfg<1>::THREADS), A2_SMEM, s, mq, mk, mv,
                  kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, pair_mode, 1,
-                 (float*)nullptr, (float2*)nullptr);
+                 (float*)nullptr, (float2*)nullptr, rshift);
     QCF_LAUNCH_CHECK("qcf_attention(tcgen05 pairs)");
     if (n_split > 1) {
       QCF_LAUNCH("attn_combine_kernel", attn_combine_kernel, dim3((unsigned)((h + 3) / 4), (unsigned)m, (unsigned)n_req),
-                 dim3(128), 0, s, (const float*)ws_o, (const float2*)ws_ml, (int)m, h, n_split, (__nv_bfloat16*)out);
+                 dim3(128), 0, s, (const float*)ws_o, (const float2*)ws_ml, (int)m, h, n_split, (__nv_bfloat16*)out,
+                 rshift);
     }
   } else {
     dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
     QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m,
-               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out);
+               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, rshift);
   }
   QCF_LAUNCH_CHECK("qcf_attention(tcgen05)");
   return QCF_OK;
