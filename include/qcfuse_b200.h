@@ -162,10 +162,12 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
  * M <= 32 (the probe's query rows) with a workspace (qcf_gemm_workspace, zeroed):
  * split-K weight streaming, the rotation + scatter applied in the split-K
  * reduction. Returns QCF_EUNSUPPORTED when d % 32 != 0 (callers then use
- * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478. */
+ * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478.
+ * cs_tbl: float32 [n_pos][d/2][2] = (float(cos), float(sin)) of the float64
+ * angle table (the bf16 epilogue rotates in fp32; 16-byte aligned). */
 int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m, int64_t k,
                       int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
-                      const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
+                      const float* cs_tbl, int64_t n_pos, void* q_out,
                       void* k_tab, void* v_tab, void* ws, size_t ws_bytes, qcf_stream_t stream);
 
 /* ---- location-aware attention: fusion.py:194-208 -> model.py:326-338 -------

@@ -111,16 +111,16 @@ extern "C" int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b,
 
 extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, int b_layout, int64_t m,
                                  int64_t k, int h, int hkv, int d, const int32_t* pos, const int32_t* dst_rows,
-                                 const double* cos_tbl, const double* sin_tbl, int64_t n_pos, void* q_out,
+                                 const float* cs_tbl, int64_t n_pos, void* q_out,
                                  void* k_tab, void* v_tab, void* ws, size_t ws_bytes, qcf_stream_t stream) {
   (void)n_pos;
-  QCF_REQUIRE(a && w && pos && dst_rows && cos_tbl && sin_tbl && q_out && k_tab && v_tab, QCF_EINVAL,
+  QCF_REQUIRE(a && w && pos && dst_rows && cs_tbl && q_out && k_tab && v_tab, QCF_EINVAL,
               "qcf_gemm_qkv_rope: null pointer");
   QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && d > 0 && d % 2 == 0 && k > 0 && m >= 0, QCF_EINVAL,
               "qcf_gemm_qkv_rope: bad shape");
   if (m == 0) return QCF_OK;
   QCF_REQUIRE(qcf::tc_ok(), QCF_EUNSUPPORTED, "qcf_gemm_qkv_rope: needs an sm_100 device");
-  const int st = qcf::gemm_qkv_rope_launch(a, lda, w, ldb, m, k, h, hkv, d, pos, dst_rows, cos_tbl, sin_tbl,
+  const int st = qcf::gemm_qkv_rope_launch(a, lda, w, ldb, m, k, h, hkv, d, pos, dst_rows, cs_tbl,
                                            q_out, k_tab, v_tab, qcf::as_stream(stream), b_layout, ws, ws_bytes);
   if (st == QCF_EUNSUPPORTED) qcf::set_error("qcf_gemm_qkv_rope: shape not covered (d %% 32, alignment)");
   return st;

@@ -40,8 +40,8 @@ int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void*
 
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k);
 int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k, int h,
-                         int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
-                         const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
+                         int hkv, int d, const int32_t* pos, const int32_t* dst, const float* cs_tbl,
+                         void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
                          int b_layout, void* ws, size_t ws_bytes);
 int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                    int64_t n, int64_t k, int epilogue, int out_dtype, int b_layout, void* ws, size_t ws_bytes,

@@ -42,8 +42,7 @@ struct EpiArgs {
   int b_tiled;  // B stored tile-major (64x64 tiles, 8 KB contiguous) -> 4D TMA boxes
   const int32_t* pos;
   const int32_t* dst;
-  const double* cos_tbl;
-  const double* sin_tbl;
+  const float* cs_tbl;  // RoPE (cos, sin) pairs, float32 [n_pos][d/2][2]
   void* q_out;
   void* k_tab;
   void* v_tab;
@@ -77,12 +76,19 @@ __device__ __forceinline__ void epilogue_row32(void* __restrict__ C, int64_t ldc
     }
     const int half = ea.d >> 1;
     const int64_t t0 = (int64_t)ea.pos[row] * half + ((base % ea.d) >> 1);
+    // 16 (cos, sin) pairs = 128 contiguous bytes: 8 vector loads, all issued up front
+    float4 cs[8];
+    if (rot) {
+      const float4* src = reinterpret_cast<const float4*>(ea.cs_tbl + 2 * t0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cs[i] = __ldg(src + i);
+    }
     uint32_t pk[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       float e = __uint_as_float(r[2 * i]), o = __uint_as_float(r[2 * i + 1]);
       if (rot) {
-        const float c = (float)ea.cos_tbl[t0 + i], sn = (float)ea.sin_tbl[t0 + i];
+        const float c = (i & 1) ? cs[i >> 1].z : cs[i >> 1].x, sn = (i & 1) ? cs[i >> 1].w : cs[i >> 1].y;
         const float oe = e * c - o * sn, oo = e * sn + o * c;
         e = oe;
         o = oo;
@@ -607,8 +613,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
       }
       if (rot) {
         const int64_t t0 = (int64_t)ea.pos[row] * (ea.d >> 1) + ((base % ea.d) >> 1);
-        const float c0 = (float)ea.cos_tbl[t0], s0 = (float)ea.sin_tbl[t0];
-        const float c1 = (float)ea.cos_tbl[t0 + 1], s1 = (float)ea.sin_tbl[t0 + 1];
+        const float4 cs = __ldg(reinterpret_cast<const float4*>(ea.cs_tbl + 2 * t0));
+        const float c0 = cs.x, s0 = cs.y, c1 = cs.z, s1 = cs.w;
         const float x = acc.x * c0 - acc.y * s0, y = acc.x * s0 + acc.y * c0;
         const float z = acc.z * c1 - acc.w * s1, w = acc.z * s1 + acc.w * c1;
         acc = make_float4(x, y, z, w);
@@ -897,12 +903,12 @@ int gemm_tc_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void*
 }
 
 int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb, int64_t m, int64_t k, int h,
-                         int hkv, int d, const int32_t* pos, const int32_t* dst, const double* cos_tbl,
-                         const double* sin_tbl, void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
+                         int hkv, int d, const int32_t* pos, const int32_t* dst, const float* cs_tbl,
+                         void* q_out, void* k_tab, void* v_tab, cudaStream_t s,
                          int b_layout, void* ws, size_t ws_bytes) {
   if (d % 32) return QCF_EUNSUPPORTED;  // 32-column epilogue chunks must stay inside a head
-  if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab) & 15) return QCF_EUNSUPPORTED;
-  EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cos_tbl, sin_tbl, q_out, k_tab, v_tab, h, hkv, d};
+  if (((uintptr_t)q_out | (uintptr_t)k_tab | (uintptr_t)v_tab | (uintptr_t)cs_tbl) & 15) return QCF_EUNSUPPORTED;
+  EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cs_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
   if (m <= 32 && ws) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction

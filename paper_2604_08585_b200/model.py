@@ -282,7 +282,7 @@ class RopeTable:
     def __init__(self, d_head: int, theta: float, device, n_pos: int = 8192):
         self.d_head, self.theta, self.device = d_head, theta, torch.device(device)
         self.n_pos = 0
-        self.cos = self.sin = None
+        self.cos = self.sin = self.cs32 = None
         self.ensure(n_pos)
 
     def ensure(self, n_pos: int) -> None:
@@ -294,4 +294,7 @@ class RopeTable:
         ang = np.arange(n, dtype=np.float64)[:, None] * inv[None, :]
         self.cos = torch.as_tensor(np.cos(ang)).to(self.device)
         self.sin = torch.as_tensor(np.sin(ang)).to(self.device)
+        # (cos, sin) pairs in float32 for the bf16 tcgen05 QKV epilogue (which
+        # rotates in fp32: same values as casting the float64 tables there)
+        self.cs32 = torch.stack([self.cos, self.sin], -1).float().contiguous()
         self.n_pos = n

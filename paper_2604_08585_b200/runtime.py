@@ -141,7 +141,7 @@ class Executor:
             # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue (M <= 32:
             # split-K weight streaming with the rotation applied in the split-K reduction)
             call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, self.w.b_layout, m, d, H, Hkv, D,
-                 pos.data_ptr(), dst.data_ptr(), self.rope.cos.data_ptr(), self.rope.sin.data_ptr(),
+                 pos.data_ptr(), dst.data_ptr(), self.rope.cs32.data_ptr(),
                  self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), sc.ws.data_ptr(), sc.ws.numel(), s)
         else:
             self.gemm(sc, sc.a, d, lw.wqkv, d, sc.qkv, nq, m, nq, d, EPI_STORE, QCF_F32, s)

@@ -310,7 +310,7 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads, kdim):
     v1 = torch.zeros_like(k1)
     ws = torch.zeros(int(L.lib.qcf_gemm_workspace(m, N, K)), dtype=torch.uint8, device="cuda")
     # M <= 32 with a workspace: split-K streaming + RoPE in the reduction (or the 1-CTA fallback)
-    L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos), p(rope.sin),
+    L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cs32),
            rope.n_pos, p(q1), p(k1), p(v1), p(ws), ws.numel(), S())
     qkv = torch.empty(m, N, device="cuda")
     L.call("qcf_gemm", L.QCF_BF16, p(a), K, p(w), K, p(qkv), N, m, N, K, 0, L.QCF_F32, S())
@@ -558,8 +558,8 @@ def test_fused_qkv_rope_pair_128_rows(L):
             q = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
             kt = torch.zeros(m + 7, heads, D, device="cuda", dtype=torch.bfloat16)
             vt = torch.zeros_like(kt)
-            L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cos),
-                   p(rope.sin), rope.n_pos, p(q), p(kt), p(vt), None, 0, S())
+            L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, heads, D, p(pos), p(dst), p(rope.cs32),
+                   rope.n_pos, p(q), p(kt), p(vt), None, 0, S())
             res.append((q, kt, vt))
         torch.cuda.synchronize()
     finally:

@@ -22,7 +22,7 @@ if epi == 9:  # fused QKV + RoPE + KV scatter (n = 3*H*D)
     wsq = torch.zeros(int(_lib.lib.qcf_gemm_workspace(m, n, k)), dtype=torch.uint8, device="cuda")
     for _ in range(4):
         _lib.call("qcf_gemm_qkv_rope", a.data_ptr(), k, w.data_ptr(), k, LAY, m, k, H, H, D, pos.data_ptr(), pos.data_ptr(),
-                  rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, q.data_ptr(), kt.data_ptr(), vt.data_ptr(), wsq.data_ptr(), wsq.numel(), s)
+                  rope.cs32.data_ptr(), rope.n_pos, q.data_ptr(), kt.data_ptr(), vt.data_ptr(), wsq.data_ptr(), wsq.numel(), s)
     torch.cuda.synchronize()
     sys.exit(0)
 a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
