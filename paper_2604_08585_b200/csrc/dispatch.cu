@@ -133,7 +133,7 @@ extern "C" int qcf_set_attention_kernel(int version) {
 }
 
 extern "C" int qcf_set_gemm_plan(int plan) {
-  QCF_REQUIRE((plan & 7) <= 5 && plan >= 0 && plan < 16, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 5, +8 = stream-K on");
+  QCF_REQUIRE(plan >= 0 && plan < 16, QCF_EINVAL, "qcf_set_gemm_plan: 0 (auto) .. 7, +8 = stream-K on");
   qcf::set_gemm_plan(plan);
   return QCF_OK;
 }

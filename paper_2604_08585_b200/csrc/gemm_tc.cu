@@ -319,7 +319,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 template <int BN, int PM = 256>
 struct Tc2Cfg {
   static constexpr int ROWS = PM / 2;                         // A rows per CTA
-  static constexpr int STAGES = PM == 256 ? 6 : 8;
+  static constexpr int STAGES = (PM == 256 && BN == 256) ? 6 : 8;
   static constexpr int A_BYTES = ROWS * TC_BK * 2;            // this CTA's rows
   static constexpr int B_BYTES = (BN / 2) * TC_BK * 2;        // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -569,6 +569,208 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Swapped 2-CTA GEMM for mid-size M (the single request's ~800 recompute rows):
+// the WEIGHT rows are the MMA's M side (256 per CTA pair, 128 per CTA) and the
+// activation rows its N side, a runtime width BNA (multiple of 16, <= 256) chosen
+// so the activation rows split into near-equal tiles: M = 800 runs as 4 x 208
+// (4% padding) instead of 4 x 256 rows (28%). TMEM lanes = output columns, TMEM
+// columns = activation rows, so the epilogue thread of lane n writes column n
+// of 32 consecutive rows per tcgen05.ld (warp-coalesced along the row).
+// Unit u -> (weight pair u / n_act, activation tile u % n_act): the clusters
+// running one weight pair's activation tiles side by side share it in L2.
+constexpr int SW_STAGES = 6;
+constexpr int SW_A_BYTES = 128 * TC_BK * 2;  // this CTA's 128 weight rows
+constexpr int SW_B_BYTES = 128 * TC_BK * 2;  // up to 128 activation rows (BNA / 2)
+constexpr int SW_STAGE = SW_A_BYTES + SW_B_BYTES;
+constexpr int SW_SMEM = SW_STAGES * SW_STAGE + 1024 + 256;
+
+// out[row][col] for one element of the swapped epilogue (col = this lane's column)
+__device__ __forceinline__ void swap_store(void* __restrict__ C, int64_t ldc, int row, int col, float v,
+                                           const EpiArgs& ea) {
+  if (ea.out_dtype == QCF_F32) {
+    float* p = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
+    if (ea.kind == QCF_EPI_ADD_F32) v += *p;
+    else if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
+    *p = v;
+  } else {
+    if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
+    reinterpret_cast<__nv_bfloat16*>(C)[(int64_t)row * ldc + col] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                 void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int bna, int n_act) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                // weights [stage]
+  uint8_t* sB = smem + SW_STAGES * SW_A_BYTES;       // activations [stage]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SW_STAGES * SW_STAGE);
+  uint64_t* empty = full + SW_STAGES;
+  uint64_t* tfull = empty + SW_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2] (leader's copy is the one used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int n_wp = (N + 255) / 256;
+  const int n_units = n_wp * n_act;
+  const int k_blocks = (K + TC_BK - 1) / TC_BK;
+  const int xrows = bna >> 1;  // activation rows per CTA
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&map_x);
+    for (int s = 0; s < SW_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * 128); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t stage_tx = 2 * (SW_A_BYTES + (uint32_t)xrows * 128);
+      uint32_t it = 0;
+      for (int u = cluster; u < n_units; u += n_clusters) {
+        const int wrow = (u / n_act) * 256 + rank * 128;
+        const int xrow = (u % n_act) * bna + rank * xrows;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % SW_STAGES;
+          const uint32_t ph = (it / SW_STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], stage_tx);
+          if (ea.b_tiled)
+            tma_load_4d_pair(sA + s * SW_A_BYTES, &map_w, &full[s], 0, 0, kb, wrow / 64);
+          else
+            tma_load_2d_pair(sA + s * SW_A_BYTES, &map_w, &full[s], kb * TC_BK, wrow);
+          tma_load_2d_pair(sB + s * SW_B_BYTES, &map_x, &full[s], kb * TC_BK, xrow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+      const uint32_t idesc = idesc_bf16_f32(256, bna);
+      uint32_t it = 0, t = 0;
+      for (int u = cluster; u < n_units; u += n_clusters, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % SW_STAGES;
+          const uint32_t ph = (it / SW_STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_k_sw128(sA + s * SW_A_BYTES);
+          const uint64_t b0 = umma_desc_k_sw128(sB + s * SW_B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk)
+            mma_bf16_pair(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) ? 1u : 0u);
+          mma_commit_pair(&empty[s]);
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5: lane = output column
+    const int g = warp & 3;
+    const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
+    const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    const bool rope = ea.kind == QCF_EPI_ROPE_QKV;
+    const int qd = ea.h * ea.d, kd = ea.hkv * ea.d, half = ea.d >> 1;
+    uint32_t t = 0;
+    for (int u = cluster; u < n_units; u += n_clusters, ++t) {
+      const int acc = t & 1;
+      const int col = (u / n_act) * 256 + rank * 128 + g * 32 + lane;
+      const int row0 = (u % n_act) * bna;
+      const int rows = min(bna, M - row0);
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      // RoPE: columns [Q | K | V]; this warp's 32 columns lie inside one head
+      int region = 0;  // 0 Q, 1 K, 2 V
+      int base = col;
+      if (rope) {
+        if (col >= qd + kd) { region = 2; base = col - qd - kd; }
+        else if (col >= qd) { region = 1; base = col - qd; }
+      }
+      const int jp = (base % (ea.d > 0 ? ea.d : 1)) >> 1;
+      const bool odd = lane & 1;
+#pragma unroll 1
+      for (int c0 = 0; c0 < rows; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + acc * 256 + c0 + ((uint32_t)(g * 32) << 16), r);
+        tmem_ld_wait();
+        const int nr = min(32, rows - c0);
+        // lane L holds row (row0 + c0 + L)'s metadata; rows are then broadcast by
+        // shuffles, and every batch of 8 rows issues all its loads before its stores
+        // (a store may alias the tables, so the compiler cannot hoist loads itself)
+        const int myrow = row0 + c0 + lane;
+        if (!rope) {
+          if (ea.kind == QCF_EPI_ADD_F32 && ea.out_dtype == QCF_F32) {
+            float* cp = reinterpret_cast<float*>(C) + (int64_t)(row0 + c0) * ldc + col;
+#pragma unroll
+            for (int jb = 0; jb < 32; jb += 8) {
+              float o[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o[e] = (col < N && jb + e < nr) ? cp[(int64_t)(jb + e) * ldc] : 0.f;
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (col < N && jb + e < nr) cp[(int64_t)(jb + e) * ldc] = o[e] + __uint_as_float(r[jb + e]);
+            }
+          } else if (col < N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nr) swap_store(C, ldc, row0 + c0 + j, col, __uint_as_float(r[j]), ea);
+          }
+        } else {
+          const int mpos = lane < nr ? ea.pos[myrow] : 0;
+          const int mdst = (region != 0 && lane < nr) ? ea.dst[myrow] : 0;
+          const float2* cst = reinterpret_cast<const float2*>(ea.cs_tbl) + jp;
+          __nv_bfloat16* tab = reinterpret_cast<__nv_bfloat16*>(region == 1 ? ea.k_tab : ea.v_tab) + base;
+          __nv_bfloat16* qo = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)(row0 + c0) * qd + base;
+          // all 32 rows' (cos, sin) loads in flight at once: one L2 round trip per chunk
+          float2 cs[32];
+          if (region != 2) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) cs[e] = __ldg(cst + (int64_t)__shfl_sync(0xffffffffu, mpos, e) * half);
+          }
+#pragma unroll
+          for (int jb = 0; jb < 32; jb += 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int j = jb + e;
+              float v = __uint_as_float(r[j]);
+              const float p = __shfl_xor_sync(0xffffffffu, v, 1);
+              const int drow = __shfl_sync(0xffffffffu, mdst, j);
+              // pair (e, o) = (even column, odd column): e' = e c - o s, o' = e s + o c
+              if (region != 2) v = odd ? (p * cs[j].y + v * cs[j].x) : (v * cs[j].x - p * cs[j].y);
+              if (j < nr && col < N) {
+                __nv_bfloat16* out = region == 0 ? qo + (int64_t)j * qd : tab + (int64_t)drow * kd;
+                *out = __float2bfloat16_rn(v);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, 512);
   }
 }
 
@@ -828,13 +1030,76 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   return QCF_OK;
 }
 
+// swapped 2-CTA kernel: activation tile width (multiple of 16, <= 256) and count
+// minimising waves x (width + per-unit overhead); returns that cost in the same
+// units as the normal 256 x 256 pair schedule (pair_cost)
+// (tiles narrower than 128 activation rows stream too many weight bytes per flop:
+// at M = 256 the 64-wide plan measured slower than 1-CTA 128 x 64 tiles)
+static double swap_plan(int64_t m, int64_t n, int& bna, int& n_act, int min_w = 128) {
+  const int64_t clusters = sm_count() / 2, wp = (n + 255) / 256;
+  double best = 1e30;
+  for (int64_t na = (m + 255) / 256; na <= (m + 255) / 256 + 8; ++na) {
+    const int64_t w = ((m + na - 1) / na + 15) / 16 * 16;
+    if (w > 256 || w < std::min<int64_t>(min_w, (m + 15) / 16 * 16)) continue;
+    const int64_t units = wp * na;
+    const double cost = (double)((units + clusters - 1) / clusters) * (double)(w + 24);
+    if (cost < best - 1e-9) {
+      best = cost;
+      bna = (int)w;
+      n_act = (int)na;
+    }
+  }
+  return best;
+}
+static double pair_cost(int64_t m, int64_t n) {
+  const int64_t clusters = sm_count() / 2, units = ((m + 255) / 256) * ((n + 255) / 256);
+  return (double)((units + clusters - 1) / clusters) * (256.0 + 24.0);
+}
+
+static int launch_swap(const void* a, int64_t lda, const void* w, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                       int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s, int bna, int n_act) {
+  CUtensorMap mw, mx;
+  int st = make_b_map(&mw, w, n, k, ldb, 128, ea.b_tiled);
+  if (st != QCF_OK) return st;
+  st = make_kmajor_map(&mx, a, m, k, lda, bna / 2);
+  if (st != QCF_OK) return st;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SW_SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_tc2s attr");
+    attr_set = true;
+  }
+  const int64_t units = ((n + 255) / 256) * n_act;
+  const int clusters = (int)std::min<int64_t>(units, sm_count() / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = SW_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2s_kernel, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea, bna, n_act);
+  if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 swapped pair)");
+  QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 swapped pair)");
+  return QCF_OK;
+}
+
+static int g_swap_mode = -1;  // QCF_GEMM_SWAP env: 0 off, 1 on (default on)
 static int g_pair_mode = -1;  // QCF_GEMM_PAIR env: 0 off, 1 on (default on)
-static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64, 5 pair-128-rows
+static int g_gemm_plan = 0;   // qcf_set_gemm_plan: 0 auto, 1 pair/256, 2 one/256, 3 one/128, 4 one/64, 5 pair-128-rows,
+                              // 6 pair/128 (256 x 128 tiles, measured slower), 7 swapped pair
 
 void set_gemm_plan(int p) {
   g_streamk = (p & 8) ? 1 : 0;  // +8: stream-K on (measurement)
   p &= 7;
-  g_gemm_plan = (p >= 0 && p <= 5) ? p : 0;
+  g_gemm_plan = (p >= 0 && p <= 7) ? p : 0;
 }
 
 // Skinny-M (probe) plan: BN=64 tiles, split K until ~2 waves of CTAs stream the
@@ -949,7 +1214,32 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
         return launch_pair<256, 128>(ma64, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes);
       }
       break;
+    case 6: if (m >= 192 && n >= 128) return launch_pair<128>(ma, b, ldb, c, ldc, m, n, k, ea, s, ws, ws_bytes); break;
+    case 7:
+      if (n >= 256) {
+        int bna = 0, na = 0;
+        swap_plan(m, n, bna, na, 16);
+        if (bna) return launch_swap(a, lda, b, ldb, c, ldc, m, n, k, ea, s, bna, na);
+      }
+      break;
     default: break;
+  }
+  if (g_swap_mode < 0) {
+    const char* e = getenv("QCF_GEMM_SWAP");
+    g_swap_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  // swapped pairs when the activation rows pad badly into 256-row pairs (M ~ 800:
+  // 4 x 208 vs 4 x 256 rows) or their tiles fill the waves better. Not for the
+  // RoPE epilogue: its per-column rotation (partner column in the neighbouring
+  // lane, one (cos, sin) gather per row) measured 15% slower than the row-per-
+  // thread epilogue at M = 800, and its fp32 rounding of the rotation differs.
+  // The other epilogues are bit-identical to the normal orientation (same MMA
+  // k order, same rounding), so the plan choice never changes a result.
+  if (g_swap_mode && g_pair_mode && ea.kind != QCF_EPI_ROPE_QKV && m >= 64 && n >= 256 && n % 32 == 0) {
+    int bna = 0, na = 0;
+    const double cs = swap_plan(m, n, bna, na);
+    if (bna && cs < 0.97 * pair_cost(m, n) && (n + 255) / 256 * na >= sms / 4)
+      return launch_swap(a, lda, b, ldb, c, ldc, m, n, k, ea, s, bna, na);
   }
   // 2-CTA 256-row tiles vs 1-CTA 128-row tiles: estimate each one's useful
   // fraction (wave quantisation x row padding; 1-CTA pays ~15% for its

@@ -566,3 +566,78 @@ def test_fused_qkv_rope_pair_128_rows(L):
         L.call("qcf_set_gemm_plan", 0)
     for x, y in zip(res[0], res[1]):
         assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
+
+
+@pytest.mark.parametrize("m,n,k,epi,tiled", [(800, 4096, 4096, 0, 1), (800, 12288, 1024, 1, 1), (777, 2048, 512, 2, 0),
+                                             (200, 4096, 2048, 0, 1), (64, 768, 256, 1, 0), (1000, 1280, 4096, 0, 1),
+                                             (6400, 4096, 1024, 0, 1), (33, 512, 256, 2, 1)])
+def test_gemm_swapped_pair(L, m, n, k, epi, tiled):
+    """Swapped 2-CTA GEMM (weight rows on the MMA's M side, activation tiles of a
+    runtime width on its N side; qcf_set_gemm_plan 7) vs an fp32 torch reference
+    and vs the auto plan, for store / ReLU (bf16) / residual add (f32), row-major
+    and tile-major weights, ragged M and N not a multiple of 256; bit-identical
+    to the normal 256-row pair plan (same MMA k order and rounding)."""
+    from paper_2604_08585_b200.model import tile64
+    torch.manual_seed(m + n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bw = tile64(b) if tiled else b
+    out_dt = L.QCF_BF16 if epi == 1 else L.QCF_F32
+    tdt = torch.bfloat16 if epi == 1 else torch.float32
+    init = torch.randn(m, n, device="cuda").to(tdt)
+    ws = torch.zeros(max(int(L.lib.qcf_gemm_workspace(m, n, k)), 16), dtype=torch.uint8, device="cuda")
+    outs = []
+    try:
+        for plan in (7, 0, 7) + ((1,) if m >= 192 and n >= 256 else ()):
+            L.call("qcf_set_gemm_plan", plan)
+            c = init.clone()
+            L.call("qcf_gemm_ws", L.QCF_BF16, p(a), k, p(bw), k, p(c), n, m, n, k, epi, out_dt, tiled, p(ws),
+                   ws.numel(), S())
+            outs.append(c)
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_gemm_plan", 0)
+    ref = a.float() @ b.float().t()
+    if epi == 1:
+        ref = ref.relu()
+    elif epi == 2:
+        ref = ref + init
+    tol = 2e-2 if epi == 1 else 1e-3
+    scale = max(1.0, ref.abs().max().item())
+    assert (outs[0].float() - ref).abs().max().item() < tol * scale
+    assert torch.equal(outs[0], outs[2])
+    assert (outs[0].float() - outs[1].float()).abs().max().item() < tol * scale
+    if len(outs) > 3:
+        assert torch.equal(outs[0], outs[3])
+
+
+@pytest.mark.parametrize("m,heads,hkv", [(800, 8, 8), (250, 4, 2), (1000, 32, 8)])
+def test_fused_qkv_rope_swapped(L, m, heads, hkv):
+    """The QKV + RoPE + KV-scatter epilogue of the swapped GEMM (lane = output
+    column; the rotation partner comes from the neighbouring lane) equals the
+    256-row pair plan's (thread = output row); GQA column layout."""
+    from paper_2604_08585_b200.model import RopeTable
+    torch.manual_seed(m + heads)
+    D, K = 128, 1024
+    N = (heads + 2 * hkv) * D
+    a = (torch.randn(m, K, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    pos = torch.sort(torch.randperm(6000, device="cuda")[:m]).values.int()
+    dst = torch.randperm(m + 7, device="cuda")[:m].int()
+    rope = RopeTable(D, 10000.0, "cuda", 8192)
+    res = []
+    try:
+        for plan in (7, 1 if m >= 192 else 4):
+            L.call("qcf_set_gemm_plan", plan)
+            q = torch.zeros(m, heads, D, device="cuda", dtype=torch.bfloat16)
+            kt = torch.zeros(m + 7, hkv, D, device="cuda", dtype=torch.bfloat16)
+            vt = torch.zeros_like(kt)
+            L.call("qcf_gemm_qkv_rope", p(a), K, p(w), K, 0, m, K, heads, hkv, D, p(pos), p(dst), p(rope.cs32),
+                   rope.n_pos, p(q), p(kt), p(vt), None, 0, S())
+            res.append((q, kt, vt))
+        torch.cuda.synchronize()
+    finally:
+        L.call("qcf_set_gemm_plan", 0)
+    for x, y in zip(res[0], res[1]):
+        assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
+    assert torch.equal(res[0][2], res[1][2]) or (res[0][2].float() - res[1][2].float()).abs().max().item() < 1e-2

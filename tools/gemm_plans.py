@@ -1,6 +1,7 @@
 """TFLOP/s of every tcgen05 GEMM tile plan at the fused-path shapes (CUDA events; +8 = stream-K on;
 tile-major weights as in production). Plans: 1 = 2-CTA 256x256, 2 = 1-CTA
-128x256, 3 = 128x128, 4 = 128x64, 0 = the auto choice."""
+128x256, 3 = 128x128, 4 = 128x64, 6 = 2-CTA 256x128, 0 = the auto choice
+(QCF_PLANS=0,1,6 selects)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -19,7 +20,8 @@ for m in ms:
         c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16 if epi == 1 else torch.float32)
         row = {"m": m, "n": n, "k": k}
         ws = torch.zeros(int(_lib.lib.qcf_gemm_workspace(m, n, k)), dtype=torch.uint8, device="cuda")
-        for plan in (0, 8, 1, 9, 2, 3, 4):
+        plans = [int(x) for x in __import__("os").environ.get("QCF_PLANS", "0,8,1,9,2,3,4,6").split(",")]
+        for plan in plans:
             _lib.call("qcf_set_gemm_plan", plan)
             f = lambda: _lib.call("qcf_gemm_ws", 1, a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k, epi,
                                   out_dt, 1, ws.data_ptr(), ws.numel(), S)
