@@ -774,6 +774,63 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
   }
 }
 
+// epilogue of 4 consecutive columns [col, col+4) of one row from fp32 sums
+// (split-K reductions): store / ReLU / residual add, or the QKV RoPE + scatter
+// (4 columns = 2 interleaved pairs of one head)
+__device__ __forceinline__ void epi_store4(void* __restrict__ C, int64_t ldc, int row, int col, float4 acc,
+                                           const EpiArgs& ea) {
+  const int epi = ea.kind, out_dtype = ea.out_dtype;
+  if (epi == QCF_EPI_ROPE_QKV) {
+    // columns [Q | K | V] (h / hkv heads x d); 4 columns = 2 interleaved pairs of one head
+    const int qd = ea.h * ea.d, kd = ea.hkv * ea.d;
+    __nv_bfloat16* out;
+    int base;
+    bool rot = true;
+    if (col < qd) {
+      base = col;
+      out = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)row * qd + base;
+    } else {
+      const int64_t drow = ea.dst[row];
+      if (col < qd + kd) {
+        base = col - qd;
+        out = reinterpret_cast<__nv_bfloat16*>(ea.k_tab) + drow * kd + base;
+      } else {
+        base = col - qd - kd;
+        out = reinterpret_cast<__nv_bfloat16*>(ea.v_tab) + drow * kd + base;
+        rot = false;
+      }
+    }
+    if (rot) {
+      const int64_t t0 = (int64_t)ea.pos[row] * (ea.d >> 1) + ((base % ea.d) >> 1);
+      const float4 cs = __ldg(reinterpret_cast<const float4*>(ea.cs_tbl + 2 * t0));
+      const float c0 = cs.x, s0 = cs.y, c1 = cs.z, s1 = cs.w;
+      const float x = acc.x * c0 - acc.y * s0, y = acc.x * s0 + acc.y * c0;
+      const float z = acc.z * c1 - acc.w * s1, w = acc.z * s1 + acc.w * c1;
+      acc = make_float4(x, y, z, w);
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    *reinterpret_cast<uint2*>(out) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    return;
+  }
+  if (out_dtype == QCF_F32) {
+    float4* c = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)row * ldc + col);
+    if (epi == QCF_EPI_ADD_F32) {
+      const float4 o = *c;
+      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+    } else if (epi == QCF_EPI_RELU) {
+      acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+    }
+    *c = acc;
+  } else {
+    if (epi == QCF_EPI_RELU) {
+      acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
 // deterministic split-K reduction: C = epi(sum_s partial[s]) in split order.
 // Epilogues: store / ReLU / residual add (f32 or bf16 C) and the fused QKV
 // RoPE + KV scatter (the probe's M <= 32 projection: the rotation happens here,
@@ -782,7 +839,6 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
                                      void* __restrict__ C, int64_t ldc, const EpiArgs ea) {
   pdl_wait();
   pdl_trigger();
-  const int epi = ea.kind, out_dtype = ea.out_dtype;
   const int64_t total4 = (int64_t)M * N / 4;
   const int64_t mn = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -793,55 +849,137 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     const int row = (int)(e / N), col = (int)(e - (int64_t)row * N);
-    if (epi == QCF_EPI_ROPE_QKV) {
-      // columns [Q | K | V] (h / hkv heads x d); 4 columns = 2 interleaved pairs of one head
-      const int qd = ea.h * ea.d, kd = ea.hkv * ea.d;
-      __nv_bfloat16* out;
-      int base;
-      bool rot = true;
-      if (col < qd) {
-        base = col;
-        out = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)row * qd + base;
-      } else {
-        const int64_t drow = ea.dst[row];
-        if (col < qd + kd) {
-          base = col - qd;
-          out = reinterpret_cast<__nv_bfloat16*>(ea.k_tab) + drow * kd + base;
-        } else {
-          base = col - qd - kd;
-          out = reinterpret_cast<__nv_bfloat16*>(ea.v_tab) + drow * kd + base;
-          rot = false;
-        }
+    epi_store4(C, ldc, row, col, acc, ea);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Skinny GEMM (M <= 64: the probe's query rows) as a weight stream with the
+// split-K reduction inside a thread-block cluster. CTA (tile, split) of a
+// cluster of S CTAs: 128 weight rows (the MMA's M side) x one of S equal
+// k-ranges, the <= 64 activation rows on the MMA's N side (32 or 64). Each CTA
+// parks its fp32 partial [m][128] in its own shared memory (the drained stage
+// ring); after a cluster barrier, CTA r sums slice r of the tile over the S
+// partials in rank order through distributed shared memory (deterministic) and
+// applies the epilogue -- no fp32 partials in HBM and no second kernel.
+// ~100 KB of shared memory -> 2 CTAs per SM, 4 x 16 KB weight stages each.
+constexpr int SKC_STAGES = 4;
+constexpr int SKC_A = 128 * TC_BK * 2;   // weight rows
+constexpr int SKC_B = 64 * TC_BK * 2;    // activation rows (up to 64)
+constexpr int SKC_STAGE = SKC_A + SKC_B;
+constexpr int SKC_SMEM = SKC_STAGES * SKC_STAGE + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+template <int NM>
+__global__ void __launch_bounds__(TC_THREADS, 2)
+gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + SKC_STAGES * SKC_A;
+  float* part = reinterpret_cast<float*>(smem);  // [NM][128], after the ring has drained
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SKC_STAGES * SKC_STAGE);
+  uint64_t* empty = full + SKC_STAGES;
+  uint64_t* done = empty + SKC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank(), S = cluster_nctarank();
+  const int tile = blockIdx.x / S;
+  const int kbt = (K + TC_BK - 1) / TC_BK;
+  const int kb0 = (int)(rank * kbt / S), kb1 = (int)((rank + 1) * kbt / S);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&map_x);
+    for (int s = 0; s < SKC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, NM);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int it = kb - kb0, s = it % SKC_STAGES;
+        mbar_wait(&empty[s], ((it / SKC_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], SKC_A + NM * 128);
+        if (ea.b_tiled)
+          tma_load_4d(sA + s * SKC_A, &map_w, &full[s], 0, 0, kb, tile * 2);
+        else
+          tma_load_2d(sA + s * SKC_A, &map_w, &full[s], kb * TC_BK, tile * 128);
+        tma_load_2d(sB + s * SKC_B, &map_x, &full[s], kb * TC_BK, 0);
       }
-      if (rot) {
-        const int64_t t0 = (int64_t)ea.pos[row] * (ea.d >> 1) + ((base % ea.d) >> 1);
-        const float4 cs = __ldg(reinterpret_cast<const float4*>(ea.cs_tbl + 2 * t0));
-        const float c0 = cs.x, s0 = cs.y, c1 = cs.z, s1 = cs.w;
-        const float x = acc.x * c0 - acc.y * s0, y = acc.x * s0 + acc.y * c0;
-        const float z = acc.z * c1 - acc.w * s1, w = acc.z * s1 + acc.w * c1;
-        acc = make_float4(x, y, z, w);
-      }
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
-      *reinterpret_cast<uint2*>(out) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-      continue;
     }
-    if (out_dtype == QCF_F32) {
-      float4* c = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (int64_t)row * ldc + col);
-      if (epi == QCF_EPI_ADD_F32) {
-        const float4 o = *c;
-        acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
-      } else if (epi == QCF_EPI_RELU) {
-        acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(128, NM);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int it = kb - kb0, s = it % SKC_STAGES;
+        mbar_wait(&full[s], (it / SKC_STAGES) & 1);
+        tc_fence_after();
+        const uint64_t a0 = umma_desc_k_sw128(sA + s * SKC_A);
+        const uint64_t b0 = umma_desc_k_sw128(sB + s * SKC_B);
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 16; ++kk)
+          mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb > kb0 || kk) ? 1u : 0u);
+        mma_commit(&empty[s]);
       }
-      *c = acc;
-    } else {
-      if (epi == QCF_EPI_RELU) {
-        acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
-      }
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)row * ldc + col) =
-          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      mma_commit(done);  // also fires when this split has no k-blocks
     }
+  } else {  // ---------------- warps 2..5: TMEM partial -> shared memory [m][n]
+    const int g = warp & 3;
+    mbar_wait(done, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < NM; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + c0 + ((uint32_t)(g * 32) << 16), r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) part[(c0 + j) * 128 + g * 32 + lane] = kb1 > kb0 ? __uint_as_float(r[j]) : 0.f;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // every partial of the tile is in its CTA's shared memory
+  // ---------------- CTA r: slice r of the tile's float4 groups, summed in rank order
+  const int G = M * 32;  // float4 groups: M rows x 128 columns / 4
+  const int g0 = (int)(rank * G / S), g1 = (int)((rank + 1) * G / S);
+  for (int gi = g0 + (int)threadIdx.x; gi < g1; gi += blockDim.x) {
+    const int m = gi >> 5, n4 = (gi & 31) * 4;
+    const uint32_t off = smem_u32(part + m * 128 + n4);
+    float4 acc = ld_dsmem_f4(map_to_rank_addr(off, 0));
+    for (uint32_t s2 = 1; s2 < S; ++s2) {
+      const float4 v = ld_dsmem_f4(map_to_rank_addr(off, s2));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const int col = tile * 128 + n4;
+    if (col < N) epi_store4(C, ldc, m, col, acc, ea);
+  }
+  cluster_sync();  // the peers are done reading this CTA's partial
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, NM);
   }
 }
 
@@ -1143,8 +1281,60 @@ int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void*
   return gemm_tc_skinny_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, ws, ws_bytes, s);
 }
 
+// cluster split-K skinny launch (M <= 64): S CTAs per 128 weight rows, S chosen so
+// the grid fills two CTAs per SM (<= 8, the portable cluster size)
+static int g_skinny_cl = -1;  // QCF_SKINNY_CL env: 0 -> the global-memory split-K path
+static int launch_skc(const void* a, int64_t lda, const void* w, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+  if (m > 64 || (n % 4) || (k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)w & 15))
+    return QCF_EUNSUPPORTED;
+  if (ea.kind != QCF_EPI_ROPE_QKV && ((ldc % 4) || ((uintptr_t)c & 15))) return QCF_EUNSUPPORTED;
+  const int nm = m <= 32 ? 32 : 64;
+  const int64_t tiles = (n + 127) / 128, kbt = (k + TC_BK - 1) / TC_BK;
+  int S = (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * sm_count()) / tiles));
+  S = (int)std::min<int64_t>(S, kbt);
+  CUtensorMap mw, mx;
+  int st = make_b_map(&mw, w, n, k, ldb, 128, ea.b_tiled);
+  if (st != QCF_OK) return st;
+  st = make_kmajor_map(&mx, a, m, k, lda, nm);
+  if (st != QCF_OK) return st;
+  auto kern = nm == 32 ? gemm_skc_kernel<32> : gemm_skc_kernel<64>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[nm == 64]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SKC_SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_skc attr");
+    attr_set[nm == 64] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles * S));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = SKC_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea);
+  if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 cluster split-K)");
+  QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 cluster split-K)");
+  return QCF_OK;
+}
+
 static int gemm_tc_skinny_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
                              int64_t n, int64_t k, const EpiArgs& ea, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (g_skinny_cl < 0) {
+    const char* e = getenv("QCF_SKINNY_CL");
+    g_skinny_cl = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (g_skinny_cl) {
+    const int st = launch_skc(a, lda, b, ldb, c, ldc, m, n, k, ea, s);
+    if (st != QCF_EUNSUPPORTED) return st;
+  }
   const int sp = skinny_splits(m, n, k);
   if (sp <= 1 || ws_bytes < gemm_workspace_bytes(m, n, k) || (n % 4) || ((uintptr_t)ws & 15)) return QCF_EUNSUPPORTED;
   if ((k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)b & 15)) return QCF_EUNSUPPORTED;
@@ -1176,7 +1366,7 @@ int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb,
   EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cs_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
-  if (m <= 32 && ws) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction
+  if (m <= 64) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction
     const int st = gemm_tc_skinny_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, ws, ws_bytes, s);
     if (st != QCF_EUNSUPPORTED) return st;
   }

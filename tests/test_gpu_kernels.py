@@ -267,8 +267,13 @@ def test_attention_tensor_core_long_and_rescale(L, m, n, H, growth):
 
 
 @pytest.mark.parametrize("m,n,k,epi", [(32, 12288, 4096, 0), (32, 4096, 14336, 2), (32, 14336, 4096, 1),
-                                       (20, 4096, 4096, 2), (64, 1024, 2048, 0), (1, 4096, 4096, 0)])
+                                       (20, 4096, 4096, 2), (64, 1024, 2048, 0), (1, 4096, 4096, 0),
+                                       (48, 4096, 4096, 1), (33, 12288, 1024, 2), (50, 2000, 1000, 0),
+                                       (64, 14336, 4096, 0), (7, 128, 64, 0)])
 def test_gemm_skinny_splitk_deterministic(L, m, n, k, epi):
+    """M <= 64: weight-streaming split-K (the cluster kernel reduces the fp32
+    partials through distributed shared memory in rank order) vs an fp32 torch
+    reference; bit-identical across launches."""
     torch.manual_seed(m + n)
     a = (torch.randn(m, k, device="cuda") * 0.5).bfloat16()
     b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
@@ -319,7 +324,7 @@ def test_fused_qkv_rope_matches_two_step(L, m, heads, kdim):
            p(q2), p(k2), p(v2), L.QCF_BF16, S())
     for x, y in ((q1, q2), (k1, k2), (v1, v2)):
         assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
-    if m > 32:  # same single-pass accumulation -> V bit-identical (split-K sums in another order)
+    if m > 64:  # same single-pass accumulation -> V bit-identical (M <= 64 split-K sums in another order)
         assert torch.equal(v1, v2)
 
 

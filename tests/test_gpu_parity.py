@@ -558,8 +558,10 @@ def test_llama_width_bf16_against_oracle(tmp_path):
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_precompute_batch_equals_precompute(tmp_path, dtype):
     """Batched chunk precompute (one layer stack over B equal-length chunks)
-    produces the same records as one-at-a-time precompute: K/V bit-identical,
-    same anchors, cache hits for known chunks, mixed lengths grouped."""
+    produces the same records as one-at-a-time precompute: K/V bit-identical
+    (bf16 chunks of <= 64 tokens precomputed ALONE take the split-K weight-
+    streaming GEMM, whose fp32 sums associate differently: equal to bf16
+    rounding there), same anchors, cache hits for known chunks, mixed lengths grouped."""
     import paper_2604_08585_b200 as Q
     cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=5)
     w = Q.init_weights(cfg, dtype=dtype)
@@ -571,10 +573,14 @@ def test_precompute_batch_equals_precompute(tmp_path, dtype):
     s2.precompute(w, toks[1], 0.1)                    # one already cached
     r2 = s2.precompute_batch(w, toks + [toks[0]], 0.1)
     assert s2.manifest.cache_hits == 2                # the cached chunk + the in-call duplicate
-    for a, b in zip(r1, r2):
+    for t, a, b in zip(toks, r1, r2):
         assert a.chunk_id == b.chunk_id
         assert np.array_equal(a.anchor_indices, b.anchor_indices)
-        assert torch.equal(a.k, b.k) and torch.equal(a.v, b.v)
+        if dtype == "bf16" and len(t) <= 64:
+            for x, y in ((a.k, b.k), (a.v, b.v)):
+                assert (x.float() - y.float()).abs().max().item() <= 2 ** -6 * max(1.0, y.float().abs().max().item())
+        else:
+            assert torch.equal(a.k, b.k) and torch.equal(a.v, b.v)
     assert r2[-1].chunk_id == r1[0].chunk_id
 
 
