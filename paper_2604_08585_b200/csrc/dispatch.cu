@@ -92,7 +92,7 @@ extern "C" int qcf_gemm_ws(int dtype, const void* a, int64_t lda, const void* b,
   QCF_REQUIRE(b_layout == QCF_B_ROWMAJOR || b_layout == QCF_B_TILE64, QCF_EINVAL, "qcf_gemm_ws: bad b_layout");
   if (m == 0 || n == 0) return QCF_OK;
   auto s = qcf::as_stream(stream);
-  if (dtype == QCF_BF16 && qcf::tc_ok() && m <= 64) {
+  if (dtype == QCF_BF16 && qcf::tc_ok() && m <= 256) {
     st = qcf::gemm_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, b_layout, ws, ws_bytes, s);
     if (st != QCF_EUNSUPPORTED) return st;
   }

@@ -854,20 +854,25 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
 }
 
 // ---------------------------------------------------------------------------
-// Skinny GEMM (M <= 64: the probe's query rows) as a weight stream with the
-// split-K reduction inside a thread-block cluster. CTA (tile, split) of a
-// cluster of S CTAs: 128 weight rows (the MMA's M side) x one of S equal
-// k-ranges, the <= 64 activation rows on the MMA's N side (32 or 64). Each CTA
-// parks its fp32 partial [m][128] in its own shared memory (the drained stage
-// ring); after a cluster barrier, CTA r sums slice r of the tile over the S
-// partials in rank order through distributed shared memory (deterministic) and
-// applies the epilogue -- no fp32 partials in HBM and no second kernel.
-// ~100 KB of shared memory -> 2 CTAs per SM, 4 x 16 KB weight stages each.
-constexpr int SKC_STAGES = 4;
-constexpr int SKC_A = 128 * TC_BK * 2;   // weight rows
-constexpr int SKC_B = 64 * TC_BK * 2;    // activation rows (up to 64)
-constexpr int SKC_STAGE = SKC_A + SKC_B;
-constexpr int SKC_SMEM = SKC_STAGES * SKC_STAGE + 1024 + 256;
+// Skinny GEMM (M <= 256: the probe's query rows, one request or a batch) as a
+// weight stream with the split-K reduction inside a thread-block cluster. CTA
+// (tile, split) of a cluster of S CTAs: 128 weight rows (the MMA's M side) x
+// one of S equal k-ranges, the activation rows on the MMA's N side (NM = 32,
+// 64, 128 or 256). Each CTA parks its fp32 partial [m][128] in its own shared
+// memory (the drained stage ring); after a cluster barrier, CTA r sums slice r
+// of the tile over the S partials in rank order through distributed shared
+// memory (deterministic) and applies the epilogue -- no fp32 partials in HBM
+// and no second kernel.
+constexpr int SKC_A = 128 * TC_BK * 2;   // weight rows per stage
+template <int NM>
+struct SkcCfg {
+  static constexpr int B = NM * TC_BK * 2;                    // activation rows per stage
+  static constexpr int STAGES = NM <= 64 ? 4 : (NM == 128 ? 3 : 4);  // (5 at NM = 32: no gain)
+  static constexpr int STAGE = SKC_A + B;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int OCC = NM <= 128 ? 2 : 1;               // CTAs per SM
+  static_assert(NM * 128 * 4 <= STAGES * STAGE, "partial must fit in the ring");
+};
 
 __device__ __forceinline__ uint32_t cluster_nctarank() {
   uint32_t r;
@@ -884,15 +889,17 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
 }
 
 template <int NM>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, SkcCfg<NM>::OCC)
 gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                 void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea) {
+  using Cfg = SkcCfg<NM>;
+  constexpr int SKC_STAGES = Cfg::STAGES, SKC_B = Cfg::B;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + SKC_STAGES * SKC_A;
   float* part = reinterpret_cast<float*>(smem);  // [NM][128], after the ring has drained
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SKC_STAGES * SKC_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SKC_STAGES * Cfg::STAGE);
   uint64_t* empty = full + SKC_STAGES;
   uint64_t* done = empty + SKC_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -951,7 +958,7 @@ gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant
     const int g = warp & 3;
     mbar_wait(done, 0);
     tc_fence_after();
-#pragma unroll
+#pragma unroll 1
     for (int c0 = 0; c0 < NM; c0 += 32) {
       uint32_t r[32];
       tmem_ld32(tmem + c0 + ((uint32_t)(g * 32) << 16), r);
@@ -1281,34 +1288,38 @@ int gemm_tc_skinny(const void* a, int64_t lda, const void* b, int64_t ldb, void*
   return gemm_tc_skinny_ea(a, lda, b, ldb, c, ldc, m, n, k, EpiArgs{epilogue, out_dtype, b_layout}, ws, ws_bytes, s);
 }
 
-// cluster split-K skinny launch (M <= 64): S CTAs per 128 weight rows, S chosen so
-// the grid fills two CTAs per SM (<= 8, the portable cluster size)
-static int g_skinny_cl = -1;  // QCF_SKINNY_CL env: 0 -> the global-memory split-K path
-static int launch_skc(const void* a, int64_t lda, const void* w, int64_t ldb, void* c, int64_t ldc, int64_t m,
-                      int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
-  if (m > 64 || (n % 4) || (k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)w & 15))
-    return QCF_EUNSUPPORTED;
-  if (ea.kind != QCF_EPI_ROPE_QKV && ((ldc % 4) || ((uintptr_t)c & 15))) return QCF_EUNSUPPORTED;
-  const int nm = m <= 32 ? 32 : 64;
+// cluster split-K skinny launch (M <= 256): S CTAs per 128 weight rows (<= 8, the
+// portable cluster size). S from a cold-L2 sweep at M = 32 (tools/gemm_plans.py,
+// QCF_SKC_S): ~1.5 CTAs per SM is best (QKV 96 tiles: S = 2 28 us vs S = 3 36 us;
+// the o / down projections' 32 tiles: S = 6-8); a cluster's CTAs never share an
+// SM, which caps the co-resident clusters well below 2 CTAs/SM worth.
+static int g_skinny_cl = -1;  // QCF_SKINNY_CL env: 0 -> the global-memory split-K path (M <= 32)
+static int g_skc_max_m = 256;
+static int g_skc_splits = 0;  // QCF_SKC_S: forced cluster size (measurement)
+template <int NM>
+static int launch_skc_nm(const CUtensorMap& mw, const void* a, int64_t lda, void* c, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+  using Cfg = SkcCfg<NM>;
   const int64_t tiles = (n + 127) / 128, kbt = (k + TC_BK - 1) / TC_BK;
-  int S = (int)std::max<int64_t>(1, std::min<int64_t>(8, (2 * sm_count()) / tiles));
-  S = (int)std::min<int64_t>(S, kbt);
-  CUtensorMap mw, mx;
-  int st = make_b_map(&mw, w, n, k, ldb, 128, ea.b_tiled);
+  // CTAs in flight: ~1.5 per SM at 2 CTAs/SM; just under one wave at 1 CTA/SM (M = 256:
+  // the down projection's 32 tiles x 4 = 128 CTAs, 63 -> 40 us cold)
+  const int64_t target = Cfg::OCC == 2 ? sm_count() * 3 / 2 : sm_count() * 7 / 8;
+  int S = (int)std::max<int64_t>(1, std::min<int64_t>(8, (target + tiles / 2) / tiles));
+  if (g_skc_splits > 0) S = g_skc_splits;
+  S = (int)std::max<int64_t>(1, std::min<int64_t>(S, kbt));
+  CUtensorMap mx;
+  int st = make_kmajor_map(&mx, a, m, k, lda, NM);
   if (st != QCF_OK) return st;
-  st = make_kmajor_map(&mx, a, m, k, lda, nm);
-  if (st != QCF_OK) return st;
-  auto kern = nm == 32 ? gemm_skc_kernel<32> : gemm_skc_kernel<64>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[nm == 64]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SKC_SMEM);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_skc_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "gemm_skc attr");
-    attr_set[nm == 64] = true;
+    attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles * S));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = SKC_SMEM;
+  cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1319,10 +1330,29 @@ static int launch_skc(const void* a, int64_t lda, const void* w, int64_t ldb, vo
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_skc_kernel<NM>, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 cluster split-K)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 cluster split-K)");
   return QCF_OK;
+}
+
+static int launch_skc(const void* a, int64_t lda, const void* w, int64_t ldb, void* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, const EpiArgs& ea, cudaStream_t s) {
+  if (m > g_skc_max_m || (n % 4) || (k % 8) || (lda % 8) || (ldb % 8) || ((uintptr_t)a & 15) || ((uintptr_t)w & 15))
+    return QCF_EUNSUPPORTED;
+  // M > 64: every 128-row weight tile re-reads all M activation rows (2x the weight
+  // bytes at M = 256) through L2 into one CTA per SM; that only pays off when the
+  // tiles x splits fit one wave (N <= 4096: the down projection 63 -> 40 us cold,
+  // QKV / up measured 1.4-1.9x slower than the 2-CTA / 1-CTA tiles)
+  if (m > 64 && n > 4096) return QCF_EUNSUPPORTED;
+  if (ea.kind != QCF_EPI_ROPE_QKV && ((ldc % 4) || ((uintptr_t)c & 15))) return QCF_EUNSUPPORTED;
+  CUtensorMap mw;
+  int st = make_b_map(&mw, w, n, k, ldb, 128, ea.b_tiled);
+  if (st != QCF_OK) return st;
+  if (m <= 32) return launch_skc_nm<32>(mw, a, lda, c, ldc, m, n, k, ea, s);
+  if (m <= 64) return launch_skc_nm<64>(mw, a, lda, c, ldc, m, n, k, ea, s);
+  if (m <= 128) return launch_skc_nm<128>(mw, a, lda, c, ldc, m, n, k, ea, s);
+  return launch_skc_nm<256>(mw, a, lda, c, ldc, m, n, k, ea, s);
 }
 
 static int gemm_tc_skinny_ea(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int64_t m,
@@ -1330,6 +1360,10 @@ static int gemm_tc_skinny_ea(const void* a, int64_t lda, const void* b, int64_t 
   if (g_skinny_cl < 0) {
     const char* e = getenv("QCF_SKINNY_CL");
     g_skinny_cl = (e && e[0] == '0') ? 0 : 1;
+    const char* mm = getenv("QCF_SKC_MAX_M");  // measurement knob: largest M on the cluster path
+    if (mm) g_skc_max_m = atoi(mm);
+    const char* ss = getenv("QCF_SKC_S");
+    if (ss) g_skc_splits = atoi(ss);
   }
   if (g_skinny_cl) {
     const int st = launch_skc(a, lda, b, ldb, c, ldc, m, n, k, ea, s);
@@ -1366,7 +1400,7 @@ int gemm_qkv_rope_launch(const void* a, int64_t lda, const void* w, int64_t ldb,
   EpiArgs ea{QCF_EPI_ROPE_QKV, QCF_BF16, b_layout, pos, dst, cs_tbl, q_out, k_tab, v_tab, h, hkv, d};
   const int64_t n = (int64_t)(h + 2 * hkv) * d;
   void* dummy_c = q_out;  // C is not written by this epilogue
-  if (m <= 64) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction
+  if (m <= 256) {  // the probe's q rows: split-K weight streaming, RoPE + scatter applied in the reduction
     const int st = gemm_tc_skinny_ea(a, lda, w, ldb, dummy_c, n, m, n, k, ea, ws, ws_bytes, s);
     if (st != QCF_EUNSUPPORTED) return st;
   }

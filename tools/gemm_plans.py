@@ -11,6 +11,8 @@ from paper_2604_08585_b200 import _lib
 from paper_2604_08585_b200.model import tile64
 
 S = torch.cuda.current_stream().cuda_stream
+FLUSH = __import__("os").environ.get("QCF_FLUSH", "0") == "1"
+flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda") if FLUSH else None
 ms = [int(x) for x in sys.argv[1:]] or [800, 6400]
 for m in ms:
     for n, k, epi in [(12288, 4096, 0), (4096, 4096, 0), (14336, 4096, 1), (4096, 14336, 0)]:
@@ -28,13 +30,25 @@ for m in ms:
             for _ in range(3):
                 f()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(20):
-                f()
-            e1.record()
-            torch.cuda.synchronize()
-            ms_ = e0.elapsed_time(e1) / 20
+            if FLUSH:  # cold L2 per launch (a 256 MB READ between launches -- clean lines, no write-back
+                # traffic during the timed launch -- outside the events)
+                ms_ = 0.0
+                for _ in range(10):
+                    flush.sum()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    f()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms_ += e0.elapsed_time(e1) / 10
+            else:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(20):
+                    f()
+                e1.record()
+                torch.cuda.synchronize()
+                ms_ = e0.elapsed_time(e1) / 20
             row[f"plan{plan}_us"] = round(ms_ * 1e3, 1)
             row[f"plan{plan}_tflops"] = round(2 * m * n * k / ms_ / 1e9, 1)
         _lib.call("qcf_set_gemm_plan", 0)
