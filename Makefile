@@ -15,7 +15,14 @@ build/obj/%.o: paper_2604_08585_b200/csrc/%.cu paper_2604_08585_b200/csrc/*.cuh 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 
-clean:
-	rm -rf build $(LIB)
+# measurement build (tools/attn_trace.py): per-CTA timeline stamps in the attention kernel
+trace: tools/bin/libqcf_trace.so
+tools/bin/libqcf_trace.so: $(SRC) paper_2604_08585_b200/csrc/*.cuh include/qcfuse_b200.h
+	@mkdir -p build/trace tools/bin
+	for f in $(SRC); do $(NVCC) $(NVFLAGS) -DQCF_ATTN_TRACE -c $$f -o build/trace/$$(basename $$f .cu).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ build/trace/*.o
 
-.PHONY: all clean
+clean:
+	rm -rf build $(LIB) tools/bin/libqcf_trace.so
+
+.PHONY: all clean trace

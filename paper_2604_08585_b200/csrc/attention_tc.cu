@@ -141,6 +141,25 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16
       "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]));
 }
 
+#ifdef QCF_ATTN_TRACE
+// measurement build only (tools/attn_trace.py): per-CTA globaltimer stamps
+__device__ unsigned long long* g_attn_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define QCF_TRACE(slot, val)                                                                              \
+  do {                                                                                                    \
+    if (g_attn_trace) {                                                                                   \
+      const int64_t cta = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z); \
+      g_attn_trace[cta * 8 + (slot)] = (val);                                                             \
+    }                                                                                                     \
+  } while (0)
+#else
+#define QCF_TRACE(slot, val) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
@@ -178,6 +197,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   const int m0 = qt * AT_BM - rshift;
   constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
 
+#ifdef QCF_ATTN_TRACE
+  if (threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    QCF_TRACE(0, sm);
+    QCF_TRACE(1, gtimer());
+  }
+#endif
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&map_q);
     tma_prefetch_desc(&map_k);
@@ -200,6 +227,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   __syncthreads();
   pdl_wait();  // barrier init + TMEM alloc overlap the previous kernel's tail
   pdl_trigger();
+  if (threadIdx.x == 0) {  // Q and the first K tile (every tile has >= 1 key tile) in flight
+    mbar_expect_tx(q_full, AT_TILE_BYTES);    // while the key range is being scanned
+    tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
+    tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
+    mbar_expect_tx(&k_full[0], AT_TILE_BYTES);
+    tma_load_3d(sK, &map_k, &k_full[0], kvh * AT_D, 0, req);
+    tma_load_3d(sK + AT_TILE_BYTES / 2, &map_k, &k_full[0], kvh * AT_D + 64, 0, req);
+  }
   // key range of this tile = 1 + max kmax over its rows (rows are normally
   // sorted by position, but the kernel does not rely on it)
   if (threadIdx.x < AT_BM) {
@@ -207,7 +242,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     int v = (rr >= 0 && rr < M) ? kmax[rr] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, min(v + 1, n_keys));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_kend, max(1, min(v + 1, n_keys)));
   }
   tc_fence_before();
   __syncthreads();
@@ -215,12 +250,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
   const uint32_t tS0 = tmem, tO = tmem + 256, tP0 = tmem + 384;  // S[2] | O | P[2] (64 cols each)
+#ifdef QCF_ATTN_TRACE
+  if (threadIdx.x == 0) { QCF_TRACE(2, gtimer()); QCF_TRACE(7, n_tiles); }
+#endif
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      mbar_expect_tx(q_full, AT_TILE_BYTES);
-      tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
-      tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
+    if (lane == 0) {  // ---------------- TMA producer (Q and K_0 were issued above)
       // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
       // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
       auto load_k = [&](int j) {
@@ -239,7 +274,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
         tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
       };
-      load_k(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) load_k(j + 1);
         load_v(j);
@@ -294,6 +328,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     for (int j = 0; j < n_tiles; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
+#ifdef QCF_ATTN_TRACE
+      if (j == 0 && threadIdx.x == 64) QCF_TRACE(3, gtimer());
+#endif
       tc_fence_after();
       uint32_t v[32];
       tmem_ld32(tS0 + sb * 128 + cg * 32 + lane_off, v);
@@ -394,6 +431,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       mbar_arrive(&p_full[j & 1]);
     }
     // epilogue: combine the 4 partial row sums, then O / l for this warp's 32 columns
+#ifdef QCF_ATTN_TRACE
+    if (threadIdx.x == 64) QCF_TRACE(4, gtimer());
+#endif
     named_bar(bar_id, 128);
     red[0][cg][r] = l;
     named_bar(bar_id, 128);
@@ -404,6 +444,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     uint32_t o[32];
     tmem_ld32(tO + cg * 32 + lane_off, o);
     tmem_ld_wait();
+#ifdef QCF_ATTN_TRACE
+    if (threadIdx.x == 64) QCF_TRACE(5, gtimer());
+#endif
     if (row >= 0 && row < M) {
       __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cg * 32;
 #pragma unroll
@@ -422,6 +465,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+#ifdef QCF_ATTN_TRACE
+    if (lane == 0) QCF_TRACE(6, gtimer());
+#endif
   }
 }
 
@@ -1057,7 +1103,10 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  const int ver = g_attn_ver ? g_attn_ver : ((grid_pairs > sms || n_split > 1) ? 2 : 1);
+  // ping-pong pairs pay off for long row lists (full prefill 5152 rows: 236 vs 268 us,
+  // 32k Mistral: 1216 vs 1341 us); at the recompute shape (~800 rows per request) single
+  // tiles are as fast for MHA and 10% faster for GQA-8 (tools/attn_bench.py)
+  const int ver = g_attn_ver ? g_attn_ver : (((grid_pairs > sms && m > 2048) || n_split > 1) ? 2 : 1);
   if (ver == 2) {
     static int pair_mode = -1;  // QCF_ATTN_PAIR: 0 adjacent (default), 1 mirrored
     if (pair_mode == -1) {
@@ -1093,3 +1142,10 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
 }
 
 }  // namespace qcf
+
+#ifdef QCF_ATTN_TRACE
+extern "C" int qcf_debug_set_attn_trace(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(qcf::g_attn_trace, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
+}
+#endif
