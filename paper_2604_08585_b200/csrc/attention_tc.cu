@@ -31,7 +31,9 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
 constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
 constexpr int AT_THREADS = 576;  // 2 control warps + 16 softmax warps
 constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
-constexpr int AT_SMEM = AT_TILE_BYTES * 5 + 1024 + 256;  // Q, K[2], V[2] (P lives in TMEM)
+constexpr int AT_VS = 3;  // V ring depth: a V tile is consumed a full key tile after its K tile, and
+                          // at 2 stages its TMA latency gated P.V (traced: ~1100 cycles per key tile)
+constexpr int AT_SMEM = AT_TILE_BYTES * (3 + AT_VS) + 1024 + 256;  // Q, K[2], V[3] (P lives in TMEM)
 
 // MN-major SW128 descriptor (B = V: N = head dim contiguous, K = keys):
 // 8-key groups 1024 B apart (SBO), 64-column atoms 16 KB apart (LBO).
@@ -113,6 +115,15 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ void mma_bf16_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -149,6 +160,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ unsigned long long* g_attn_trace2 = nullptr;  // [64 key tiles][8] clock64 stamps, CTA (0, 0, 0)
+#define QCF_TRACE2(j, k)                                                                                  \
+  do {                                                                                                    \
+    if (g_attn_trace2 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)               \
+      g_attn_trace2[(j) * 8 + (k)] = clock64();                                                           \
+  } while (0)
 #define QCF_TRACE(slot, val)                                                                              \
   do {                                                                                                    \
     if (g_attn_trace) {                                                                                   \
@@ -158,6 +175,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #else
 #define QCF_TRACE(slot, val) do {} while (0)
+#define QCF_TRACE2(j, k) do {} while (0)
 #endif
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
@@ -174,8 +192,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = smem + AT_TILE_BYTES;          // [2]
-  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [2]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * AT_TILE_BYTES);
+  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [AT_VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (3 + AT_VS) * AT_TILE_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;     // [2]  K ring: freed as soon as S_j is computed
   uint64_t* k_empty = bars + 3;    // [2]
@@ -183,9 +201,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   uint64_t* s_free = bars + 7;     // [2]
   uint64_t* p_full = bars + 9;     // [2]  per TMEM P buffer (one phase per use: no parity aliasing)
   uint64_t* pv_done = bars + 11;   // [2]
-  uint64_t* v_full = bars + 13;    // [2]  V ring: freed when P_j.V_j is done
-  uint64_t* v_empty = bars + 15;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* v_full = bars + 13;    // [AT_VS]  V ring: freed when P_j.V_j is done
+  uint64_t* v_empty = bars + 13 + AT_VS;  // [AT_VS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 2 * AT_VS);
   __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
   __shared__ int s_kend;
 
@@ -195,7 +213,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   const int head = blockIdx.x;
   const int kvh = head / (H / Hkv);
   const int m0 = qt * AT_BM - rshift;
-  constexpr int N_SOFT = (AT_THREADS / 32 - 2) * 32;  // 512 softmax threads
+  constexpr int N_SOFT_WARPS = AT_THREADS / 32 - 2;  // 16 softmax warps (one arrive each)
 
 #ifdef QCF_ATTN_TRACE
   if (threadIdx.x == 0) {
@@ -213,12 +231,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], N_SOFT_WARPS);
+      mbar_init(&p_full[s], N_SOFT_WARPS);
+      mbar_init(&pv_done[s], 1);
+    }
+    for (int s = 0; s < AT_VS; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], N_SOFT);
-      mbar_init(&p_full[s], N_SOFT);
-      mbar_init(&pv_done[s], 1);
     }
     fence_barrier_init();
     s_kend = 0;
@@ -267,8 +287,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
       };
       auto load_v = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % AT_VS;
+        mbar_wait(&v_empty[st], ((j / AT_VS) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
         uint8_t* v = sV + st * AT_TILE_BYTES;
         tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
@@ -280,7 +300,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp converged; one elected lane issues)
       constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A, K-major B
       constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
       mbar_wait(q_full, 0);
@@ -288,16 +308,30 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       auto issue_pv = [&](int jj) {
         const int st = jj & 1;
         mbar_wait(&p_full[st], (jj >> 1) & 1);
-        mbar_wait(&v_full[st], (jj >> 1) & 1);
+#ifdef QCF_ATTN_TRACE
+        QCF_TRACE2(jj, 7);
+#endif
+        const int vs = jj % AT_VS;
+        mbar_wait(&v_full[vs], (jj / AT_VS) & 1);
+#ifdef QCF_ATTN_TRACE
+        QCF_TRACE2(jj, 1);
+#endif
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {   // A = P_jj straight from TMEM (packed bf16)
-          const uint64_t b = umma_desc_mn_sw128(sV + st * AT_TILE_BYTES + kk * 16 * 128);
-          mma_bf16_ts(tO, tP0 + st * 64 + kk * 8, b, idesc_o, (jj | kk) != 0);
+          const uint64_t b = umma_desc_mn_sw128(sV + vs * AT_TILE_BYTES + kk * 16 * 128);
+          mma_bf16_ts_e(tO, tP0 + st * 64 + kk * 8, b, idesc_o, (jj | kk) != 0);
         }
-        mma_commit(&v_empty[st]);
-        mma_commit(&pv_done[st]);
+#ifdef QCF_ATTN_TRACE
+        QCF_TRACE2(jj, 2);
+#endif
+        mma_commit_e(&v_empty[vs]);
+        mma_commit_e(&pv_done[st]);
+#ifdef QCF_ATTN_TRACE
+        QCF_TRACE2(jj, 6);
+#endif
       };
+      // (issuing S_{j+2} ahead of P_j.V_j instead measured 4% slower)
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1, sb = j & 1;
         mbar_wait(&k_full[st], (j >> 1) & 1);
@@ -308,10 +342,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
           const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
                              (uint64_t)((kk & 3) * 2);
-          mma_bf16(tS0 + sb * 128, a, b, idesc_s, kk != 0);
+          mma_bf16_e(tS0 + sb * 128, a, b, idesc_s, kk != 0);
         }
-        mma_commit(&s_full[sb]);
-        mma_commit(&k_empty[st]);
+        mma_commit_e(&s_full[sb]);
+        mma_commit_e(&k_empty[st]);
+#ifdef QCF_ATTN_TRACE
+        QCF_TRACE2(j, 5);
+#endif
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_tiles - 1);
@@ -330,11 +367,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       mbar_wait(&s_full[sb], (j >> 1) & 1);
 #ifdef QCF_ATTN_TRACE
       if (j == 0 && threadIdx.x == 64) QCF_TRACE(3, gtimer());
+      if (threadIdx.x == 64) QCF_TRACE2(j, 0);
 #endif
       tc_fence_after();
       uint32_t v[32];
       tmem_ld32(tS0 + sb * 128 + cg * 32 + lane_off, v);
       tmem_ld_wait();
+
       const int lim = my_kmax - j * AT_BN - cg * 32;  // columns <= lim are visible
       const bool all_vis = __all_sync(0xffffffffu, lim >= 31);
       const bool none_vis = __all_sync(0xffffffffu, lim < 0);
@@ -348,6 +387,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       }
       red[sb][cg][r] = pmax * scale_log2;
       named_bar(bar_id, 128);
+
       const float tmax = fmaxf(fmaxf(red[sb][0][r], red[sb][1][r]), fmaxf(red[sb][2][r], red[sb][3][r]));
       const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
       float alpha = 1.f;
@@ -424,11 +464,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         }
       }
       l += psum;
+#ifdef QCF_ATTN_TRACE
+      if (threadIdx.x == 64) QCF_TRACE2(j, 3);
+#endif
       tmem_st16(tP0 + (j & 1) * 64 + cg * 16 + lane_off, pk);  // keys 32cg.. -> P cols 16cg..
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(&s_free[sb]);
-      mbar_arrive(&p_full[j & 1]);
+      __syncwarp();
+      if (lane == 0) {  // one arrive per warp: 512 per-thread arrives cost ~1000 cycles per key tile
+        mbar_arrive(&s_free[sb]);
+        mbar_arrive(&p_full[j & 1]);
+      }
+#ifdef QCF_ATTN_TRACE
+      if (threadIdx.x == 64) QCF_TRACE2(j, 4);
+#endif
     }
     // epilogue: combine the 4 partial row sums, then O / l for this warp's 32 columns
 #ifdef QCF_ATTN_TRACE
@@ -1147,5 +1196,9 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
 extern "C" int qcf_debug_set_attn_trace(void* buf) {
   unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
   return cudaMemcpyToSymbol(qcf::g_attn_trace, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int qcf_debug_set_attn_trace2(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(qcf::g_attn_trace2, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
 }
 #endif

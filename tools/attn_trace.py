@@ -40,10 +40,28 @@ def run(name, m, n_keys, H, Hkv, n_req, kmax):
     for _ in range(3):
         f()
     torch.cuda.synchronize()
+    buf2 = torch.zeros(64 * 8, dtype=torch.int64, device="cuda")
     _lib.lib.qcf_debug_set_attn_trace(ctypes.c_void_p(buf.data_ptr()))
+    _lib.lib.qcf_debug_set_attn_trace2(ctypes.c_void_p(buf2.data_ptr()))
     f()
     torch.cuda.synchronize()
     _lib.lib.qcf_debug_set_attn_trace(ctypes.c_void_p(0))
+    _lib.lib.qcf_debug_set_attn_trace2(ctypes.c_void_p(0))
+    c = buf2.view(64, 8).cpu().numpy().astype(np.int64)
+    nj = int((c[:, 0] > 0).sum())
+    if nj > 12:
+        js = range(4, min(nj - 2, 14))
+        d = lambda a, b: [int(c[j, b] - c[j, a]) for j in js]
+        print(json.dumps({"cta0_key_tiles": nj, "clk_per_tile": [int(c[j + 1, 0] - c[j, 0]) for j in js],
+                          "s_wait_to_exp_end": d(0, 3), "pv_p_seen_to_v_ready": d(7, 1),
+                          "pv_v_ready_to_mmas_issued": d(1, 2), "pv_mmas_to_commits": d(2, 6),
+                          "exp_end_to_arrive": d(3, 4),
+                          "arrive_to_next_s": [int(c[j + 1, 0] - c[j, 4]) for j in js],
+                          "p_seen_by_mma_to_pv_issued": d(7, 6),
+                          "p_arrive_to_p_seen_by_mma": d(4, 7),
+                          "p_arrive_to_pv_issued": [int(c[j, 6] - c[j, 4]) for j in js],
+                          "s_issued_to_s_seen": [int(c[j, 0] - c[j, 5]) for j in js],
+                          "s_issue_gap": [int(c[j + 1, 5] - c[j, 5]) for j in js]}), flush=True)
     _lib.call("qcf_set_attention_kernel", 0)
     t = buf.view(n_cta, 8).cpu().numpy().astype(np.int64)
     sm, t1, t2, t3, t4, t5, t6, nt = (t[:, i] for i in range(8))

@@ -1,0 +1,125 @@
+// tcgen05.mma issue throughput on one SM (clock64 around N back-to-back MMAs of
+// one thread, accumulate into one TMEM tile, then commit + wait):
+//   SS 128x128x16 (A, B from shared memory: the attention S = Q.K^T shape)
+//   TS 128x128x16 (A from TMEM: the P.V shape / a Q-in-TMEM S)
+//   SS 128x256x16 (two key tiles per MMA)
+// with and without concurrent shared-memory traffic from the other warps.
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2604_08585_b200/csrc \
+//        -o tools/bin/mma_bench tools/mma_bench.cu -lcuda
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "sm100.cuh"
+
+using namespace qcf::sm100;
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a), "l"(b), "r"(idesc),
+      "r"(acc));
+}
+
+// mode 0: SS N=128, 1: TS N=128, 2: SS N=256; noise: other warps hammer shared memory
+__global__ void __launch_bounds__(256, 1) kern(int mode, int n, int noise, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                 // 128 x 64 bf16 (16 KB)
+  uint8_t* sB = smem + 16384;         // 256 x 64 bf16 (32 KB)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  volatile float* junk = reinterpret_cast<float*>(smem + 70000);
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 49152 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.001f * (i & 255);
+  if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc(slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
+  if (threadIdx.x == 32) {
+    const uint32_t idesc = idesc_bf16_f32(128, mode == 2 ? 256 : (mode == 5 ? 64 : 128));
+    const uint64_t a0 = umma_desc_k_sw128(sA), b0 = umma_desc_k_sw128(sB);
+    long long t0 = clock64();
+    if (mode >= 6) {  // unrolled x8, descriptors precomputed, predicate constant (mode 6: N=128, 7: N=256)
+      const uint32_t id2 = idesc_bf16_f32(128, mode == 7 ? 256 : 128);
+      const uint64_t a1 = a0 + 2, a2 = a0 + 4, a3 = a0 + 6, b1 = b0 + 2, b2 = b0 + 4, b3 = b0 + 6;
+      for (int i = 0; i < n; i += 8) {
+        mma_bf16(tmem, a0, b0, id2, 1u);
+        mma_bf16(tmem, a1, b1, id2, 1u);
+        mma_bf16(tmem, a2, b2, id2, 1u);
+        mma_bf16(tmem, a3, b3, id2, 1u);
+        mma_bf16(tmem, a0, b0, id2, 1u);
+        mma_bf16(tmem, a1, b1, id2, 1u);
+        mma_bf16(tmem, a2, b2, id2, 1u);
+        mma_bf16(tmem, a3, b3, id2, 1u);
+      }
+    } else
+    for (int i = 0; i < n; ++i) {
+      const int kk = i & 3;
+      if (mode == 1)
+        mma_ts(tmem, tmem + 256 + kk * 8, b0 + (uint64_t)(kk * 2), idesc, 1u);
+      else if (mode == 3)  // two independent accumulators, alternating
+        mma_bf16(tmem + (i & 1) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+      else if (mode == 4)  // four independent accumulators, round-robin
+        mma_bf16(tmem + (i & 3) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+      else if (mode == 5)  // N = 64
+        mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+      else
+        mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+    }
+    long long t1 = clock64();
+    mma_commit(bar);
+    mbar_wait(bar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+    done = 1;
+  } else if (noise == 1 && warp >= 2) {
+    float acc = 0.f;
+    int i = threadIdx.x;
+    while (!done) {
+      acc += junk[(i * 33) & 8191];
+      junk[(i * 17 + 4096) & 8191] = acc;
+      ++i;
+    }
+  } else if (noise == 2 && warp >= 4) {  // TMEM load traffic from other columns (lane quarter = warp % 4)
+    uint32_t acc = 0;
+    const uint32_t base = tmem + 384 + ((uint32_t)((warp & 3) * 32) << 16);
+    while (!done) {
+      uint32_t r[32];
+      tmem_ld32(base, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc += r[q];
+    }
+    if (acc == 12345) junk[0] = 1.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 110000);
+  const char* names[8] = {"SS 128x128x16", "TS 128x128x16", "SS 128x256x16", "SS 128x128x16 2 accumulators",
+                          "SS 128x128x16 4 accumulators", "SS 128x64x16", "SS 128x128x16 unrolled",
+                          "SS 128x256x16 unrolled"};
+  for (int noise = 0; noise < 3; noise += 2)
+    for (int mode = 6; mode < 8; ++mode) {
+      const int n = 4096;
+      kern<<<1, 256, 110000>>>(mode, n, noise, d);
+      kern<<<1, 256, 110000>>>(mode, n, noise, d);
+      long long h[2];
+      cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+      const double ideal = (mode == 2 || mode == 7) ? 128.0 : (mode == 5 ? 32.0 : 64.0);  // cycles per MMA at 8192 flop/clk
+      printf("{\"mma\": \"%s\", \"smem_noise\": %d, \"clk_per_mma\": %.1f, \"ideal\": %.0f, \"err\": \"%s\"}\n",
+             names[mode], noise, (double)h[1] / n, ideal, cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
