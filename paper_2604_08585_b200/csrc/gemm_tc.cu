@@ -242,7 +242,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (converged warp, elected lane)
       constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, BN);
       uint32_t it = 0, t = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
@@ -263,12 +263,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t b0 = umma_desc_k_sw128(sB + s * Cfg::B_BYTES + j * Cfg::B_ATOM);
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 16; ++kk)  // +32 B per K=16 step inside the swizzle atom
-              mma_bf16(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
+              mma_bf16_e(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
                        (kb > kb0 || j || kk) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
+          mma_commit_e(&empty[s]);
         }
-        mma_commit(&tfull[acc]);
+        mma_commit_e(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue warps 2..5
@@ -459,7 +459,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+    if (rank == 0) {  // ---------------- MMA issuer (leader only; converged warp, elected lane)
       constexpr uint32_t idesc = idesc_bf16_f32(PM, BN);
       uint32_t it = 0, t = 0;
       SegIter sg = segs();
@@ -478,11 +478,11 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           const uint64_t b0 = umma_desc_k_sw128(sB + s * Cfg::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk)
-            mma_bf16_pair(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
+            mma_bf16_pair_e(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc,
                           (kb > kbs || kk) ? 1u : 0u);
-          mma_commit_pair(&empty[s]);
+          mma_commit_pair_e(&empty[s]);
         }
-        mma_commit_pair(&tfull[acc]);
+        mma_commit_pair_e(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue warps 2..5 (both CTAs, own 128 rows)
@@ -659,7 +659,7 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+    if (rank == 0) {  // ---------------- MMA issuer (leader only; converged warp, elected lane)
       const uint32_t idesc = idesc_bf16_f32(256, bna);
       uint32_t it = 0, t = 0;
       for (int u = cluster; u < n_units; u += n_clusters, ++t) {
@@ -676,10 +676,10 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
           const uint64_t b0 = umma_desc_k_sw128(sB + s * SW_B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk)
-            mma_bf16_pair(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) ? 1u : 0u);
-          mma_commit_pair(&empty[s]);
+            mma_bf16_pair_e(d_tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) ? 1u : 0u);
+          mma_commit_pair_e(&empty[s]);
         }
-        mma_commit_pair(&tfull[acc]);
+        mma_commit_pair_e(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue warps 2..5: lane = output column
@@ -939,7 +939,7 @@ gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (converged warp, elected lane)
       constexpr uint32_t idesc = idesc_bf16_f32(128, NM);
       for (int kb = kb0; kb < kb1; ++kb) {
         const int it = kb - kb0, s = it % SKC_STAGES;
@@ -949,10 +949,10 @@ gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant
         const uint64_t b0 = umma_desc_k_sw128(sB + s * SKC_B);
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 16; ++kk)
-          mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb > kb0 || kk) ? 1u : 0u);
-        mma_commit(&empty[s]);
+          mma_bf16_e(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb > kb0 || kk) ? 1u : 0u);
+        mma_commit_e(&empty[s]);
       }
-      mma_commit(done);  // also fires when this split has no k-blocks
+      mma_commit_e(done);  // also fires when this split has no k-blocks
     }
   } else {  // ---------------- warps 2..5: TMEM partial -> shared memory [m][n]
     const int g = warp & 3;
