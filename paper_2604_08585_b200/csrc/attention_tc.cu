@@ -677,7 +677,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nmax > 0) {  // ---------------- MMA issuer
+    if (nmax > 0) {  // ---------------- MMA issuer (converged warp, elected lane)
       constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);
       constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);  // B (V) MN-major
       mbar_wait(q_full, 0);
@@ -692,11 +692,11 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
           const uint64_t a = umma_desc_k_sw128(q + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
           const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
                              (uint64_t)((kk & 3) * 2);
-          mma_bf16(tmem + t * 128, a, b, idesc_s, kk != 0);
+          mma_bf16_e(tmem + t * 128, a, b, idesc_s, kk != 0);
         }
-        mma_commit(&s_full[t]);
+        mma_commit_e(&s_full[t]);
         const bool last_user = (t == 1) || (j >= nt1);
-        if (last_user) mma_commit(&k_empty[st]);
+        if (last_user) mma_commit_e(&k_empty[st]);
       };
       auto issue_pv = [&](int t, int j) {
         const int st = j & 1;
@@ -710,11 +710,11 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
           // of its own S columns -> col = ch*W + (16kk mod W)/2
           constexpr int W = A2Cfg<SPLIT>::W;
           const uint32_t pa = tmem + t * 128 + (kk * 16 / W) * W + ((kk * 16) % W) / 2;
-          mma_bf16_ts(tmem + 256 + t * 128, pa, b, idesc_o, (j | kk) != 0);
+          mma_bf16_ts_e(tmem + 256 + t * 128, pa, b, idesc_o, (j | kk) != 0);
         }
         const bool last_user = (t == 1) || (j >= nt1);
-        if (last_user) mma_commit(&v_empty[st]);
-        if (j == (t ? nt1 : nt0) - 1) mma_commit(&o_full[t]);
+        if (last_user) mma_commit_e(&v_empty[st]);
+        if (j == (t ? nt1 : nt0) - 1) mma_commit_e(&o_full[t]);
       };
       if (nt0 > 0) issue_s(0, 0);
       if (nt1 > 0) issue_s(1, 0);

@@ -102,21 +102,24 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_k, const __grid_constant
   pdl_trigger();
   const uint32_t tmem = tmem_slot;
 
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar_full, (uint32_t)(n_atoms * (ST_BM + N) * 128));
-    for (int a = 0; a < n_atoms; ++a) {
-      tma_load_3d(sK + a * ST_BM * 128, &map_k, &bar_full, kvh * D + a * 64, kt * ST_BM, req);
-      tma_load_3d(sQ + a * q_atom, &map_q, &bar_full, a * 64, kvh * G, req * nq + t0);
+  if (threadIdx.x < 32) {  // warp 0: one lane loads, the converged warp issues (elected lane)
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar_full, (uint32_t)(n_atoms * (ST_BM + N) * 128));
+      for (int a = 0; a < n_atoms; ++a) {
+        tma_load_3d(sK + a * ST_BM * 128, &map_k, &bar_full, kvh * D + a * 64, kt * ST_BM, req);
+        tma_load_3d(sQ + a * q_atom, &map_q, &bar_full, a * 64, kvh * G, req * nq + t0);
+      }
     }
+    __syncwarp();
     mbar_wait(&bar_full, 0);
     tc_fence_after();
     const uint32_t idesc = idesc_bf16_f32(ST_BM, n_pad);
     for (int kk = 0; kk < D / 16; ++kk) {
       const uint64_t a = umma_desc_k_sw128(sK + (kk >> 2) * (ST_BM * 128)) + (uint64_t)((kk & 3) * 2);
       const uint64_t b = umma_desc_k_sw128(sQ + (kk >> 2) * q_atom) + (uint64_t)((kk & 3) * 2);
-      mma_bf16(tmem, a, b, idesc, kk != 0);
+      mma_bf16_e(tmem, a, b, idesc, kk != 0);
     }
-    mma_commit(&bar_done);
+    mma_commit_e(&bar_done);
   }
 
   const int key = kt * ST_BM + warp * 32 + lane;
