@@ -586,21 +586,7 @@ constexpr int SW_STAGES = 6;
 constexpr int SW_A_BYTES = 128 * TC_BK * 2;  // this CTA's 128 weight rows
 constexpr int SW_B_BYTES = 128 * TC_BK * 2;  // up to 128 activation rows (BNA / 2)
 constexpr int SW_STAGE = SW_A_BYTES + SW_B_BYTES;
-constexpr int SW_SMEM = SW_STAGES * SW_STAGE + 1024 + 256;
-
-// out[row][col] for one element of the swapped epilogue (col = this lane's column)
-__device__ __forceinline__ void swap_store(void* __restrict__ C, int64_t ldc, int row, int col, float v,
-                                           const EpiArgs& ea) {
-  if (ea.out_dtype == QCF_F32) {
-    float* p = reinterpret_cast<float*>(C) + (int64_t)row * ldc + col;
-    if (ea.kind == QCF_EPI_ADD_F32) v += *p;
-    else if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
-    *p = v;
-  } else {
-    if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
-    reinterpret_cast<__nv_bfloat16*>(C)[(int64_t)row * ldc + col] = __float2bfloat16_rn(v);
-  }
-}
+constexpr int SW_SMEM = SW_STAGES * SW_STAGE + 1024 + 256 + 4 * 32 * 33 * 4;  // + epilogue staging
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
@@ -682,85 +668,35 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
         mma_commit_pair_e(&tfull[acc]);
       }
     }
-  } else {  // ---------------- epilogue warps 2..5: lane = output column
+  } else {  // ---------------- epilogue warps 2..5: lane = output column -> transposed via smem
+    // each tcgen05.ld gives lane n = column n of 32 consecutive rows; a padded 32 x 33
+    // staging tile per warp turns that into lane = row with 32 contiguous columns, so
+    // the row-per-thread epilogue (vector stores, in-register RoPE pairs) is reused
+    // and the results are bit-identical to the normal orientation's
     const int g = warp & 3;
+    float* stage = reinterpret_cast<float*>(smem + SW_STAGES * SW_STAGE + 256) + g * (32 * 33);  // after the barriers
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
-    const bool rope = ea.kind == QCF_EPI_ROPE_QKV;
-    const int qd = ea.h * ea.d, kd = ea.hkv * ea.d, half = ea.d >> 1;
     uint32_t t = 0;
     for (int u = cluster; u < n_units; u += n_clusters, ++t) {
       const int acc = t & 1;
-      const int col = (u / n_act) * 256 + rank * 128 + g * 32 + lane;
+      const int col0 = (u / n_act) * 256 + rank * 128 + g * 32;
       const int row0 = (u % n_act) * bna;
       const int rows = min(bna, M - row0);
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      // RoPE: columns [Q | K | V]; this warp's 32 columns lie inside one head
-      int region = 0;  // 0 Q, 1 K, 2 V
-      int base = col;
-      if (rope) {
-        if (col >= qd + kd) { region = 2; base = col - qd - kd; }
-        else if (col >= qd) { region = 1; base = col - qd; }
-      }
-      const int jp = (base % (ea.d > 0 ? ea.d : 1)) >> 1;
-      const bool odd = lane & 1;
 #pragma unroll 1
       for (int c0 = 0; c0 < rows; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem_base + acc * 256 + c0 + ((uint32_t)(g * 32) << 16), r);
         tmem_ld_wait();
-        const int nr = min(32, rows - c0);
-        // lane L holds row (row0 + c0 + L)'s metadata; rows are then broadcast by
-        // shuffles, and every batch of 8 rows issues all its loads before its stores
-        // (a store may alias the tables, so the compiler cannot hoist loads itself)
-        const int myrow = row0 + c0 + lane;
-        if (!rope) {
-          if (ea.kind == QCF_EPI_ADD_F32 && ea.out_dtype == QCF_F32) {
-            float* cp = reinterpret_cast<float*>(C) + (int64_t)(row0 + c0) * ldc + col;
 #pragma unroll
-            for (int jb = 0; jb < 32; jb += 8) {
-              float o[8];
+        for (int j = 0; j < 32; ++j) stage[j * 33 + lane] = __uint_as_float(r[j]);
+        __syncwarp();
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = (col < N && jb + e < nr) ? cp[(int64_t)(jb + e) * ldc] : 0.f;
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (col < N && jb + e < nr) cp[(int64_t)(jb + e) * ldc] = o[e] + __uint_as_float(r[jb + e]);
-            }
-          } else if (col < N) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < nr) swap_store(C, ldc, row0 + c0 + j, col, __uint_as_float(r[j]), ea);
-          }
-        } else {
-          const int mpos = lane < nr ? ea.pos[myrow] : 0;
-          const int mdst = (region != 0 && lane < nr) ? ea.dst[myrow] : 0;
-          const float2* cst = reinterpret_cast<const float2*>(ea.cs_tbl) + jp;
-          __nv_bfloat16* tab = reinterpret_cast<__nv_bfloat16*>(region == 1 ? ea.k_tab : ea.v_tab) + base;
-          __nv_bfloat16* qo = reinterpret_cast<__nv_bfloat16*>(ea.q_out) + (int64_t)(row0 + c0) * qd + base;
-          // all 32 rows' (cos, sin) loads in flight at once: one L2 round trip per chunk
-          float2 cs[32];
-          if (region != 2) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) cs[e] = __ldg(cst + (int64_t)__shfl_sync(0xffffffffu, mpos, e) * half);
-          }
-#pragma unroll
-          for (int jb = 0; jb < 32; jb += 8) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int j = jb + e;
-              float v = __uint_as_float(r[j]);
-              const float p = __shfl_xor_sync(0xffffffffu, v, 1);
-              const int drow = __shfl_sync(0xffffffffu, mdst, j);
-              // pair (e, o) = (even column, odd column): e' = e c - o s, o' = e s + o c
-              if (region != 2) v = odd ? (p * cs[j].y + v * cs[j].x) : (v * cs[j].x - p * cs[j].y);
-              if (j < nr && col < N) {
-                __nv_bfloat16* out = region == 0 ? qo + (int64_t)j * qd : tab + (int64_t)drow * kd;
-                *out = __float2bfloat16_rn(v);
-              }
-            }
-          }
-        }
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(stage[lane * 33 + j]);
+        __syncwarp();
+        if (lane < rows - c0 && col0 < N) epilogue_row32(C, ldc, row0 + c0 + lane, col0, N, r, ea);
       }
       tc_fence_before();
       mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
@@ -1453,13 +1389,11 @@ static int gemm_tc_launch_ea(const void* a, int64_t lda, const void* b, int64_t 
     g_swap_mode = (e && e[0] == '0') ? 0 : 1;
   }
   // swapped pairs when the activation rows pad badly into 256-row pairs (M ~ 800:
-  // 4 x 208 vs 4 x 256 rows) or their tiles fill the waves better. Not for the
-  // RoPE epilogue: its per-column rotation (partner column in the neighbouring
-  // lane, one (cos, sin) gather per row) measured 15% slower than the row-per-
-  // thread epilogue at M = 800, and its fp32 rounding of the rotation differs.
-  // The other epilogues are bit-identical to the normal orientation (same MMA
-  // k order, same rounding), so the plan choice never changes a result.
-  if (g_swap_mode && g_pair_mode && ea.kind != QCF_EPI_ROPE_QKV && m >= 64 && n >= 256 && n % 32 == 0) {
+  // 4 x 208 vs 4 x 256 rows) or their tiles fill the waves better. The epilogue is
+  // the row-per-thread one behind a shared-memory transpose, so every epilogue
+  // (RoPE included) is bit-identical to the normal orientation (same MMA k order,
+  // same rounding): the plan choice never changes a result.
+  if (g_swap_mode && g_pair_mode && m >= 64 && n >= 256 && n % 32 == 0) {
     int bna = 0, na = 0;
     const double cs = swap_plan(m, n, bna, na);
     if (bna && cs < 0.97 * pair_cost(m, n) && (n + 255) / 256 * na >= sms / 4)

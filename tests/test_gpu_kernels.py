@@ -618,9 +618,9 @@ def test_gemm_swapped_pair(L, m, n, k, epi, tiled):
 
 @pytest.mark.parametrize("m,heads,hkv", [(800, 8, 8), (250, 4, 2), (1000, 32, 8)])
 def test_fused_qkv_rope_swapped(L, m, heads, hkv):
-    """The QKV + RoPE + KV-scatter epilogue of the swapped GEMM (lane = output
-    column; the rotation partner comes from the neighbouring lane) equals the
-    256-row pair plan's (thread = output row); GQA column layout."""
+    """The QKV + RoPE + KV-scatter epilogue of the swapped GEMM (TMEM lane =
+    output column, transposed through shared memory into the row-per-thread
+    epilogue) is bit-identical to the 256-row pair plan's; GQA column layout."""
     from paper_2604_08585_b200.model import RopeTable
     torch.manual_seed(m + heads)
     D, K = 128, 1024
@@ -643,6 +643,5 @@ def test_fused_qkv_rope_swapped(L, m, heads, hkv):
         torch.cuda.synchronize()
     finally:
         L.call("qcf_set_gemm_plan", 0)
-    for x, y in zip(res[0], res[1]):
-        assert (x.float() - y.float()).abs().max().item() <= 2 ** -7 * max(1.0, y.float().abs().max().item())
-    assert torch.equal(res[0][2], res[1][2]) or (res[0][2].float() - res[1][2].float()).abs().max().item() < 1e-2
+    for x, y in zip(res[0], res[1]):   # same MMA k order and the same row epilogue behind the transpose
+        assert torch.equal(x, y)

@@ -23,7 +23,8 @@ def bench(m, n_keys, H, Hkv, n_req, kmax, it=20):
     nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H, n_keys))
     ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
     res["auto_split"] = int(_lib.lib.qcf_attention_split(m, n_req, H, n_keys))
-    for ver in (1, 2, 3, 0):   # 0 = auto with workspace (split-KV for one-wave grids)
+    order = [int(x) for x in __import__("os").environ.get("QCF_ATTN_ORDER", "1,2,3,0").split(",")]
+    for ver in order:   # 0 = auto with workspace (split-KV for one-wave grids)
         _lib.call("qcf_set_attention_kernel", ver)
         f = lambda: _lib.call("qcf_attention_batched_ws", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                               kmax.data_ptr(), m, n_req, H, Hkv, D, n_keys, out.data_ptr(),

@@ -32,8 +32,8 @@ w = tile64((torch.randn(N, K, device="cuda") * 0.05).bfloat16())
 pos = torch.sort(torch.randperm(6000, device="cuda")[:m]).values.int()
 rope = RopeTable(D, 500000.0, "cuda", 8192)
 q = torch.empty(m, H, D, device="cuda", dtype=torch.bfloat16)
-kt = torch.empty(6000, H, D, device="cuda", dtype=torch.bfloat16)
-vt = torch.empty_like(kt)
+kt = torch.zeros(6000, H, D, device="cuda", dtype=torch.bfloat16)  # unwritten rows stay 0 (not NaN garbage)
+vt = torch.zeros_like(kt)
 row = {"shape": "qkv_rope 800x12288x4096"}
 outs = {}
 for plan in (0, 1, 7, 0):
@@ -54,4 +54,8 @@ for plan in (0, 1, 7, 0):
     outs[plan] = (q.clone(), kt[:m].clone(), vt[:m].clone())
 call("qcf_set_gemm_plan", 0)
 row["rope_swap_eq_pair"] = [bool(torch.equal(x, y)) for x, y in zip(outs[7], outs[1])]
+row["rope_swap_ndiff"] = [int((x != y).sum().item()) for x, y in zip(outs[7], outs[1])]
+written = torch.zeros(m, dtype=torch.bool, device="cuda")
+written[pos[pos < m].long()] = True
+row["k_ndiff_written_rows"] = int((outs[7][1][written] != outs[1][1][written]).sum().item())
 print(json.dumps(row))
