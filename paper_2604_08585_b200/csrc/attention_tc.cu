@@ -61,6 +61,9 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 #ifndef A2_EMU16
 #define A2_EMU16 7  // of every 16 column pairs, this many take the FMA-pipe exp2 (balances MUFU vs FMA)
 #endif
+// which column pairs take the FMA-pipe exp2: spread through the loop (pair p with
+// (9p mod 16) < A2_EMU16) so the MUFU and FMA pipes are fed interleaved, not in runs
+#define A2_EMU(p) ((((p) * 9) & 15) < A2_EMU16)
 // ---- softmax arithmetic helpers (packed f32x2 FFMA2/FADD2, 3-input max, exp2
 // emulated on the FMA pipe for part of the columns: B200's MUFU ex2 rate (16/clk/SM)
 // would otherwise bound the softmax below the tensor core's rate)
@@ -379,8 +382,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       const bool none_vis = __all_sync(0xffffffffu, lim < 0);
       float pmax = -INFINITY;
       if (all_vis) {
+        {  // two independent max chains (shorter dependency chain)
+          float pm1 = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          for (int i = 0; i < 32; i += 4) {
+            pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+            pm1 = fmax3(pm1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+          }
+          pmax = fmaxf(pmax, pm1);
+        }
       } else if (!none_vis) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
@@ -436,7 +446,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           for (int i = 0; i < 32; i += 2) {
             const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
             uint64_t p2;
-            if (((i >> 1) & 15) < A2_EMU16) {
+            if (A2_EMU(i >> 1)) {
               p2 = exp2_poly2(x2);
             } else {
               float a, b;
@@ -785,7 +795,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
           for (int i = 0; i < 32; i += 2) {
             const uint64_t x2 = ffma2(f2(SROW(hh * 32 + i), SROW(hh * 32 + i + 1)), sc2, nm2);
             uint64_t p2;
-            if (((i >> 1) & 15) < A2_EMU16) {
+            if (A2_EMU(i >> 1)) {
               p2 = exp2_poly2(x2);
             } else {
               float a, b;
@@ -884,8 +894,15 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
           tmem_ld32(tS + ch * 64 + hh * 32, v);
           tmem_ld_wait();
           if (all_vis) {
+            {  // two independent max chains (shorter dependency chain)
+          float pm1 = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          for (int i = 0; i < 32; i += 4) {
+            pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+            pm1 = fmax3(pm1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+          }
+          pmax = fmaxf(pmax, pm1);
+        }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -923,7 +940,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
             for (int i = 0; i < 32; i += 2) {
               const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
               uint64_t p2;
-              if (((i >> 1) & 15) < A2_EMU16) {
+              if (A2_EMU(i >> 1)) {
                 p2 = exp2_poly2(x2);
               } else {
                 float a, b;
