@@ -31,9 +31,14 @@ int make_kmajor_map3(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
 constexpr int AT_BM = 128, AT_BN = 128, AT_D = 128;
 constexpr int AT_THREADS = 576;  // 2 control warps + 16 softmax warps
 constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
-constexpr int AT_VS = 3;  // V ring depth: a V tile is consumed a full key tile after its K tile, and
-                          // at 2 stages its TMA latency gated P.V (traced: ~1100 cycles per key tile)
-constexpr int AT_SMEM = AT_TILE_BYTES * (3 + AT_VS) + 1024 + 256;  // Q, K[2], V[3] (P lives in TMEM)
+// K / V ring depths of the single-tile kernel (Q + 5 tiles fit the 227 KB budget).
+// Traced (tools/attn_trace.py): with a 2-deep K ring the tensor pipe idled ~900
+// cycles per key tile waiting for K_{j+2}'s TMA (a K tile is 128 rows x 256 B
+// strided by the table row, ~1.5 us from HBM); separate producer lanes for K and V
+// keep a V wait from delaying the next K load
+constexpr int AT_KS = 3;
+constexpr int AT_VS = 2;
+constexpr int AT_SMEM = AT_TILE_BYTES * (1 + AT_KS + AT_VS) + 1024 + 256;  // Q, K[KS], V[VS] (P lives in TMEM)
 
 // MN-major SW128 descriptor (B = V: N = head dim contiguous, K = keys):
 // 8-key groups 1024 B apart (SBO), 64-column atoms 16 KB apart (LBO).
@@ -194,19 +199,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + AT_TILE_BYTES;          // [2]
-  uint8_t* sV = smem + 3 * AT_TILE_BYTES;      // [AT_VS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (3 + AT_VS) * AT_TILE_BYTES);
+  uint8_t* sK = smem + AT_TILE_BYTES;                  // [AT_KS]
+  uint8_t* sV = smem + (1 + AT_KS) * AT_TILE_BYTES;    // [AT_VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + AT_KS + AT_VS) * AT_TILE_BYTES);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [2]  K ring: freed as soon as S_j is computed
-  uint64_t* k_empty = bars + 3;    // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* s_free = bars + 7;     // [2]
-  uint64_t* p_full = bars + 9;     // [2]  per TMEM P buffer (one phase per use: no parity aliasing)
-  uint64_t* pv_done = bars + 11;   // [2]
-  uint64_t* v_full = bars + 13;    // [AT_VS]  V ring: freed when P_j.V_j is done
-  uint64_t* v_empty = bars + 13 + AT_VS;  // [AT_VS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 2 * AT_VS);
+  uint64_t* s_full = bars + 1;     // [2]
+  uint64_t* s_free = bars + 3;     // [2]
+  uint64_t* p_full = bars + 5;     // [2]  per TMEM P buffer (one phase per use: no parity aliasing)
+  uint64_t* pv_done = bars + 7;    // [2]
+  uint64_t* k_full = bars + 9;     // [AT_KS]  K ring: freed as soon as S_j is computed
+  uint64_t* k_empty = k_full + AT_KS;
+  uint64_t* v_full = k_empty + AT_KS;  // [AT_VS]  V ring: freed when P_j.V_j is done
+  uint64_t* v_empty = v_full + AT_VS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + AT_VS);
   __shared__ float red[2][4][AT_BM];   // per-tile partial row max (double-buffered by tile parity)
   __shared__ int s_kend;
 
@@ -231,9 +236,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     tma_prefetch_desc(&map_k);
     tma_prefetch_desc(&map_v);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < AT_KS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&s_free[s], N_SOFT_WARPS);
       mbar_init(&p_full[s], N_SOFT_WARPS);
@@ -278,28 +285,25 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
 #endif
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer (Q and K_0 were issued above)
-      // K_j is consumed by S_j (early), V_j by P_j.V_j (late): two rings, and K
-      // runs one tile ahead of V so S_{j+1} never waits on a V-gated slot
-      auto load_k = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+    // ---------------- TMA producers: lane 0 streams K (K_0 was issued above), lane 1
+    // streams V; K_j is consumed by S_j (early), V_j by P_j.V_j (a key tile later)
+    if (lane == 0) {
+      for (int j = 1; j < n_tiles; ++j) {
+        const int st = j % AT_KS;
+        mbar_wait(&k_empty[st], ((j / AT_KS) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
         uint8_t* k = sK + st * AT_TILE_BYTES;
         tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
         tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
-      };
-      auto load_v = [&](int j) {
+      }
+    } else if (lane == 1) {
+      for (int j = 0; j < n_tiles; ++j) {
         const int st = j % AT_VS;
         mbar_wait(&v_empty[st], ((j / AT_VS) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
         uint8_t* v = sV + st * AT_TILE_BYTES;
         tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
         tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
-      };
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) load_k(j + 1);
-        load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -334,10 +338,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         QCF_TRACE2(jj, 6);
 #endif
       };
-      // (issuing S_{j+2} ahead of P_j.V_j instead measured 4% slower)
+      // (issuing S_{j+2} ahead of P_j.V_j measured 4% slower, with either K ring depth)
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1, sb = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int st = j % AT_KS, sb = j & 1;
+        mbar_wait(&k_full[st], (j / AT_KS) & 1);
         mbar_wait(&s_free[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll

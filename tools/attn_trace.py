@@ -62,6 +62,11 @@ def run(name, m, n_keys, H, Hkv, n_req, kmax):
                           "p_arrive_to_pv_issued": [int(c[j, 6] - c[j, 4]) for j in js],
                           "s_issued_to_s_seen": [int(c[j, 0] - c[j, 5]) for j in js],
                           "s_issue_gap": [int(c[j + 1, 5] - c[j, 5]) for j in js]}), flush=True)
+        t0 = c[10, 4]
+        names = {0: "softmax sees S", 3: "exp end", 4: "softmax arrive P", 7: "MMA sees P", 1: "V ready",
+                 2: "PV MMAs issued", 6: "PV committed", 5: "S committed"}
+        ev = sorted((int(c[j, k] - t0), f"{names[k]}({j})") for j in range(9, 14) for k in names)
+        print(json.dumps({"timeline_rel_arrive10": ev}), flush=True)
     _lib.call("qcf_set_attention_kernel", 0)
     t = buf.view(n_cta, 8).cpu().numpy().astype(np.int64)
     sm, t1, t2, t3, t4, t5, t6, nt = (t[:, i] for i in range(8))
