@@ -6,7 +6,8 @@ import os
 import sys
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
-os.environ["QCFUSE_B200_LIB"] = str(ROOT / "tools/bin/libqcf_trace.so")
+os.environ["QCFUSE_B200_LIB"] = str(ROOT / "tools/bin" / os.environ.get("QCF_TRACE_LIB", "libqcf_trace.so"))
+
 sys.path.insert(0, str(ROOT))
 import ctypes
 import json
