@@ -49,10 +49,12 @@ __device__ __forceinline__ uint4 rotate_vec<__nv_bfloat16>(uint4 raw, int j0, co
   return outr;
 }
 
-// One CTA per (fused row, layer): the chunk lookup happens once per row, and
-// every thread moves ASM_UNROLL 16-byte vectors of K and of V with all loads
-// issued before the stores (more bytes in flight per thread; HBM-bound).
-constexpr int ASM_THREADS = 128, ASM_UNROLL = 4;
+// One CTA per (run of ASM_ROWS fused rows, layer): the chunk descriptor is looked
+// up only when a row leaves the cached chunk, and for bf16 the chunk's (cos, sin)
+// row is staged once in shared memory as float pairs (the same float casts of the
+// float64 table as before: bit-identical). Every thread moves ASM_UNROLL 16-byte
+// vectors of K and of V per row with all loads issued before the stores.
+constexpr int ASM_THREADS = 128, ASM_UNROLL = 4, ASM_ROWS = 4, ASM_MAX_HALF = 256;
 
 template <typename T>
 __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
@@ -63,49 +65,79 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
   pdl_wait();
   pdl_trigger();
   constexpr int V = Vec16<T>::N;
+  constexpr bool kBf16 = sizeof(T) == 2;
   const int layer = blockIdx.y;
   const int vpr = row_elems / V;
+  const int half = d >> 1;
   __shared__ qcf_chunk_desc sc;
   __shared__ int64_t s_delta;
-  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
-    T* dk = fk + layer * fstride + (int64_t)row * row_elems;
-    T* dv = fv + layer * fstride + (int64_t)row * row_elems;
-    if (row == 0) {
-      for (int i = threadIdx.x; i < vpr; i += blockDim.x) {
-        reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems)[i];
-        reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems)[i];
+  __shared__ float2 s_cs[ASM_MAX_HALF];   // bf16: (float cos, float sin) of the chunk's delta
+  int c_lo = 1, c_hi = 0;                 // fused rows of the cached chunk: [c_lo, c_hi)
+  for (int run = blockIdx.x * ASM_ROWS; run < n_rows; run += gridDim.x * ASM_ROWS) {
+    for (int row = run; row < min(run + ASM_ROWS, n_rows); ++row) {
+      T* dk = fk + layer * fstride + (int64_t)row * row_elems;
+      T* dv = fv + layer * fstride + (int64_t)row * row_elems;
+      if (row == 0) {
+        for (int i = threadIdx.x; i < vpr; i += blockDim.x) {
+          reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems)[i];
+          reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems)[i];
+        }
+        continue;
       }
-      continue;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int ci = find_chunk(chunks, n_chunks, row);
-      sc = chunks[ci];
-      s_delta = deltas ? deltas[ci] : sc.offset;  // rotation delta (default: the fused row)
-    }
-    __syncthreads();
-    const int64_t src_off = layer * sc.layer_stride + (int64_t)(row - sc.offset) * row_elems;
-    const uint4* sk = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.k) + src_off);
-    const uint4* sv = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.v) + src_off);
-    const double* ct = ctab + s_delta * (d / 2);
-    const double* st = stab + s_delta * (d / 2);
-    for (int i0 = threadIdx.x; i0 < vpr; i0 += blockDim.x * ASM_UNROLL) {
-      uint4 kv[ASM_UNROLL], vv[ASM_UNROLL];
-#pragma unroll
-      for (int u = 0; u < ASM_UNROLL; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < vpr) {
-          kv[u] = __ldg(sk + i);
-          vv[u] = __ldg(sv + i);
+      if (row < c_lo || row >= c_hi) {  // uniform: every thread tracks the same range
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int ci = find_chunk(chunks, n_chunks, row);
+          sc = chunks[ci];
+          s_delta = deltas ? deltas[ci] : sc.offset;  // rotation delta (default: the fused row)
+        }
+        __syncthreads();
+        c_lo = sc.offset;
+        c_hi = sc.offset + sc.n_tok;
+        if (kBf16) {
+          for (int t = threadIdx.x; t < half; t += blockDim.x)
+            s_cs[t] = make_float2((float)ctab[s_delta * half + t], (float)stab[s_delta * half + t]);
+          __syncthreads();
         }
       }
+      const int64_t src_off = layer * sc.layer_stride + (int64_t)(row - sc.offset) * row_elems;
+      const uint4* sk = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.k) + src_off);
+      const uint4* sv = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(sc.v) + src_off);
+      const double* ct = ctab + s_delta * half;
+      const double* st = stab + s_delta * half;
+      for (int i0 = threadIdx.x; i0 < vpr; i0 += blockDim.x * ASM_UNROLL) {
+        uint4 kv[ASM_UNROLL], vv[ASM_UNROLL];
 #pragma unroll
-      for (int u = 0; u < ASM_UNROLL; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < vpr) {
-          reinterpret_cast<uint4*>(dv)[i] = vv[u];
-          const int j0 = ((i * V) % d) >> 1;
-          reinterpret_cast<uint4*>(dk)[i] = rotate_vec<T>(kv[u], j0, ct, st);
+        for (int u = 0; u < ASM_UNROLL; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i < vpr) {
+            kv[u] = __ldg(sk + i);
+            vv[u] = __ldg(sv + i);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < ASM_UNROLL; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i < vpr) {
+            reinterpret_cast<uint4*>(dv)[i] = vv[u];
+            const int j0 = ((i * V) % d) >> 1;
+            if constexpr (kBf16) {
+              const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&kv[u]);
+              uint4 outr;
+              __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(&outr);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float2 f = __bfloat1622float2(p[t]);
+                const float2 cs = s_cs[j0 + t];
+                float oe, oo;
+                rotate_pair_fast(f.x, f.y, cs.x, cs.y, oe, oo);
+                q[t] = __floats2bfloat162_rn(oe, oo);
+              }
+              reinterpret_cast<uint4*>(dk)[i] = outr;
+            } else {
+              reinterpret_cast<uint4*>(dk)[i] = rotate_vec<T>(kv[u], j0, ct, st);
+            }
+          }
         }
       }
     }
@@ -152,7 +184,8 @@ extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int 
               "qcf_assemble: fused layer stride too small");
   auto s = qcf::as_stream(stream);
   QCF_REQUIRE(row_elems % (dtype == QCF_F32 ? 4 : 8) == 0, QCF_EUNSUPPORTED, "qcf_assemble: row not 16B multiple");
-  dim3 grid((unsigned)std::min<int64_t>(n_ctx + 1, 65535), n_layers);
+  QCF_REQUIRE(d / 2 <= qcf::ASM_MAX_HALF, QCF_EUNSUPPORTED, "qcf_assemble: d_head > %d", 2 * qcf::ASM_MAX_HALF);
+  dim3 grid((unsigned)std::min<int64_t>((n_ctx + 1 + qcf::ASM_ROWS - 1) / qcf::ASM_ROWS, 65535), n_layers);
   const dim3 block(qcf::ASM_THREADS);
   if (dtype == QCF_F32)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
