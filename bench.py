@@ -190,6 +190,7 @@ def phase_profile(eng, chunk_lists, queries, policy, ratio):
     plans, b = eng.prefill_batch(policy, ratio, chunk_lists, queries, use_graph=False)
     torch.cuda.synchronize()
     conc, eng.concurrent = eng.concurrent, False   # per-launch events on one stream
+    pipe, eng.pipeline_asm = eng.pipeline_asm, False
     _lib.profiler = _lib.Profiler()
     try:
         # park the GPU on a spin kernel so every launch below is queued before it
@@ -201,6 +202,7 @@ def phase_profile(eng, chunk_lists, queries, policy, ratio):
     finally:
         _lib.profiler = None
         eng.concurrent = conc
+        eng.pipeline_asm = pipe
     return plans, b, recs
 
 

@@ -90,6 +90,14 @@ int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
  * desc.offset.. but K rotates by deltas[c]: used to build the probe's anchor
  * prefix [BOS | R(off_c) K_c[anchors] ...] (fusion.py:281-303) straight from
  * device-resident anchor rows when the chunk pool lives in host memory. */
+/* Layers [layer0, layer0 + n_layers) only (bos_k/bos_v, fused_k/fused_v and the
+ * descriptors' k/v still point at layer 0): lets the assembly of layer l run on a
+ * side stream while the recompute works on earlier layers (fusion.py:234-263 per layer). */
+int qcf_assemble_range(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                       const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                       int64_t fused_layer_stride, int layer0, int n_layers, int hkv, int d,
+                       const double* cos_tbl, const double* sin_tbl, int64_t n_pos, int dtype,
+                       qcf_stream_t stream);
 int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
                      const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
                      int64_t fused_layer_stride, int n_layers, int hkv, int d,

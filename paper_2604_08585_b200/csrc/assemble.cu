@@ -61,12 +61,13 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
     const qcf_chunk_desc* __restrict__ chunks, int n_chunks, int n_rows /* 1 + n_ctx */,
     const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
     T* __restrict__ fv, int64_t fstride, int row_elems, int d,
-    const double* __restrict__ ctab, const double* __restrict__ stab, const int32_t* __restrict__ deltas) {
+    const double* __restrict__ ctab, const double* __restrict__ stab, const int32_t* __restrict__ deltas,
+    int layer0) {
   pdl_wait();
   pdl_trigger();
   constexpr int V = Vec16<T>::N;
   constexpr bool kBf16 = sizeof(T) == 2;
-  const int layer = blockIdx.y;
+  const int layer = layer0 + blockIdx.y;
   const int vpr = row_elems / V;
   const int half = d >> 1;
   __shared__ qcf_chunk_desc sc;
@@ -167,14 +168,13 @@ __global__ void gather_rows_kernel(const T* __restrict__ sk, const T* __restrict
 
 }  // namespace qcf
 
-extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
-                                const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
-                                int64_t fused_layer_stride, int n_layers, int hkv, int d,
-                                const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
-                                const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
+static int assemble_impl(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx, const void* bos_k,
+                         const void* bos_v, void* fused_k, void* fused_v, int64_t fused_layer_stride, int layer0,
+                         int n_layers, int hkv, int d, const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                         const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
   QCF_REQUIRE(chunks && bos_k && bos_v && fused_k && fused_v && cos_tbl && sin_tbl, QCF_EINVAL,
               "qcf_assemble: null pointer");
-  QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1, QCF_EINVAL,
+  QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1 && layer0 >= 0, QCF_EINVAL,
               "qcf_assemble: bad sizes");
   QCF_REQUIRE(d % 8 == 0, QCF_EUNSUPPORTED, "qcf_assemble: d_head must be a multiple of 8");
   QCF_REQUIRE(n_ctx < n_pos && max_delta < n_pos, QCF_ESHAPE, "qcf_assemble: RoPE table too short (%lld)",
@@ -190,15 +190,33 @@ extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int 
   if (dtype == QCF_F32)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
         (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl,
-        deltas);
+        deltas, layer0);
   else if (dtype == QCF_BF16)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1,
         (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
-        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas);
+        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas, layer0);
   else
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_assemble: bad dtype");
   QCF_LAUNCH_CHECK("qcf_assemble");
   return QCF_OK;
+}
+
+extern "C" int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                                const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                                int64_t fused_layer_stride, int n_layers, int hkv, int d,
+                                const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
+                                const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
+  return assemble_impl(chunks, n_chunks, n_ctx, bos_k, bos_v, fused_k, fused_v, fused_layer_stride, 0, n_layers,
+                       hkv, d, cos_tbl, sin_tbl, n_pos, deltas, max_delta, dtype, stream);
+}
+
+extern "C" int qcf_assemble_range(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                                  const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                                  int64_t fused_layer_stride, int layer0, int n_layers, int hkv, int d,
+                                  const double* cos_tbl, const double* sin_tbl, int64_t n_pos, int dtype,
+                                  qcf_stream_t stream) {
+  return assemble_impl(chunks, n_chunks, n_ctx, bos_k, bos_v, fused_k, fused_v, fused_layer_stride, layer0,
+                       n_layers, hkv, d, cos_tbl, sin_tbl, n_pos, nullptr, 0, dtype, stream);
 }
 
 extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,

@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import functools
 import math
+import os
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -439,7 +440,10 @@ class FusionEngine:
         self._oracle_cache: dict = {}
         # assembly || probe on two streams (see _launch); measured neutral on B200 at the
         # Llama-3-8B shape (tools/concurrency_check.py: both phases are HBM-bound), off by default
-        self.concurrent = False
+        self.concurrent = False   # True: the whole assembly may also overlap the probe (both HBM-bound)
+        self.asm_group = 4        # layers per side-stream assembly launch
+        # False: assembly on the main stream, in order (instrumented passes; QCF_PIPELINE_ASM=0)
+        self.pipeline_asm = os.environ.get("QCF_PIPELINE_ASM", "1") != "0"
         self._aux: torch.cuda.Stream | None = None
 
     # ------------------------------------------------------------------
@@ -485,6 +489,15 @@ class FusionEngine:
             arr[i].offset = row
             row += na
         return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
+
+    def _assemble_range(self, recs, n_ctx, fk, fv, desc_dev, layer0, n_layers, stream=None, layer_stride=None):
+        cfg = self.config
+        self.ex.rope.ensure(n_ctx + 2)
+        call("qcf_assemble_range", desc_dev.data_ptr(), len(recs), n_ctx, self._bos_k.data_ptr(),
+             self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(),
+             fk.stride(0) if layer_stride is None else layer_stride, layer0, n_layers,
+             cfg.n_kv_heads, cfg.d_head, self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(),
+             self.ex.rope.n_pos, self.weights.qcf_dtype, cuda_stream(stream))
 
     def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None, layer_stride=None):
         cfg = self.config
@@ -815,26 +828,60 @@ class FusionEngine:
         nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
         n_ch = len(plan.records)
         probe = plan.policy == "QCFuse" and n_sel > 0
-        # K1 (assembly, HBM-bound on the chunk pool) and K2+K3 (probe, HBM-bound on the
-        # weights) are independent: with `concurrent` the assembly runs on a forked
-        # stream and joins before scoring (graph capture records the fork/join)
-        fork = probe and self.concurrent and B * n_ch > 0
         main = stream or torch.cuda.current_stream()
-        asm_stream = main
-        if fork:
+        # K1 (assembly, HBM-bound on the chunk pool) runs on a side stream, layer range
+        # by layer range: the critical layer first (scoring reads it, overlapping the
+        # probe), the others once the recompute starts, each range joined by the
+        # recompute right before its layer -- so the copy overlaps the tensor-bound
+        # recompute instead of preceding it (graph capture records the fork/join).
+        # `concurrent`: start every range at once (overlaps the HBM-bound probe).
+        layer_ready: dict[int, torch.cuda.Event] = {}
+        pending: list[tuple[int, int]] = []
+        aux = None
+        last = None
+
+        def enqueue(rngs) -> None:
+            nonlocal last
+            for l0, nl in rngs:
+                for r in range(B):   # request r's slice of the batch table, layers [l0, l0+nl)
+                    self._assemble_range(plan.records, n_ctx, _view_rows(b.fk, r * b.R),
+                                         _view_rows(b.fv, r * b.R), _DescView(b.desc, r * nd), l0, nl, aux,
+                                         layer_stride=b.fk.stride(0))
+                e = torch.cuda.Event()
+                e.record(aux)
+                last = e
+                for l in range(l0, l0 + nl):
+                    layer_ready[l] = e
+
+        if B * n_ch > 0:
             if self._aux is None:
                 self._aux = torch.cuda.Stream(device=self.device)
+            aux = self._aux if self.pipeline_asm else main
             ev = torch.cuda.Event()
             ev.record(main)
-            self._aux.wait_event(ev)
-            asm_stream = self._aux
-        for r in range(B):   # K1: assembly into request r's slice of the batch table
-            self._assemble_into(plan.records, plan.offsets, n_ctx,
-                                _view_rows(b.fk, r * b.R), _view_rows(b.fv, r * b.R),
-                                _DescView(b.desc, r * nd), asm_stream, layer_stride=b.fk.stride(0))
-        if fork:
-            joined = torch.cuda.Event()
-            joined.record(asm_stream)
+            aux.wait_event(ev)
+            L, g = cfg.n_layers, max(1, self.asm_group)
+            first = [(c - 1, 1)] if probe else []
+            lo = 0
+            while lo < L:
+                hi = min(L, lo + g)
+                if probe and lo <= c - 1 < hi:   # split around the critical layer
+                    if lo < c - 1:
+                        pending.append((lo, c - 1 - lo))
+                    if c < hi:
+                        pending.append((c, hi - c))
+                else:
+                    pending.append((lo, hi - lo))
+                lo = hi
+            enqueue(first)
+            if self.concurrent or not probe:
+                enqueue(pending)
+                pending = []
+
+        def wait_layer(li: int) -> None:
+            e = layer_ready.pop(li, None)
+            if e is not None:
+                main.wait_event(e)
         if probe:
             for r in range(B):   # K2: probe prefix rows of request r from the chunks' anchor rows
                 call("qcf_assemble_rot", b.adesc.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k.data_ptr(),
@@ -849,8 +896,7 @@ class FusionEngine:
                          n_req=B)
             ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
                      q_only=True, q_out=b.qc[0], stream=stream, n_req=B)
-            if fork:
-                main.wait_event(joined)
+            wait_layer(c - 1)
             # K4: scoring of the whole batch (request r's keys at rows r*R+1.. of layer c)
             self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream, n_req=B,
                             k_req_stride=b.R * row_elems)
@@ -861,9 +907,17 @@ class FusionEngine:
             for r in range(B):
                 call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
                 call("qcf_iota", n_sel, 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+        if pending:   # the remaining layers' assembly starts with the recompute
+            ev = torch.cuda.Event()
+            ev.record(main)
+            aux.wait_event(ev)
+            enqueue(pending)
         m = B * b.Mr   # K6: recompute + query rows of the whole batch
         ex.embed(b.sc_rc, m, b.tok, rows=b.rc_dst, stream=stream)
-        ex.stack(b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk, b.fv, stream=stream, n_req=B)
+        ex.stack(b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk, b.fv, stream=stream, n_req=B,
+                 before_layer=wait_layer)
+        if last is not None:   # join the side stream (every range is complete by now anyway)
+            main.wait_event(last)
         ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
 
     # ------------------------------------------------------------------

@@ -163,11 +163,14 @@ class Executor:
 
     def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
               layers: range | None = None, q_store: torch.Tensor | None = None, stream=None,
-              n_req: int = 1) -> None:
+              n_req: int = 1, before_layer=None) -> None:
         """Run layers over m rows. tab_k/tab_v: [L, n_rows, Hkv, D].
-        q_store (optional) [L, m, H, D] receives each layer's rotated Q."""
+        q_store (optional) [L, m, H, D] receives each layer's rotated Q.
+        before_layer(li) (optional) runs before layer li is enqueued (stream waits)."""
         layers = range(self.cfg.n_layers) if layers is None else layers
         for li in layers:
+            if before_layer is not None:
+                before_layer(li)
             self.layer(li, sc, m, pos, dst, kmax, tab_k[li], tab_v[li],
                        q_out=q_store[li] if q_store is not None else None, stream=stream, n_req=n_req)
         self.flush(sc, m, stream)
