@@ -128,6 +128,12 @@ int qcf_add_rows(float* x, const float* delta, int64_t n, qcf_stream_t stream);
 int qcf_lm_head(const float* x, const int32_t* rows, int64_t n_rows, int d,
                 const float* g, const float* b, float eps, const float* emb,
                 int vocab, float* logits, qcf_stream_t stream);
+/* Greedy decode step on the device (model.py:433-465): t = argmax(logits[0:vocab])
+ * (ties -> lowest index, like np.argmax); log_tokens[*step] = t (if *step < log_cap);
+ * *tok = t; *pos += 1; *step += 1. Lets a CUDA graph of one decode step replay
+ * without a host round trip per token. */
+int qcf_decode_advance(const float* logits, int vocab, int32_t* tok, int32_t* pos, int32_t* step,
+                       int32_t* log_tokens, int log_cap, qcf_stream_t stream);
 /* norms[i] = mean_h ||k[i,h,:]||_2   (store.py:339-340) */
 int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dtype,
                   qcf_stream_t stream);

@@ -54,6 +54,7 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_add_layernorm": (_I, [_P, _P, _I64, _I, _P, _P, _F, _P, _I, _P]),
     "qcf_add_rows": (_I, [_P, _P, _I64, _P]),
     "qcf_lm_head": (_I, [_P, _P, _I64, _I, _P, _P, _F, _P, _I, _P, _P]),
+    "qcf_decode_advance": (_I, [_P, _I, _P, _P, _P, _P, _I, _P]),
     "qcf_key_norms": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "qcf_gemm": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),
     "qcf_gemm_simt": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I, _I, _P]),

@@ -284,6 +284,45 @@ __global__ void key_norms_kernel(const T* __restrict__ k, int64_t n, int hkv, in
   if (lane == 0) norms[row] = (float)(acc / hkv);
 }
 
+// greedy decode step on the device (model.py:433-465): next = argmax(logits) with
+// numpy's tie rule (lowest index among equal maxima), appended to log[*step];
+// tok <- next, pos += 1, step += 1 -- so a CUDA graph of one decode step can be
+// replayed max_new times without a host round trip per token
+__global__ void __launch_bounds__(256) decode_advance_kernel(const float* __restrict__ logits, int vocab,
+                                                             int32_t* __restrict__ tok, int32_t* __restrict__ pos,
+                                                             int32_t* __restrict__ step,
+                                                             int32_t* __restrict__ log_tokens, int log_cap) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  float best = -INFINITY;
+  int bi = vocab;  // no valid index yet
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = logits[i];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[warp] = best; si[warp] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    if (bi >= vocab) bi = 0;  // all NaN: np.argmax would return the first NaN's index; 0 is the stand-in
+    const int st = *step;
+    if (st < log_cap) log_tokens[st] = bi;
+    *tok = bi;
+    *pos += 1;
+    *step = st + 1;
+  }
+}
+
 }  // namespace qcf
 
 extern "C" {
@@ -378,6 +417,15 @@ int qcf_key_norms(const void* k, int64_t n, int hkv, int d, float* norms, int dt
   else
     QCF_LAUNCH("key_norms_kernel", qcf::key_norms_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)k, n, hkv, d, norms);
   QCF_LAUNCH_CHECK("qcf_key_norms");
+  return QCF_OK;
+}
+
+int qcf_decode_advance(const float* logits, int vocab, int32_t* tok, int32_t* pos, int32_t* step,
+                       int32_t* log_tokens, int log_cap, qcf_stream_t stream) {
+  QCF_REQUIRE(logits && tok && pos && step && vocab > 0 && log_cap >= 0, QCF_EINVAL, "qcf_decode_advance: bad args");
+  QCF_LAUNCH("decode_advance_kernel", qcf::decode_advance_kernel, dim3(1), dim3(256), 0, qcf::as_stream(stream), logits,
+             vocab, tok, pos, step, log_tokens, log_cap);
+  QCF_LAUNCH_CHECK("qcf_decode_advance");
   return QCF_OK;
 }
 

@@ -444,6 +444,8 @@ class FusionEngine:
         self.asm_group = 4        # layers per side-stream assembly launch
         # False: assembly on the main stream, in order (instrumented passes; QCF_PIPELINE_ASM=0)
         self.pipeline_asm = os.environ.get("QCF_PIPELINE_ASM", "1") != "0"
+        self.decode_graph = True  # greedy decode as a replayed CUDA graph (False: eager loop)
+        self._decode_graphs: dict = {}
         self._aux: torch.cuda.Stream | None = None
 
     # ------------------------------------------------------------------
@@ -1129,6 +1131,8 @@ class FusionEngine:
     def _decode(self, fk, fv, next_pos: int, first_logits: np.ndarray, max_new: int) -> list[int]:
         if max_new < 1:
             raise ValueError("max_new must be >= 1")
+        if self.decode_graph:
+            return self._decode_graph(fk, fv, next_pos, first_logits, max_new)
         out, logits = [], first_logits
         dev = self.device
         tok = torch.empty(1, dtype=torch.int32, device=dev)
@@ -1149,6 +1153,71 @@ class FusionEngine:
             self.ex.lm_head(sc, zero, lg)
             logits = lg[0].cpu().numpy()
             next_pos += 1
+        return out
+
+    def _decode_graph(self, fk, fv, next_pos: int, first_logits: np.ndarray, max_new: int) -> list[int]:
+        """The same greedy decode with the argmax on the device (`qcf_decode_advance`:
+        ties -> lowest index, like np.argmax) and one decode step captured as a CUDA
+        graph, replayed max_new - 1 times with no host round trip per token; the
+        tokens after the first EOS are discarded (their KV rows land in the table's
+        spare rows, as the eager loop's would not)."""
+        t0 = int(np.argmax(first_logits))
+        if t0 == EOS_ID or max_new == 1:
+            return [t0]
+        n = max_new - 1
+        dev, V = self.device, self.config.vocab_size
+        self.ex.rope.ensure(next_pos + n + 2)
+        # one captured step per (table, token budget): the graph reads tok / pos /
+        # step from device buffers, so later calls on the same table only reset them
+        rope = self.ex.rope   # (a grown RoPE table moves: part of the key)
+        key = (fk.data_ptr(), fv.data_ptr(), tuple(fk.shape), n, rope.cos.data_ptr(), rope.cs32.data_ptr())
+        st = self._decode_graphs.get(key)
+        s = torch.cuda.current_stream()
+        if st is None:
+            st = {"tok": torch.zeros(1, dtype=torch.int32, device=dev),
+                  "pos": torch.zeros(1, dtype=torch.int32, device=dev),
+                  "step": torch.zeros(1, dtype=torch.int32, device=dev),
+                  "log": torch.zeros(n, dtype=torch.int32, device=dev),
+                  "zero": torch.zeros(1, dtype=torch.int32, device=dev),
+                  "lg": torch.empty((1, V), dtype=torch.float32, device=dev),
+                  "sc": self.ex.scratch(1, key=("decode", key)), "graph": None}
+        tok, pos, step, log, lg = st["tok"], st["pos"], st["step"], st["log"], st["lg"]
+        tok.fill_(t0)
+        pos.fill_(next_pos)
+        step.zero_()
+        log.fill_(-1)
+
+        def one_step(stream) -> None:
+            self.ex.embed(st["sc"], 1, tok, stream=stream)
+            self.ex.stack(st["sc"], 1, pos, pos, pos, fk, fv, stream=stream)
+            self.ex.lm_head(st["sc"], st["zero"], lg, stream=stream)
+            call("qcf_decode_advance", lg.data_ptr(), V, tok.data_ptr(), pos.data_ptr(), step.data_ptr(),
+                 log.data_ptr(), n, cuda_stream(stream))
+
+        if st["graph"] is None:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(s)
+            with torch.cuda.stream(side):
+                one_step(side)                  # step 1, eagerly (lazy attributes, workspaces)
+            if n > 1:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    one_step(side)
+                st["graph"] = g
+            s.wait_stream(side)
+            reps = n - 1
+            if len(self._decode_graphs) >= 4:
+                self._decode_graphs.clear()
+            self._decode_graphs[key] = st
+        else:
+            reps = n
+        for _ in range(reps):
+            st["graph"].replay()
+        out = [t0]
+        for t in log.cpu().tolist():
+            out.append(int(t))
+            if t == EOS_ID:
+                break
         return out
 
     # ------------------------------------------------------------------

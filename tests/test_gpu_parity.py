@@ -637,3 +637,22 @@ def test_long_context_16k_against_oracle(tmp_path, dtype):
         err = np.abs(logits - ref.first_logits).max() / np.abs(ref.first_logits).max()
         print(f"16k bf16: overlap {overlap:.3f} rel logit err {err:.3e}")
         assert overlap >= 0.9 and err < 5e-2
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_graph_decode_equals_eager_decode(golden_dir, tmp_path, dtype):
+    """Greedy decode as a replayed CUDA graph with the argmax on the device
+    (qcf_decode_advance, np.argmax's tie rule) gives the eager loop's tokens
+    (model.py:433-465); f32 also equals the reference's golden answer."""
+    z, oc, ow, chunks, w, store, ids, eng = golden_setup(golden_dir, "small_case0", dtype, tmp_path)
+    outs = []
+    for graph in (True, False, True):
+        eng.decode_graph = graph
+        res = eng.run("QCFuse", float(z["ratio"]), ids, z["query"].tolist(), max_new=12)
+        outs.append(res.answer_tokens)
+    eng.decode_graph = True
+    assert outs[0] == outs[1] == outs[2]
+    assert 1 <= len(outs[0]) <= 12
+    if dtype == "f32":
+        n = min(len(outs[0]), z["answer"].size)
+        assert outs[0][:n] == z["answer"].tolist()[:n]
