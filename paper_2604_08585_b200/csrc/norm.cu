@@ -44,6 +44,27 @@ __device__ __forceinline__ void row_stats(const float* __restrict__ xr, int d, i
 // block reductions for mean and (x-mean)^2.
 constexpr int LN_THREADS = 256, LN_V4 = 8;  // d <= 256 * 4 * 8 = 8192
 
+// block_sum_256 of R values at once (each value reduced exactly as block_sum_256 does)
+template <int R>
+__device__ __forceinline__ void block_sum_256_rows(float (&v)[R], float (*red)[LN_THREADS / 32]) {
+#pragma unroll
+  for (int q = 0; q < R; ++q) v[q] = warp_sum(v[q]);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) red[q][w] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < LN_THREADS / 32; ++i) t += red[q][i];
+    v[q] = t;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ float block_sum_256(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5;
@@ -76,75 +97,116 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a,
 // gain/bias only at the store (L1/L2 resident), so registers stay low and
 // several rows per SM keep their loads in flight (the kernel is HBM-bound:
 // 4+4 B read, 4+2 B written per element).
-template <typename T, int V>
+template <typename T, int V, int R>
 __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                                                int64_t m, int d, const float* __restrict__ g,
                                                                const float* __restrict__ b, float eps,
                                                                T* __restrict__ out) {
+  // R rows per CTA: all R rows' loads are in flight together and the two block
+  // reductions are shared by the R rows (per-row arithmetic unchanged)
   pdl_wait();
   pdl_trigger();
-  __shared__ float red[LN_THREADS / 32];
-  const int64_t row = blockIdx.x;
-  float4* xr = reinterpret_cast<float4*>(x + row * d);
-  const float4* dr = delta ? reinterpret_cast<const float4*>(delta + row * d) : nullptr;
+  __shared__ float red[R][LN_THREADS / 32];
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
   const int n4 = d >> 2;
-  float4 v[V], t[V];
+  float4 v[R][V], t[R][V];
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int e = threadIdx.x + i * LN_THREADS;
-    v[i] = e < n4 ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
-    t[i] = (dr && e < n4) ? __ldcs(dr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  if (dr) {
+  for (int q = 0; q < R; ++q) {
+    const int64_t row = (int64_t)blockIdx.x * R + q;
+    const bool ok = row < m;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+    const float4* dr = delta ? reinterpret_cast<const float4*>(delta + row * d) : nullptr;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int e = threadIdx.x + i * LN_THREADS;
-      v[i].x += t[i].x; v[i].y += t[i].y; v[i].z += t[i].z; v[i].w += t[i].w;
-      if (e < n4) xr[e] = v[i];
+      v[q][i] = (ok && e < n4) ? xr[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+      t[q][i] = (ok && dr && e < n4) ? __ldcs(dr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  float s = 0.f;
+  float s[R];
 #pragma unroll
-  for (int i = 0; i < V; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  const float mean = block_sum_256(s, red) / d;
-  float q = 0.f;
+  for (int q = 0; q < R; ++q) {
+    const int64_t row = (int64_t)blockIdx.x * R + q;
+    if (delta) {
+      float4* xr = reinterpret_cast<float4*>(x + row * d);
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    if (threadIdx.x + i * LN_THREADS < n4) {
-      const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
-      q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+      for (int i = 0; i < V; ++i) {
+        const int e = threadIdx.x + i * LN_THREADS;
+        v[q][i].x += t[q][i].x; v[q][i].y += t[q][i].y; v[q][i].z += t[q][i].z; v[q][i].w += t[q][i].w;
+        if (row < m && e < n4) xr[e] = v[q][i];
+      }
     }
-  }
-  const float var = block_sum_256(q, red) / d;
-  const float sd = sqrtf(var + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b  (model.py:308)
-  T* orow = out + row * d;
+    s[q] = 0.f;
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const int e = threadIdx.x + i * LN_THREADS;
-    if (e < n4) {
-      const float4 gv = g4[e], bv = b4[e];
-      store4<T>(orow + 4 * e, ((v[i].x - mean) / sd) * gv.x + bv.x, ((v[i].y - mean) / sd) * gv.y + bv.y,
-                ((v[i].z - mean) / sd) * gv.z + bv.z, ((v[i].w - mean) / sd) * gv.w + bv.w);
+    for (int i = 0; i < V; ++i) s[q] += (v[q][i].x + v[q][i].y) + (v[q][i].z + v[q][i].w);
+  }
+  float mean[R];
+  block_sum_256_rows<R>(s, red);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    mean[q] = s[q] / d;
+    float qs = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      if (threadIdx.x + i * LN_THREADS < n4) {
+        const float a0 = v[q][i].x - mean[q], a1 = v[q][i].y - mean[q], a2 = v[q][i].z - mean[q],
+                    a3 = v[q][i].w - mean[q];
+        qs += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+      }
+    }
+    s[q] = qs;
+  }
+  block_sum_256_rows<R>(s, red);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int64_t row = (int64_t)blockIdx.x * R + q;
+    if (row >= m) break;
+    const float var = s[q] / d;
+    const float sd = sqrtf(var + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b  (model.py:308)
+    T* orow = out + row * d;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int e = threadIdx.x + i * LN_THREADS;
+      if (e < n4) {
+        const float4 gv = g4[e], bv = b4[e];
+        const float mu = mean[q];
+        store4<T>(orow + 4 * e, ((v[q][i].x - mu) / sd) * gv.x + bv.x, ((v[q][i].y - mu) / sd) * gv.y + bv.y,
+                  ((v[q][i].z - mu) / sd) * gv.z + bv.z, ((v[q][i].w - mu) / sd) * gv.w + bv.w);
+      }
     }
   }
 }
 
+// rows per CTA: 2 for short row lists (one request's 800 rows: 18.4 -> 16.4 us, the
+// probe's rows), 1 for long ones (6400 rows: 63.5 vs 65.6 us; tools/ln_bench.py);
+// QCF_LN_ROWS=1/2 forces it (measurement)
+static int g_ln_rows = -1;
+template <typename T, int R>
+static int launch_ln_rows(float* x, const float* delta, int64_t m, int d, const float* g, const float* b, float eps,
+                          T* out, cudaStream_t s) {
+  const int n4 = d / 4;
+  const unsigned grid = (unsigned)((m + R - 1) / R);
+  if (n4 <= LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 1, R>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else if (n4 <= 2 * LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 2, R>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else if (n4 <= 4 * LN_THREADS)
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 4, R>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  else
+    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, LN_V4, 1>), dim3((unsigned)m), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
+  return QCF_OK;
+}
 template <typename T>
 static int launch_ln_vec(float* x, const float* delta, int64_t m, int d, const float* g, const float* b, float eps,
                          T* out, cudaStream_t s) {
-  const int n4 = d / 4;
-  const unsigned grid = (unsigned)m;
-  if (n4 <= LN_THREADS)
-    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 1>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
-  else if (n4 <= 2 * LN_THREADS)
-    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 2>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
-  else if (n4 <= 4 * LN_THREADS)
-    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, 4>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
-  else
-    QCF_LAUNCH("layernorm_kernel", (layernorm_kernel<T, LN_V4>), dim3(grid), dim3(LN_THREADS), 0, s, x, delta, m, d, g, b, eps, out);
-  return QCF_OK;
+  if (g_ln_rows < 0) {
+    const char* e = getenv("QCF_LN_ROWS");
+    g_ln_rows = e ? ((atoi(e) == 2) ? 2 : 1) : 0;  // 0 = by row count
+  }
+  const bool two = g_ln_rows == 2 || (g_ln_rows == 0 && m <= 2048);
+  if (two && d / 4 <= 4 * LN_THREADS) return launch_ln_rows<T, 2>(x, delta, m, d, g, b, eps, out, s);
+  return launch_ln_rows<T, 1>(x, delta, m, d, g, b, eps, out, s);
 }
 
 // generic fallback (d % 4 != 0): one CTA per row, strided scalar loop
