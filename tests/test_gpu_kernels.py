@@ -645,3 +645,42 @@ def test_fused_qkv_rope_swapped(L, m, heads, hkv):
         L.call("qcf_set_gemm_plan", 0)
     for x, y in zip(res[0], res[1]):   # same MMA k order and the same row epilogue behind the transpose
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_assemble_range_equals_full_assembly(golden_dir, tmp_path, dtype):
+    """qcf_assemble_range over layer ranges (the side-stream schedule: critical
+    layer first, then ranges) writes exactly what one all-layer qcf_assemble writes."""
+    from tests.gpu_util import golden_setup
+    z, oc, ow, chunks, w, store, ids, eng = golden_setup(golden_dir, "small_case1", dtype, tmp_path)
+    full = eng.assemble_context(ids)
+    recs, offs, n_ctx = eng._records(ids)
+    desc = eng._desc_bytes(recs, offs).to(eng.device)
+    fk = torch.full_like(full.k, 7.0)
+    fv = torch.full_like(full.v, 7.0)
+    L = oc.n_layers
+    for l0, nl in [(L // 2, 1), (0, L // 2)] + ([(L // 2 + 1, L - L // 2 - 1)] if L // 2 + 1 < L else []):
+        eng._assemble_range(recs, n_ctx, fk, fv, desc, l0, nl)
+    torch.cuda.synchronize()
+    rows = 1 + n_ctx
+    assert torch.equal(fk[:, :rows], full.k[:, :rows]) and torch.equal(fv[:, :rows], full.v[:, :rows])
+
+
+def test_decode_advance_argmax_tie_rule(L):
+    """qcf_decode_advance: np.argmax semantics (lowest index among equal maxima),
+    token log, position and step advance."""
+    V = 259
+    lg = torch.randn(1, V, device="cuda")
+    lg[0, 17] = 5.0
+    lg[0, 200] = 5.0   # tie: 17 wins
+    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pos = torch.full((1,), 41, dtype=torch.int32, device="cuda")
+    step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    log = torch.full((4,), -1, dtype=torch.int32, device="cuda")
+    L.call("qcf_decode_advance", p(lg), V, p(tok), p(pos), p(step), p(log), 4, S())
+    lg[0, 3] = 9.0
+    L.call("qcf_decode_advance", p(lg), V, p(tok), p(pos), p(step), p(log), 4, S())
+    torch.cuda.synchronize()
+    assert log.tolist() == [17, 3, -1, -1]
+    assert int(tok.item()) == 3 and int(pos.item()) == 43 and int(step.item()) == 2
+    assert int(np.argmax(lg[0].cpu().numpy())) == 3
