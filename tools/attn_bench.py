@@ -62,6 +62,11 @@ print(json.dumps({"shape": "full prefill causal", "m": 5152, "keys": 5153, **ben
 km = (torch.arange(32, dtype=torch.int32) + 5121)[None].cuda().contiguous()
 print(json.dumps({"shape": "query rows only (FullReuse)", "m": 32, "keys": 5153, **bench(32, 5153, 32, 32, 1, km)}),
       flush=True)
+km = (torch.arange(32, dtype=torch.int32) + 261)[None].cuda().contiguous()   # probe: q rows over the anchor prefix
+print(json.dumps({"shape": "probe rows (anchor prefix)", "m": 32, "keys": 293, **bench(32, 293, 32, 32, 1, km)}),
+      flush=True)
+km = (torch.arange(32, dtype=torch.int32) + 261)[None].repeat(8, 1).cuda().contiguous()
+print(json.dumps({"shape": "probe rows batch8", "m": 32, "keys": 293, **bench(32, 293, 32, 32, 8, km)}), flush=True)
 km = sel_kmax(32768, 4916, 32, 1)
 print(json.dumps({"shape": "mistral 32k single", "m": 4948, "keys": 32801, **bench(4948, 32801, 32, 8, 1, km, it=5)}),
       flush=True)
