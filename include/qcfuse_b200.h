@@ -146,8 +146,10 @@ int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb,
              int out_dtype, qcf_stream_t stream);
 /* Same contract with a caller-owned workspace (qcf_gemm_workspace() bytes,
  * ZERO-FILLED once before first use; the kernels leave its flag words zeroed):
- *  - skinny M (the probe's q rows) splits K across CTAs so the weights stream
- *    at HBM rate; partials are summed in a fixed order (deterministic);
+ *  - skinny M (<= 256, the probe's q rows) splits K across the CTAs of a thread-
+ *    block cluster so the weights stream at HBM rate; the fp32 partials are summed
+ *    in rank order through distributed shared memory (deterministic, no workspace
+ *    needed; the older global-memory split-K with a workspace remains the fallback);
  *  - opt-in (qcf_set_gemm_plan +8) stream-K for the 2-CTA kernel: equal k-block
  *    ranges per CTA pair, split tiles fixed up through the workspace in
  *    cluster order (deterministic).
@@ -173,9 +175,10 @@ int qcf_rope_qkv_scatter(const float* qkv, int64_t m, int h, int hkv, int d,
 /* Fused QKV projection + RoPE + KV scatter (bf16, tcgen05): the projection
  * a[M,K] . w[(H+2Hkv)D, K]^T never touches HBM in fp32; its epilogue rotates
  * Q/K at pos[i] and writes q_out[i], k_tab[dst_rows[i]], v_tab[dst_rows[i]].
- * M <= 32 (the probe's query rows) with a workspace (qcf_gemm_workspace, zeroed):
- * split-K weight streaming, the rotation + scatter applied in the split-K
- * reduction. Returns QCF_EUNSUPPORTED when d % 32 != 0 (callers then use
+ * M <= 256 (the probe's query rows): cluster split-K weight streaming with the
+ * rotation + scatter applied in the distributed-shared-memory reduction; other M:
+ * the 2-CTA (normal or swapped) tiles, rotation in the epilogue (bit-identical
+ * across the two orientations). Returns QCF_EUNSUPPORTED when d % 32 != 0 (callers then use
  * qcf_gemm + qcf_rope_qkv_scatter). fusion.py:470-478.
  * cs_tbl: float32 [n_pos][d/2][2] = (float(cos), float(sin)) of the float64
  * angle table (the bf16 epilogue rotates in fp32; 16-byte aligned). */

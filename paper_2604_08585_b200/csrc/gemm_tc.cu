@@ -769,7 +769,7 @@ __device__ __forceinline__ void epi_store4(void* __restrict__ C, int64_t ldc, in
 
 // deterministic split-K reduction: C = epi(sum_s partial[s]) in split order.
 // Epilogues: store / ReLU / residual add (f32 or bf16 C) and the fused QKV
-// RoPE + KV scatter (the probe's M <= 32 projection: the rotation happens here,
+// RoPE + KV scatter (the global-memory split-K fallback of the probe's projection: the rotation happens here,
 // no separate rope kernel).
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M, int N,
                                      void* __restrict__ C, int64_t ldc, const EpiArgs ea) {

@@ -138,8 +138,8 @@ class Executor:
         self._norm(sc, m, lw.ln1_g, lw.ln1_b, s)
         qdst = q_out if q_out is not None else sc.q
         if self.fused_qkv:
-            # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue (M <= 32:
-            # split-K weight streaming with the rotation applied in the split-K reduction)
+            # bf16: projection + RoPE + KV scatter in one tcgen05 kernel epilogue (M <= 256:
+            # cluster split-K weight streaming with the rotation applied in the reduction)
             call("qcf_gemm_qkv_rope", sc.a.data_ptr(), d, lw.wqkv.data_ptr(), d, self.w.b_layout, m, d, H, Hkv, D,
                  pos.data_ptr(), dst.data_ptr(), self.rope.cs32.data_ptr(),
                  self.rope.n_pos, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(), sc.ws.data_ptr(), sc.ws.numel(), s)
