@@ -38,7 +38,8 @@ constexpr int AT_TILE_BYTES = AT_BM * AT_D * 2;  // 32 KB: two 16 KB SW128 atoms
 // keep a V wait from delaying the next K load
 constexpr int AT_KS = 3;
 constexpr int AT_VS = 2;
-constexpr int AT_SMEM = AT_TILE_BYTES * (1 + AT_KS + AT_VS) + 1024 + 256;  // Q, K[KS], V[VS] (P lives in TMEM)
+constexpr int AT_ONES_BYTES = 16 * AT_BN * 2;  // bf16 ones, 16 x 128 K-major: B operand of the row-sum MMA
+constexpr int AT_SMEM = AT_TILE_BYTES * (1 + AT_KS + AT_VS) + AT_ONES_BYTES + 1024 + 256;  // Q, K, V, ones
 
 // MN-major SW128 descriptor (B = V: N = head dim contiguous, K = keys):
 // 8-key groups 1024 B apart (SBO), 64-column atoms 16 KB apart (LBO).
@@ -152,6 +153,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&o)[32
       "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
 }
 
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return r;
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -201,7 +207,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   uint8_t* sQ = smem;
   uint8_t* sK = smem + AT_TILE_BYTES;                  // [AT_KS]
   uint8_t* sV = smem + (1 + AT_KS) * AT_TILE_BYTES;    // [AT_VS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + AT_KS + AT_VS) * AT_TILE_BYTES);
+  uint8_t* sOnes = smem + (1 + AT_KS + AT_VS) * AT_TILE_BYTES;  // 16 x 128 bf16 ones (K-major, any swizzle)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + AT_ONES_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* s_full = bars + 1;     // [2]
   uint64_t* s_free = bars + 3;     // [2]
@@ -253,6 +260,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     fence_barrier_init();
     s_kend = 0;
   }
+  if (threadIdx.x < AT_ONES_BYTES / 16)   // ones for the row-sum MMA, then visible to the tensor core
+    reinterpret_cast<uint4*>(sOnes)[threadIdx.x] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   __syncthreads();
   pdl_wait();  // barrier init + TMEM alloc overlap the previous kernel's tail
@@ -279,7 +289,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
-  const uint32_t tS0 = tmem, tO = tmem + 256, tP0 = tmem + 384;  // S[2] | O | P[2] (64 cols each)
+  // S[2] | O | row sums: P_j is written over its own S buffer (each softmax warp over the
+  // S columns it alone read), and P_j . 1 (16 equal columns at tOS) gives the row sums on
+  // the tensor core instead of 16 FADD2 per thread and key tile (traced: -170 cycles/tile)
+  const uint32_t tS0 = tmem, tO = tmem + 256, tOS = tmem + 384;
 #ifdef QCF_ATTN_TRACE
   if (threadIdx.x == 0) { QCF_TRACE(2, gtimer()); QCF_TRACE(7, n_tiles); }
 #endif
@@ -310,6 +323,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     {  // ---------------- MMA issuer (whole warp converged; one elected lane issues)
       constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A, K-major B
       constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
+      constexpr uint32_t idesc_l = idesc_bf16_f32(AT_BM, 16);                     // B = ones, K-major
       mbar_wait(q_full, 0);
       tc_fence_after();
       auto issue_pv = [&](int jj) {
@@ -326,8 +340,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_BN / 16; ++kk) {   // A = P_jj straight from TMEM (packed bf16)
+          // keys 16kk..16kk+15 were written by softmax warp cg = kk/2 at the start of its S columns
+          const uint32_t pa = tS0 + st * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
           const uint64_t b = umma_desc_mn_sw128(sV + vs * AT_TILE_BYTES + kk * 16 * 128);
-          mma_bf16_ts_e(tO, tP0 + st * 64 + kk * 8, b, idesc_o, (jj | kk) != 0);
+          mma_bf16_ts_e(tO, pa, b, idesc_o, (jj | kk) != 0);
+          const uint64_t bl = umma_desc_k_sw128(sOnes + (kk >> 2) * (AT_ONES_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+          mma_bf16_ts_e(tOS, pa, bl, idesc_l, (jj | kk) != 0);
         }
 #ifdef QCF_ATTN_TRACE
         QCF_TRACE2(jj, 2);
@@ -370,7 +388,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
     const int my_kmax = (row >= 0 && row < M) ? kmax[row] : -1;
     const uint32_t lane_off = (uint32_t)(g * 32) << 16;
     const int bar_id = 1 + g;             // named barrier of the 4 warps sharing these rows
-    float m_ref = -INFINITY, l = 0.f;
+    float m_ref = -INFINITY;
     for (int j = 0; j < n_tiles; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -410,7 +428,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
       if (need) {
         alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
         m_ref = tmax;
-        l *= alpha;
       }
       // P buffer j&1 was read by P_{j-2}.V_{j-2}; the O rescale needs P_{j-1}.V_{j-1}
       if (j >= 2) {
@@ -436,18 +453,29 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
             "r"(o[9]), "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]),
             "r"(o[17]), "r"(o[18]), "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]),
             "r"(o[25]), "r"(o[26]), "r"(o[27]), "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31]));
+        if (cg == 0) {  // the row sums (16 equal columns) scale with O
+          uint32_t ls[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(ls[0]), "=r"(ls[1]), "=r"(ls[2]), "=r"(ls[3]), "=r"(ls[4]), "=r"(ls[5]), "=r"(ls[6]),
+                "=r"(ls[7]), "=r"(ls[8]), "=r"(ls[9]), "=r"(ls[10]), "=r"(ls[11]), "=r"(ls[12]), "=r"(ls[13]),
+                "=r"(ls[14]), "=r"(ls[15])
+              : "r"(tOS + lane_off));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ls[i] = __float_as_uint(__uint_as_float(ls[i]) * alpha);
+          tmem_st16(tOS + lane_off, ls);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       // P = exp2(s*scale - m_ref) -> packed bf16 for keys 32cg..32cg+31 (TMEM P buffer j&1)
       uint32_t pk[16];
-      float psum = 0.f;
       if (none_vis) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = 0u;
       } else {
         if (all_vis) {  // packed f32x2 math, part of the exp2 on the FMA pipe
           const uint64_t sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_ref, -m_ref);
-          uint64_t l2 = f2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
@@ -459,14 +487,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
               f2_split(x2, a, b);
               p2 = f2(ex2_approx(a), ex2_approx(b));
             }
-            l2 = fadd2(l2, p2);
             float p0, p1;
             f2_split(p2, p0, p1);
             pk[i >> 1] = bf16x2_bits(p0, p1);
           }
-          float la, lb;
-          f2_split(l2, la, lb);
-          psum = la + lb;
         } else {
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -474,16 +498,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
             float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
             p0 = (i <= lim) ? p0 : 0.f;
             p1 = (i + 1 <= lim) ? p1 : 0.f;
-            psum += p0 + p1;
             pk[i >> 1] = bf16x2_bits(p0, p1);
           }
         }
       }
-      l += psum;
 #ifdef QCF_ATTN_TRACE
       if (threadIdx.x == 64) QCF_TRACE2(j, 3);
 #endif
-      tmem_st16(tP0 + (j & 1) * 64 + cg * 16 + lane_off, pk);  // keys 32cg.. -> P cols 16cg..
+      tmem_st16(tS0 + sb * 128 + cg * 32 + lane_off, pk);  // keys 32cg.. -> the first 16 of this warp's S cols
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -499,12 +521,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
 #ifdef QCF_ATTN_TRACE
     if (threadIdx.x == 64) QCF_TRACE(4, gtimer());
 #endif
-    named_bar(bar_id, 128);
-    red[0][cg][r] = l;
-    named_bar(bar_id, 128);
-    const float lt = (red[0][0][r] + red[0][1][r]) + (red[0][2][r] + red[0][3][r]);
     mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
+    const float lt = __uint_as_float(tmem_ld1(tOS + lane_off));   // row sum = (P . 1)
+    tmem_ld_wait();
     const float inv = lt > 0.f ? 1.f / lt : 0.f;
     uint32_t o[32];
     tmem_ld32(tO + cg * 32 + lane_off, o);
