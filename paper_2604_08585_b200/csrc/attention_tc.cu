@@ -70,6 +70,12 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // which column pairs take the FMA-pipe exp2: spread through the loop (pair p with
 // (9p mod 16) < A2_EMU16) so the MUFU and FMA pipes are fed interleaved, not in runs
 #define A2_EMU(p) ((((p) * 9) & 15) < A2_EMU16)
+// the single-tile kernel, with its row sums on the tensor core, has less FMA-pipe work:
+// 5 of 16 measured best there (3..5 within 1%, 7 +1.2%, 9 +2.6%)
+#ifndef A1_EMU16
+#define A1_EMU16 5
+#endif
+#define A1_EMU(p) ((((p) * 9) & 15) < A1_EMU16)
 // ---- softmax arithmetic helpers (packed f32x2 FFMA2/FADD2, 3-input max, exp2
 // emulated on the FMA pipe for part of the columns: B200's MUFU ex2 rate (16/clk/SM)
 // would otherwise bound the softmax below the tensor core's rate)
@@ -480,7 +486,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
           for (int i = 0; i < 32; i += 2) {
             const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
             uint64_t p2;
-            if (A2_EMU(i >> 1)) {
+            if (A1_EMU(i >> 1)) {
               p2 = exp2_poly2(x2);
             } else {
               float a, b;
