@@ -79,15 +79,8 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// D[tmem] (+)= A[smem] . B[smem]^T   (kind::f16, bf16 in, f32 accumulate)
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
+// D[tmem] (+)= A[smem] . B[smem]^T (kind::f16, bf16 in, f32 accumulate); commit = arrive
+// on `bar` once every previously issued tcgen05.mma of the issuing thread completes.
 // Warp-converged issue: the whole warp runs the MMA loop (descriptors are then
 // warp-uniform and stay in uniform registers) and elect.sync picks the one lane
 // that issues. Issuing from a lone lane (`if (lane == 0)`) made ptxas wrap every
@@ -108,11 +101,6 @@ __device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
-}
-// arrive on `bar` once every previously issued tcgen05.mma of this thread completes
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
 }
 
 // 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread (thread i = lane i)
@@ -202,15 +190,8 @@ __device__ __forceinline__ void tmem_alloc2(uint32_t* smem_result, uint32_t ncol
 __device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
-__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-// warp-converged, elected variants of the pair MMA / commit (see mma_bf16_e)
+// 2-CTA (cta_group::2) MMA and commit, warp-converged and elected like mma_bf16_e; the
+// commit arrives on the barrier at the same offset in both CTAs of the pair
 __device__ __forceinline__ void mma_bf16_pair_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                 uint32_t accumulate) {
   asm volatile(
@@ -225,14 +206,6 @@ __device__ __forceinline__ void mma_commit_pair_e(uint64_t* bar) {
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)0x3)
-      : "memory");
-}
-// commit the pair's MMAs to the barrier at the same offset in both CTAs
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
       "h"((uint16_t)0x3)
       : "memory");

@@ -13,6 +13,17 @@
 
 using namespace qcf::sm100;
 
+// lone-lane (non-elected) issue, as measured here
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(a), "l"(b), "r"(idesc),
+      "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -61,10 +72,10 @@ __global__ void __launch_bounds__(256, 1) kern(int mode, int n, int noise, long 
       const uint32_t id2 = idesc_bf16_f32(128, 128), id3 = id2 | (1u << 16);
       const uint64_t a1 = a0 + 2, a2 = a0 + 4, a3 = a0 + 6, b1 = b0 + 2, b2 = b0 + 4, b3 = b0 + 6;
       for (int i = 0; i < n; i += 16) {
-        mma_bf16(tmem, a0, b0, id2, 1u); mma_bf16(tmem, a1, b1, id2, 1u);
-        mma_bf16(tmem, a2, b2, id2, 1u); mma_bf16(tmem, a3, b3, id2, 1u);
-        mma_bf16(tmem, a0, b0, id2, 1u); mma_bf16(tmem, a1, b1, id2, 1u);
-        mma_bf16(tmem, a2, b2, id2, 1u); mma_bf16(tmem, a3, b3, id2, 1u);
+        mma_ss(tmem, a0, b0, id2, 1u); mma_ss(tmem, a1, b1, id2, 1u);
+        mma_ss(tmem, a2, b2, id2, 1u); mma_ss(tmem, a3, b3, id2, 1u);
+        mma_ss(tmem, a0, b0, id2, 1u); mma_ss(tmem, a1, b1, id2, 1u);
+        mma_ss(tmem, a2, b2, id2, 1u); mma_ss(tmem, a3, b3, id2, 1u);
         mma_ts(tmem + 128, tmem + 256, b0, id3, 1u); mma_ts(tmem + 128, tmem + 264, b1, id3, 1u);
         mma_ts(tmem + 128, tmem + 272, b2, id3, 1u); mma_ts(tmem + 128, tmem + 280, b3, id3, 1u);
         mma_ts(tmem + 128, tmem + 288, b0, id3, 1u); mma_ts(tmem + 128, tmem + 296, b1, id3, 1u);
@@ -74,14 +85,14 @@ __global__ void __launch_bounds__(256, 1) kern(int mode, int n, int noise, long 
       const uint32_t id2 = idesc_bf16_f32(128, mode == 7 ? 256 : 128);
       const uint64_t a1 = a0 + 2, a2 = a0 + 4, a3 = a0 + 6, b1 = b0 + 2, b2 = b0 + 4, b3 = b0 + 6;
       for (int i = 0; i < n; i += 8) {
-        mma_bf16(tmem, a0, b0, id2, 1u);
-        mma_bf16(tmem, a1, b1, id2, 1u);
-        mma_bf16(tmem, a2, b2, id2, 1u);
-        mma_bf16(tmem, a3, b3, id2, 1u);
-        mma_bf16(tmem, a0, b0, id2, 1u);
-        mma_bf16(tmem, a1, b1, id2, 1u);
-        mma_bf16(tmem, a2, b2, id2, 1u);
-        mma_bf16(tmem, a3, b3, id2, 1u);
+        mma_ss(tmem, a0, b0, id2, 1u);
+        mma_ss(tmem, a1, b1, id2, 1u);
+        mma_ss(tmem, a2, b2, id2, 1u);
+        mma_ss(tmem, a3, b3, id2, 1u);
+        mma_ss(tmem, a0, b0, id2, 1u);
+        mma_ss(tmem, a1, b1, id2, 1u);
+        mma_ss(tmem, a2, b2, id2, 1u);
+        mma_ss(tmem, a3, b3, id2, 1u);
       }
     } else
     for (int i = 0; i < n; ++i) {
@@ -89,16 +100,16 @@ __global__ void __launch_bounds__(256, 1) kern(int mode, int n, int noise, long 
       if (mode == 1)
         mma_ts(tmem, tmem + 256 + kk * 8, b0 + (uint64_t)(kk * 2), idesc, 1u);
       else if (mode == 3)  // two independent accumulators, alternating
-        mma_bf16(tmem + (i & 1) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+        mma_ss(tmem + (i & 1) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
       else if (mode == 4)  // four independent accumulators, round-robin
-        mma_bf16(tmem + (i & 3) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+        mma_ss(tmem + (i & 3) * 128, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
       else if (mode == 5)  // N = 64
-        mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+        mma_ss(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
       else
-        mma_bf16(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
+        mma_ss(tmem, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, 1u);
     }
     long long t1 = clock64();
-    mma_commit(bar);
+    commit(bar);
     mbar_wait(bar, 0);
     long long t2 = clock64();
     out[0] = t1 - t0;
