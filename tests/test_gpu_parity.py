@@ -656,3 +656,21 @@ def test_graph_decode_equals_eager_decode(golden_dir, tmp_path, dtype):
     if dtype == "f32":
         n = min(len(outs[0]), z["answer"].size)
         assert outs[0][:n] == z["answer"].tolist()[:n]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_side_stream_assembly_matches_serial(golden_dir, tmp_path, dtype):
+    """The assembly on a side stream by layer ranges (joined layer by layer by the
+    recompute; graph-captured fork/join) gives bit-identical logits and selections
+    to the serial main-stream assembly, eager and graph replay."""
+    z, oc, ow, chunks, w, store, ids, eng = golden_setup(golden_dir, "small_case0", dtype, tmp_path)
+    out = []
+    for pipe, graph in ((False, False), (True, False), (True, True), (False, True)):
+        eng.pipeline_asm = pipe
+        eng._bufs.clear()
+        plan, b = eng.prefill("QCFuse", float(z["ratio"]), ids, z["query"].tolist(), use_graph=graph)
+        torch.cuda.synchronize()
+        out.append((b.logits[0].cpu().clone(), b.rc_pos[:plan.n_sel].cpu().clone()))
+    eng.pipeline_asm = True
+    for lg, sel in out[1:]:
+        assert torch.equal(lg, out[0][0]) and torch.equal(sel, out[0][1])
