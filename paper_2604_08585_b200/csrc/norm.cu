@@ -178,9 +178,9 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict
   }
 }
 
-// rows per CTA: 2 for short row lists (one request's 800 rows: 18.4 -> 16.4 us, the
-// probe's rows), 1 for long ones (6400 rows: 63.5 vs 65.6 us; tools/ln_bench.py);
-// QCF_LN_ROWS=1/2 forces it (measurement)
+// rows per CTA: 2 for one request's ~800 rows (18.4 -> 14.5 us), 1 for the probe's
+// 32 / 256 rows (256: 10.2 vs 12.3 us) and the batch's 6400 (63.5 vs 65.6 us); 4 rows
+// per CTA was slower everywhere (tools/ln_bench.py). QCF_LN_ROWS=1/2 forces it.
 static int g_ln_rows = -1;
 template <typename T, int R>
 static int launch_ln_rows(float* x, const float* delta, int64_t m, int d, const float* g, const float* b, float eps,
@@ -204,7 +204,7 @@ static int launch_ln_vec(float* x, const float* delta, int64_t m, int d, const f
     const char* e = getenv("QCF_LN_ROWS");
     g_ln_rows = e ? ((atoi(e) == 2) ? 2 : 1) : 0;  // 0 = by row count
   }
-  const bool two = g_ln_rows == 2 || (g_ln_rows == 0 && m <= 2048);
+  const bool two = g_ln_rows == 2 || (g_ln_rows == 0 && m >= 512 && m <= 2048);
   if (two && d / 4 <= 4 * LN_THREADS) return launch_ln_rows<T, 2>(x, delta, m, d, g, b, eps, out, s);
   return launch_ln_rows<T, 1>(x, delta, m, d, g, b, eps, out, s);
 }

@@ -9,7 +9,7 @@ from paper_2604_08585_b200 import _lib
 
 s = torch.cuda.current_stream().cuda_stream
 d = 4096
-for m in (800, 6400, 5153):
+for m in (32, 256, 800, 6400):
     x = torch.randn(m, d, device="cuda")
     dl = torch.randn(m, d, device="cuda")
     g = torch.ones(d, device="cuda")
