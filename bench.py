@@ -484,8 +484,14 @@ def run_reference(args, cfgd, rank):
         norms = np.linalg.norm(k[0], axis=2).mean(axis=1)
         kv.append((k, v))
         anchors.append(O.extract_anchors(norms, 0.05))
+    # the whole arm stays within a few minutes: once the time budget is spent the
+    # remaining steps are not sampled and the line says how many were
+    budget = float(os.environ.get("QCF_REF_BUDGET_S", "150"))
+    t_start = time.perf_counter()
     times = []
     for i in range(args.warmup + args.steps):
+        if i > args.warmup and time.perf_counter() - t_start > budget:
+            break
         qt = np.random.default_rng(10_000 + i).integers(0, 256, cfgd["q"])
         r = cpu_sample(cfgd, kv, toks, anchors, qt, sample_layers)
         if i >= args.warmup:
@@ -498,7 +504,8 @@ def run_reference(args, cfgd, rank):
                                                        f"q={cfgd['q']}, recompute {cfgd['ratio']:.0%}, QCFuse"},
            "cpu_baseline": {"value": 1.0 / per, "unit": "requests/s", "cores": cpu_cores(), "kind": "port",
                             "sample": f"oracle numpy port, full width, {sample_layers} of {L} layers per phase, "
-                                      f"extrapolated to {L} layers"},
+                                      f"extrapolated to {L} layers; {len(times)} of {args.steps} steps sampled "
+                                      f"within the {budget:.0f} s budget"},
            "e2e": {"value": 1.0 / per, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
