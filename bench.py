@@ -434,6 +434,9 @@ def main():
                 "launches_per_step": n_gemm, "share_of_step": gemm_ms / sum(phases.values()),
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step); "
                                 "burst = bf16_tflops") if not pk.get("_fallback") else "fallback"}
+    if achieved and achieved > peak_sus:
+        roofline["peak_note"] = ("frac > 1: the sustained peak is a cuBLAS loop measured by the driver on another "
+                                 "box and clock; this box's power-capped clock ran above it")
 
     # ---- full prefill on the same box (the TTFT denominator, config 2 request)
     full_ms = None
