@@ -435,8 +435,8 @@ def main():
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step); "
                                 "burst = bf16_tflops") if not pk.get("_fallback") else "fallback"}
     if achieved and achieved > peak_sus:
-        roofline["peak_note"] = ("frac > 1: the sustained peak is a cuBLAS loop measured by the driver on another "
-                                 "box and clock; this box's power-capped clock ran above it")
+        roofline["peak_note"] = ("frac > 1: the sustained peak is the driver's cuBLAS measurement on a pool box; "
+                                 "these GEMMs run at that rate, and box-to-box power-capped clocks spread +-3%")
 
     # ---- full prefill on the same box (the TTFT denominator, config 2 request)
     full_ms = None
