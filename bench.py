@@ -3,13 +3,15 @@
 Contract (one JSON line from rank 0):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 A step = one fused prefill (assemble → probe → score → Top-N → selective
-recompute + query rows → first-token logits) of one RAG request of
-BASELINE.json configs[1]: random-init Llama-3-8B shape (L32 H32 D128 F14336,
-reference architecture: LayerNorm, ReLU FFN, tied byte vocab 259), 10 chunks ×
-512 tokens precomputed into the HBM chunk pool, 32-token query, 15% recompute.
+recompute + query rows → first-token logits) of a batch of --batch (8)
+concurrent RAG requests (BASELINE.json configs[2]), each request as in
+configs[1]: random-init Llama-3-8B shape (L32 H32 D128 F14336, reference
+architecture: LayerNorm, ReLU FFN, tied byte vocab 259), 10 chunks × 512
+tokens drawn from a 64-chunk HBM pool, 32-token query, 15% recompute.
 `value` = requests/s over all ranks (device-resident inputs, CUDA-graph
-replay); `e2e` = the same through the public `FusionEngine.fuse()` call with
-host query tokens in and host logits/selection out. Under torchrun each rank
+replay); `ttft_ms` = one request alone (configs[1]); `e2e` = the same metric
+through the public `FusionEngine.fuse_batch()` call with host query tokens in
+and host logits/selections out. Under torchrun each rank
 serves its own requests (weak scaling); results are gathered to rank 0 over
 NCCL once per step. `--impl reference` times the CPU oracle port on a bounded
 layer sample (rank 0 only).
