@@ -203,3 +203,30 @@ def test_oracle_gqa_equals_mha_with_repeated_kv_weights():
     b = O.forward_full(wm, toks, 0)
     assert np.allclose(a.logits, b.logits, atol=1e-6)
     assert np.array_equal(np.repeat(a.kv[2].keys, 2, axis=1), b.kv[2].keys)
+
+
+def _bench_reference(env_extra):
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **env_extra)
+    return subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "tiny",
+                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True, env=env, timeout=300)
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the CPU arm the driver times beside ours) prints
+    one JSON line with the contract keys; warm-up is clamped to >= 3."""
+    p = _bench_reference({"RANK": "0", "WORLD_SIZE": "1"})
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["unit"] == "requests/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] >= 3 and d["n_gpus"] == 1
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_bench_reference_arm_other_ranks_exit_silently():
+    p = _bench_reference({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert p.returncode == 0 and p.stdout.strip() == ""
