@@ -55,6 +55,13 @@ const char* qcf_version(void);
 const char* qcf_last_error(void);
 /* 1 when the sm_100a tcgen05 GEMM is usable on the current device. */
 int qcf_tc_available(void);
+/* Number of bf16 GEMM / attention calls that ran on the SIMT (FFMA) kernels
+ * because the shape is outside the tcgen05 contract (e.g. head dim != 128).
+ * A speed-mode run reports it; it must stay 0 at the benchmarked shapes. */
+long long qcf_simt_fallbacks(void);
+/* 1: such a bf16 call fails with QCF_EUNSUPPORTED instead of running on SIMT
+ * (also env QCF_STRICT_TC=1). 0 (default): it runs on SIMT and is counted. */
+int qcf_set_strict_tc(int on);
 
 /* ---- deterministic init: model.py:35-46 (splitmix64_at), 67-69, 225-257 ----
  * Writes draws [start, start + rows*cols) of the splitmix64 stream keyed by
@@ -257,8 +264,9 @@ int qcf_received_attention(int dtype, const void* q, const void* k, int64_t n_ke
 
 /* ---- Top-N selection: fusion.py:141-158 (stable argsort, ties -> lower index)
  * idx_out[0..n_sel) = ascending (1-based + base) positions of the n_sel largest
- * scores (scores must be >= +0 or NaN-free). n_sel is computed by the host as
- * ceil(ratio*n) in double. workspace >= qcf_topn_workspace(n). */
+ * scores, in the order numpy's stable argsort of -float64(scores) gives:
+ * -0.0 == +0.0 (lower index first), NaN after every number. n_sel is computed
+ * by the host as ceil(ratio*n) in double. workspace >= qcf_topn_workspace(n). */
 size_t qcf_topn_workspace(int64_t n);
 int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
              int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream);
@@ -268,6 +276,11 @@ int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
 int qcf_topn_batched(const float* scores, int64_t n, int n_req, int64_t n_sel, int32_t base,
                      int32_t* idx_out, int64_t out_stride, int32_t* dst_out, int32_t dst_add,
                      qcf_stream_t stream);
+
+/* The same selection over float64 scores (the public select_topn ranks
+ * float64, fusion.py:156): 64-bit keys, no float32 rounding of the input. */
+int qcf_topn_f64(const double* scores, int64_t n, int64_t n_sel, int32_t base, int32_t* idx_out,
+                 qcf_stream_t stream);
 
 /* Small device helpers used by the request graph. */
 /* out[i] = a[i] + add (int32) */

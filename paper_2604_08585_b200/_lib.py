@@ -44,6 +44,8 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_version": (ctypes.c_char_p, []),
     "qcf_last_error": (ctypes.c_char_p, []),
     "qcf_tc_available": (_I, []),
+    "qcf_simt_fallbacks": (ctypes.c_longlong, []),
+    "qcf_set_strict_tc": (_I, [_I]),
     "qcf_init_uniform": (_I, [_U64, _U64, _I64, _I64, _I, _I, _P, _I64, _P]),
     "qcf_assemble": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _P, _I64, _I, _P]),
     "qcf_assemble_rot": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _P, _I64, _P, _I, _I, _P]),
@@ -80,6 +82,7 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_topn_workspace": (_SZ, [_I64]),
     "qcf_topn": (_I, [_P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
     "qcf_topn_batched": (_I, [_P, _I64, _I, _I64, _I32, _P, _I64, _P, _I32, _P]),
+    "qcf_topn_f64": (_I, [_P, _I64, _I64, _I32, _P, _P]),
     "qcf_iota_add": (_I, [_P, _I64, _I32, _P, _P]),
     "qcf_iota": (_I, [_I64, _I32, _P, _P]),
 }
@@ -119,7 +122,7 @@ def check(status: int, what: str = "") -> None:
 
 # kernels launched per successful call (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {"qcf_score": 3}
-_NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_score_workspace",
+_NON_KERNEL = {"qcf_version", "qcf_last_error", "qcf_tc_available", "qcf_simt_fallbacks", "qcf_set_strict_tc", "qcf_score_workspace",
                "qcf_score_batched_workspace", "qcf_attention_workspace", "qcf_attention_split", "qcf_set_attention_kernel", "qcf_set_gemm_plan", "qcf_set_attention_split",
                "qcf_topn_workspace", "qcf_gemm_workspace"}
 launch_count = 0

@@ -4,7 +4,38 @@
 #include "common.cuh"
 #include "gemm.cuh"
 
+#include <atomic>
+#include <cstdlib>
+
 namespace qcf {
+
+// bf16 calls that left the tcgen05 kernels for the SIMT (FFMA) ones because
+// the shape is outside the tensor-core contract (head dim != 128, K % 8, toy
+// widths). Counted so a speed-mode run can prove it never fell back; with
+// strict mode on (qcf_set_strict_tc(1) or QCF_STRICT_TC=1) such a call fails
+// with QCF_EUNSUPPORTED instead.
+static std::atomic<long long> g_simt_fallbacks{0};
+static std::atomic<int> g_strict_tc{-1};
+
+static bool strict_tc() {
+  int v = g_strict_tc.load();
+  if (v < 0) {
+    const char* e = std::getenv("QCF_STRICT_TC");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_strict_tc.store(v);
+  }
+  return v == 1;
+}
+
+// returns QCF_OK when the SIMT path may run, QCF_EUNSUPPORTED in strict mode
+static int note_bf16_fallback(const char* what) {
+  g_simt_fallbacks.fetch_add(1);
+  if (strict_tc()) {
+    set_error("%s: bf16 shape outside the tcgen05 contract and strict tensor-core mode is on", what);
+    return QCF_EUNSUPPORTED;
+  }
+  return QCF_OK;
+}
 
 static int g_tc_state = -1;  // -1 unknown, 0 no, 1 yes
 
@@ -27,6 +58,14 @@ void set_gemm_plan(int p);
 
 extern "C" int qcf_tc_available(void) { return qcf::tc_ok() ? 1 : 0; }
 
+extern "C" long long qcf_simt_fallbacks(void) { return qcf::g_simt_fallbacks.load(); }
+
+extern "C" int qcf_set_strict_tc(int on) {
+  QCF_REQUIRE(on == 0 || on == 1, QCF_EINVAL, "qcf_set_strict_tc: 0 or 1");
+  qcf::g_strict_tc.store(on);
+  return QCF_OK;
+}
+
 extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, int64_t ldb, void* c,
                         int64_t ldc, int64_t m, int64_t n, int64_t k, int epilogue, int out_dtype,
                         qcf_stream_t stream) {
@@ -40,6 +79,8 @@ extern "C" int qcf_gemm(int dtype, const void* a, int64_t lda, const void* b, in
     if (st != QCF_EUNSUPPORTED) return st;
     // shapes outside the tcgen05 kernel's alignment contract (K % 8 != 0, tiny
     // toy widths) run on the SIMT kernel; still on the GPU, never on the host
+    st = qcf::note_bf16_fallback("qcf_gemm");
+    if (st != QCF_OK) return st;
   }
   return qcf::gemm_simt_launch(dtype, a, lda, b, ldb, c, ldc, m, n, k, epilogue, out_dtype, s);
 }
@@ -66,6 +107,8 @@ extern "C" int qcf_attention_batched_ws(int dtype, const void* q, const void* k,
   if (dtype == QCF_BF16 && qcf::tc_ok()) {
     int st = qcf::attention_tc_launch(q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req, ws, ws_bytes);
     if (st != QCF_EUNSUPPORTED) return st;
+    st = qcf::note_bf16_fallback("qcf_attention");
+    if (st != QCF_OK) return st;
   }
   return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, s, n_req);
 }

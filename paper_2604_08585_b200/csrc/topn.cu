@@ -5,6 +5,11 @@
 // image of the float32 scores), then an index-ordered block scan keeps every
 // key > T plus the first N - count(> T) keys == T (ties -> lower index) and
 // compacts them in ascending order. Bit-exact by construction.
+// Key map = the order numpy's stable argsort of -float64(score) induces:
+// -0.0 and +0.0 compare equal (one key, so the lower index wins), and NaN
+// sorts after every number (key 0: selected last, lower index first).
+// float64 scores (the public select_topn, fusion.py:156) use 64-bit keys
+// and 8 digit passes instead of 4.
 #include "common.cuh"
 
 namespace qcf {
@@ -12,9 +17,22 @@ namespace qcf {
 constexpr int TN_THREADS = 1024;
 
 __device__ __forceinline__ uint32_t order_key(float f) {
+  if (f != f) return 0u;                       // NaN: after every number
   uint32_t b = __float_as_uint(f);
+  if (b == 0x80000000u) b = 0u;                // -0.0 == +0.0
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
+
+__device__ __forceinline__ uint64_t order_key(double f) {
+  if (f != f) return 0ull;
+  uint64_t b = (uint64_t)__double_as_longlong(f);
+  if (b == 0x8000000000000000ull) b = 0ull;
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename S> struct KeyOf;
+template <> struct KeyOf<float> { using T = uint32_t; };
+template <> struct KeyOf<double> { using T = uint64_t; };
 
 // inclusive block scan of one int per thread (1024 threads)
 __device__ __forceinline__ int block_scan_incl(int v, int* warp_tot, int& total) {
@@ -48,15 +66,18 @@ __device__ __forceinline__ int block_scan_incl(int v, int* warp_tot, int& total)
 // request's rows in the batched fused table (the recompute scatter targets).
 constexpr int TN_SMEM_KEYS = 48 * 1024;
 
-template <bool SMEM>
-__global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restrict__ scores, int64_t n,
+template <bool SMEM, typename S>
+__global__ void __launch_bounds__(TN_THREADS) topn_kernel(const S* __restrict__ scores, int64_t n,
                                                           int64_t n_sel, int32_t base,
                                                           int32_t* __restrict__ out, int64_t out_stride,
                                                           int32_t* __restrict__ dst, int32_t dst_add) {
-  extern __shared__ uint32_t s_keys[];
+  using K = typename KeyOf<S>::T;
+  constexpr int TOP = 8 * (int)sizeof(K) - 8;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  K* s_keys = reinterpret_cast<K*>(s_raw);
   __shared__ int hist[256];
   __shared__ int warp_tot[32];
-  __shared__ uint32_t s_prefix;
+  __shared__ K s_prefix;
   __shared__ int s_need;
   const int tid = threadIdx.x;
   const int req = blockIdx.x;
@@ -70,15 +91,15 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
   if (SMEM) {
     for (int64_t i = tid; i < n; i += blockDim.x) s_keys[i] = order_key(scores[i]);
   }
-  auto key_at = [&](int64_t i) -> uint32_t { return SMEM ? s_keys[i] : order_key(scores[i]); };
-  // ---- radix select of the n_sel-th largest key, 4 digits of 8 bits (MSB first)
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  auto key_at = [&](int64_t i) -> K { return SMEM ? s_keys[i] : order_key(scores[i]); };
+  // ---- radix select of the n_sel-th largest key, digits of 8 bits (MSB first)
+  for (int shift = TOP; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
-    const uint32_t prefix = s_prefix;
-    const uint32_t hi_mask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
+    const K prefix = s_prefix;
+    const K hi_mask = shift == TOP ? (K)0 : (~(K)0 << (shift + 8));
     for (int64_t i = tid; i < n; i += blockDim.x) {
-      const uint32_t key = key_at(i);
+      const K key = key_at(i);
       if ((key & hi_mask) == (prefix & hi_mask)) atomicAdd(&hist[(key >> shift) & 0xff], 1);
     }
     __syncthreads();
@@ -104,19 +125,19 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
           if (cnt[u] >= rem) break;
           rem -= cnt[u];
         }
-        s_prefix = prefix | ((uint32_t)b << shift);
+        s_prefix = prefix | ((K)b << shift);
         s_need = rem;  // how many keys equal to the final threshold must be taken
       }
     }
     __syncthreads();
   }
-  const uint32_t T = s_prefix;
+  const K T = s_prefix;
   const int need_eq = s_need;
   // ---- ordered compaction: key > T always, key == T for the first need_eq (index order)
   int eq_before = 0, sel_before = 0;
   for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
     const int64_t i = c0 + tid;
-    const uint32_t key = i < n ? key_at(i) : 0u;
+    const K key = i < n ? key_at(i) : (K)0;
     const int is_eq = (i < n && key == T) ? 1 : 0;
     int eq_total;
     const int eq_incl = block_scan_incl(is_eq, warp_tot, eq_total);
@@ -134,6 +155,34 @@ __global__ void __launch_bounds__(TN_THREADS) topn_kernel(const float* __restric
   }
 }
 
+template <typename S>
+static int topn_launch(const S* scores, int64_t n, int n_req, int64_t n_sel, int32_t base, int32_t* idx_out,
+                       int64_t out_stride, int32_t* dst_out, int32_t dst_add, qcf_stream_t stream) {
+  QCF_REQUIRE(scores && (idx_out || n_sel == 0), QCF_EINVAL, "qcf_topn: null pointer");
+  QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n && n_req >= 1, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
+  QCF_REQUIRE(n_req == 1 || out_stride >= n_sel, QCF_EINVAL, "qcf_topn: output stride < n_sel");
+  QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
+  if (n_sel == 0) return QCF_OK;
+  auto s = as_stream(stream);
+  constexpr int64_t kSmemKeys = TN_SMEM_KEYS * 4 / (int64_t)sizeof(typename KeyOf<S>::T);
+  if (n <= kSmemKeys) {
+    static bool attr = false;
+    const size_t smem = (size_t)n * sizeof(typename KeyOf<S>::T);
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(topn_kernel<true, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           TN_SMEM_KEYS * (int)sizeof(uint32_t));
+      if (e != cudaSuccess) return cuda_status(e, "qcf_topn attr");
+      attr = true;
+    }
+    QCF_LAUNCH("topn_kernel", (topn_kernel<true, S>), dim3(n_req), dim3(TN_THREADS), smem, s, scores, n, n_sel,
+               base, idx_out, out_stride, dst_out, dst_add);
+  } else {
+    QCF_LAUNCH("topn_kernel", (topn_kernel<false, S>), dim3(n_req), dim3(TN_THREADS), 0, s, scores, n, n_sel,
+               base, idx_out, out_stride, dst_out, dst_add);
+  }
+  QCF_LAUNCH_CHECK("qcf_topn");
+  return QCF_OK;
+}
 }  // namespace qcf
 
 extern "C" size_t qcf_topn_workspace(int64_t n) { (void)n; return 0; }
@@ -141,33 +190,16 @@ extern "C" size_t qcf_topn_workspace(int64_t n) { (void)n; return 0; }
 extern "C" int qcf_topn_batched(const float* scores, int64_t n, int n_req, int64_t n_sel, int32_t base,
                                 int32_t* idx_out, int64_t out_stride, int32_t* dst_out, int32_t dst_add,
                                 qcf_stream_t stream) {
-  QCF_REQUIRE(scores && (idx_out || n_sel == 0), QCF_EINVAL, "qcf_topn: null pointer");
-  QCF_REQUIRE(n >= 0 && n_sel >= 0 && n_sel <= n && n_req >= 1, QCF_EINVAL, "qcf_topn: need 0 <= n_sel <= n");
-  QCF_REQUIRE(n_req == 1 || out_stride >= n_sel, QCF_EINVAL, "qcf_topn: output stride < n_sel");
-  QCF_REQUIRE(n < 0x7fffffff, QCF_EUNSUPPORTED, "qcf_topn: n too large");
-  if (n_sel == 0) return QCF_OK;
-  auto s = qcf::as_stream(stream);
-  if (n <= qcf::TN_SMEM_KEYS) {
-    static bool attr = false;
-    const size_t smem = (size_t)n * sizeof(uint32_t);
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(qcf::topn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           qcf::TN_SMEM_KEYS * (int)sizeof(uint32_t));
-      if (e != cudaSuccess) return qcf::cuda_status(e, "qcf_topn attr");
-      attr = true;
-    }
-    QCF_LAUNCH("topn_kernel", qcf::topn_kernel<true>, dim3(n_req), dim3(qcf::TN_THREADS), smem, s, scores, n, n_sel,
-               base, idx_out, out_stride, dst_out, dst_add);
-  } else {
-    QCF_LAUNCH("topn_kernel", qcf::topn_kernel<false>, dim3(n_req), dim3(qcf::TN_THREADS), 0, s, scores, n, n_sel,
-               base, idx_out, out_stride, dst_out, dst_add);
-  }
-  QCF_LAUNCH_CHECK("qcf_topn");
-  return QCF_OK;
+  return qcf::topn_launch<float>(scores, n, n_req, n_sel, base, idx_out, out_stride, dst_out, dst_add, stream);
 }
 
 extern "C" int qcf_topn(const float* scores, int64_t n, int64_t n_sel, int32_t base,
                         int32_t* idx_out, void* workspace, size_t ws_bytes, qcf_stream_t stream) {
   (void)workspace; (void)ws_bytes;
   return qcf_topn_batched(scores, n, 1, n_sel, base, idx_out, n_sel, nullptr, 0, stream);
+}
+
+extern "C" int qcf_topn_f64(const double* scores, int64_t n, int64_t n_sel, int32_t base, int32_t* idx_out,
+                            qcf_stream_t stream) {
+  return qcf::topn_launch<double>(scores, n, 1, n_sel, base, idx_out, n_sel, nullptr, 0, stream);
 }

@@ -31,6 +31,7 @@ import math
 import os
 import time
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -259,20 +260,36 @@ def topn_device(scores: torch.Tensor, n: int, base: int = 1, out: torch.Tensor |
     return out[:n]
 
 
+def _topn_f64(scores, n: int) -> np.ndarray:
+    """Ascending 1-based positions of the n largest float64 scores on the
+    device (`qcf_topn_f64`): the order of np.argsort(-float64, stable) --
+    ties and ±0 toward the lower index, NaN last -- with no float32 rounding."""
+    s = np.ascontiguousarray(np.asarray(scores, dtype=np.float64).reshape(-1))
+    n = int(n)
+    if not (0 <= n <= s.size):
+        raise ValueError("n must be in [0, len(scores)]")
+    if n == 0:
+        return np.zeros(0, np.int64)
+    ts = torch.as_tensor(s, device="cuda")
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    call("qcf_topn_f64", ts.data_ptr(), s.size, n, 1, out.data_ptr(), cuda_stream())
+    return out.cpu().numpy().astype(np.int64)
+
+
 def top_n_positions(scores, n: int) -> np.ndarray:
-    """fusion.py:141-145 on the device."""
-    s = torch.as_tensor(np.asarray(scores, dtype=np.float32), device="cuda")
-    return topn_device(s, int(n)).cpu().numpy().astype(np.int64)
+    """fusion.py:141-145 on the device (float64 keys)."""
+    return _topn_f64(scores, n)
 
 
 def select_topn(scores, ratio: float, policy: str = "QCFuse") -> SelectionResult:
-    """fusion.py:148-158: N = ceil(ratio·n_ctx), ties toward the lower index."""
+    """fusion.py:148-158: N = ceil(ratio·n_ctx), float64 ranking, ties toward
+    the lower index, ascending output; scores returned as float32 like the
+    reference's SelectionResult."""
     if not (0.0 <= ratio <= 1.0):
         raise ValueError("ratio must be in [0, 1]")
-    s = np.asarray(scores, dtype=np.float64).astype(np.float32)
+    s = np.asarray(scores, dtype=np.float64)
     n = n_select(ratio, s.size)
-    idx = topn_device(torch.as_tensor(s, device="cuda"), n).cpu().numpy().astype(np.int64)
-    return SelectionResult(policy, ratio, idx, s)
+    return SelectionResult(policy, ratio, _topn_f64(s, n), s.astype(np.float32))
 
 
 def epic_select(n_ctx: int, ratio: float, chunk_spans=None) -> SelectionResult:
@@ -409,6 +426,7 @@ class _Bufs:
         self.sc_probe = eng.ex.scratch(B * q, key=("probe", id(self)))
         self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
+        self.rope_key: tuple | None = None   # RoPE table pointers the graph baked in
         self.h_staged: list[torch.Tensor] | None = None   # pinned host mirrors of staged()
         self.h_done: torch.cuda.Event | None = None
 
@@ -436,7 +454,8 @@ class FusionEngine:
         bos = torch.tensor([BOS_ID], dtype=torch.int32, device=self.device)
         bk, bv, _ = self.ex.forward_full(bos, 0)
         self._bos_k, self._bos_v = bk[:, 0].contiguous(), bv[:, 0].contiguous()
-        self._bufs: dict[tuple, _Bufs] = {}
+        self._bufs: "OrderedDict[tuple, _Bufs]" = OrderedDict()
+        self.max_shapes = int(os.environ.get("QCF_MAX_SHAPES", "8"))
         self._oracle_cache: dict = {}
         # assembly || probe on two streams (see _launch); measured neutral on B200 at the
         # Llama-3-8B shape (tools/concurrency_check.py: both phases are HBM-bound), off by default
@@ -779,12 +798,22 @@ class FusionEngine:
         return _Plan(list(chunk_ids), recs, offs, n_ctx, q, n_sel, rows, policy)
 
     def _buffers(self, plans: list[_Plan], extra_rows: int = 0) -> _Bufs:
+        """Per-shape buffers + graph, least-recently-used first out: at most
+        `max_shapes` shapes stay resident (each holds a full fused table)."""
         key = (plans[0].shape_key(), len(plans), extra_rows)
-        b = self._bufs.get(key)
+        b = self._bufs.pop(key, None)
         if b is None:
+            while len(self._bufs) >= max(1, self.max_shapes):
+                self._evict(next(iter(self._bufs)))
             b = _Bufs(self, plans[0], len(plans), extra_rows)
-            self._bufs[key] = b
+        self._bufs[key] = b      # most recently used last
         return b
+
+    def _evict(self, key) -> None:
+        b = self._bufs.pop(key)
+        b.graph = None
+        for k in (("probe", id(b)), ("rc", id(b))):
+            self.ex._scratch.pop(k, None)
 
     def _stage(self, plans: list[_Plan], b: _Bufs, queries, stream=None) -> dict:
         """Host -> device copies of the batch's inputs (chunk descriptors,
@@ -1029,6 +1058,9 @@ class FusionEngine:
                     base += n
                 staged[li].record(cs)
 
+        # the previous call's last assemblies (main stream) may still read these
+        # slots: the copy stream starts only after everything enqueued so far
+        cs.wait_stream(main)
         for li in range(min(n_slots, L)):
             fetch(li)
         m = B * b.Mr
@@ -1080,6 +1112,10 @@ class FusionEngine:
         if not use_graph:
             self._launch(plans, b, stream)
             return plans, b
+        rope = self.ex.rope
+        rope_key = (rope.cos.data_ptr(), rope.sin.data_ptr(), rope.cs32.data_ptr(), rope.n_pos)
+        if b.graph is not None and b.rope_key != rope_key:
+            b.graph = None      # the RoPE table grew (moved) since capture: re-capture
         if b.graph is None:
             s = stream or torch.cuda.current_stream()
             side = torch.cuda.Stream(device=self.device)
@@ -1092,6 +1128,7 @@ class FusionEngine:
                 self._launch(plans, b, side)
             s.wait_stream(side)
             b.graph = g
+            b.rope_key = rope_key
         b.graph.replay()
         return plans, b
 

@@ -283,11 +283,17 @@ class RopeTable:
         self.d_head, self.theta, self.device = d_head, theta, torch.device(device)
         self.n_pos = 0
         self.cos = self.sin = self.cs32 = None
+        # tables replaced by growth stay allocated: captured graphs and launches
+        # still in flight on other streams keep valid pointers (each old table is
+        # a prefix of the new one, so their positions still read correct values)
+        self.retired: list[tuple] = []
         self.ensure(n_pos)
 
     def ensure(self, n_pos: int) -> None:
         if n_pos <= self.n_pos:
             return
+        if self.cos is not None:
+            self.retired.append((self.cos, self.sin, self.cs32))
         n = max(n_pos, 2 * self.n_pos)
         j = np.arange(self.d_head // 2, dtype=np.float64)
         inv = self.theta ** (-2.0 * j / self.d_head)

@@ -170,6 +170,57 @@ def test_topn_bit_exact(L, n, frac, levels):
     assert np.array_equal(out[:k].cpu().numpy(), ref)
 
 
+def _special_scores(rng, n, dtype):
+    """Scores mixing ±0, negatives, ±inf and NaN with heavy ties."""
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 0.5, np.inf, -np.inf, np.nan, 1e-30, -1e-30], dtype=dtype)
+    return rng.choice(pool, size=n).astype(dtype)
+
+
+@pytest.mark.parametrize("n,frac", [(2, 0.5), (37, 0.4), (1000, 0.3), (5120, 0.15), (70000, 0.1)])
+def test_topn_signed_zero_nan_edge_cases(L, n, frac):
+    """±0 tie (lower index wins) and NaN last, as np.argsort(-float64, stable)
+    orders them (fusion.py:141-158), for the f32 and the f64 kernels."""
+    rng = np.random.default_rng(n + 7)
+    k = math.ceil(frac * n)
+    for dt in (np.float32, np.float64):
+        s = _special_scores(rng, n, dt)
+        ref = np.sort(np.argsort(-s.astype(np.float64), kind="stable")[:k]) + 1
+        ts = torch.as_tensor(s, device="cuda")
+        out = torch.full((max(k, 1),), -7, dtype=torch.int32, device="cuda")
+        if dt is np.float32:
+            L.call("qcf_topn", p(ts), n, k, 1, p(out), None, 0, S())
+        else:
+            L.call("qcf_topn_f64", p(ts), n, k, 1, p(out), S())
+        assert np.array_equal(out[:k].cpu().numpy(), ref), dt
+
+
+def test_select_topn_reference_examples():
+    """fusion.py:148-158 examples: [-0.0, 0.0] at 0.5 -> [1] (tie, lower index);
+    NaN never outranks a number; float64 values that collapse in float32 keep
+    their float64 order."""
+    import paper_2604_08585_b200 as Q
+    assert Q.select_topn([-0.0, 0.0], 0.5).indices.tolist() == [1]
+    assert Q.select_topn([0.0, -0.0], 0.5).indices.tolist() == [1]
+    assert Q.select_topn([np.nan, 0.1, 0.2], 2 / 3).indices.tolist() == [2, 3]
+    a = 1.0 + 2.0 ** -40       # equal to 1.0 in float32, larger in float64
+    assert Q.select_topn([1.0, a, 0.0], 1 / 3).indices.tolist() == [2]
+    assert Q.select_topn([0.9, 0.1, 0.5, 0.4], 0.5).indices.tolist() == [1, 3]
+    assert Q.top_n_positions([0.2, 0.9, 0.9, 0.1], 2).tolist() == [2, 3]
+
+
+@pytest.mark.parametrize("n,frac,levels", [(5120, 0.15, None), (1000, 0.3, 4), (32768, 0.15, 16),
+                                           (30000, 0.2, None)])
+def test_topn_f64_bit_exact(L, n, frac, levels):
+    rng = np.random.default_rng(n + 1)
+    s = (rng.choice(np.linspace(0, 1, levels), size=n) if levels else rng.random(n)).astype(np.float64)
+    k = math.ceil(frac * n)
+    ref = np.sort(np.argsort(-s, kind="stable")[:k]) + 1
+    ts = torch.as_tensor(s, device="cuda")
+    out = torch.full((max(k, 1),), -7, dtype=torch.int32, device="cuda")
+    L.call("qcf_topn_f64", p(ts), n, k, 1, p(out), S())
+    assert np.array_equal(out[:k].cpu().numpy(), ref)
+
+
 # ---------------------------------------------------------------- scoring
 @pytest.mark.parametrize("agg", ["mean", "last"])
 def test_score_vs_oracle_and_topn_on_reference_inputs(L, golden_dir, agg):

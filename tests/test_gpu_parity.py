@@ -674,3 +674,49 @@ def test_side_stream_assembly_matches_serial(golden_dir, tmp_path, dtype):
     eng.pipeline_asm = True
     for lg, sel in out[1:]:
         assert torch.equal(lg, out[0][0]) and torch.equal(sel, out[0][1])
+
+
+def test_rope_growth_keeps_captured_graphs_correct(tmp_path):
+    """fuse() at a 5k context (graph captured), then at 16k (the RoPE table
+    grows past its initial 8192 positions and moves), then the 5k request
+    again: the replayed graph must give bit-identical logits and selection."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=256, d_head=128, d_ff=512, seed=11)
+    w = Q.init_weights(cfg, dtype="bf16")
+    store = Q.ChunkStore(tmp_path, cfg, dtype="bf16", persist=False)
+    rng = np.random.default_rng(3)
+    pool = [store.precompute(w, rng.integers(0, 256, 512)).chunk_id for _ in range(32)]
+    eng = Q.FusionEngine(w, store)
+    query = rng.integers(0, 256, 16).tolist()
+    small = pool[:10]
+    l1, s1 = eng.fuse(query, small, 0.15)
+    ptr0 = eng.ex.rope.cos.data_ptr()
+    l_big, s_big = eng.fuse(query, pool, 0.15)          # 16384 context rows
+    assert eng.ex.rope.n_pos > 8192 and eng.ex.rope.cos.data_ptr() != ptr0
+    l2, s2 = eng.fuse(query, small, 0.15)
+    assert np.array_equal(s1, s2) and np.array_equal(l1, l2)
+    # a fresh engine (no captured graph) agrees with the replayed one
+    eng2 = Q.FusionEngine(w, store)
+    l3, s3 = eng2.fuse(query, small, 0.15)
+    assert np.array_equal(s1, s3) and np.array_equal(l1, l3)
+
+
+def test_shape_cache_is_bounded_lru(tmp_path):
+    """At most max_shapes per-shape buffer sets stay resident; an evicted
+    shape is rebuilt with identical results."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=256, d_head=128, d_ff=512, seed=12)
+    w = Q.init_weights(cfg, dtype="bf16")
+    store = Q.ChunkStore(tmp_path, cfg, dtype="bf16", persist=False)
+    rng = np.random.default_rng(4)
+    ids = [store.precompute(w, rng.integers(0, 256, 128)).chunk_id for _ in range(4)]
+    eng = Q.FusionEngine(w, store)
+    eng.max_shapes = 2
+    q = rng.integers(0, 256, 8).tolist()
+    first = eng.fuse(q, ids[:2], 0.2)
+    eng.fuse(q, ids[:3], 0.2)
+    eng.fuse(q, ids[:4], 0.2)
+    assert len(eng._bufs) == 2
+    again = eng.fuse(q, ids[:2], 0.2)
+    assert len(eng._bufs) == 2
+    assert np.array_equal(first[0], again[0]) and np.array_equal(first[1], again[1])
