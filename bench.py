@@ -235,8 +235,15 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="concurrent requests per GPU per step (config 3)")
     ap.add_argument("--pool", type=int, default=64, help="chunk pool size (config 3: 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity", action="store_true",
+                    help="instead of timing: configs[1] at full depth vs the CPU oracle (tools/parity_l32.py)")
     ap.add_argument("--no-full", action="store_true", help="skip the full-prefill comparison")
     args = ap.parse_args()
+    if args.parity:   # correctness leg at full depth (not a timing run)
+        sys.argv = [sys.argv[0], "--out", os.environ.get("QCF_PARITY_OUT", "gpurun_out/parity_l32.json")]
+        sys.path.insert(0, str(ROOT / "tools"))
+        import parity_l32
+        return parity_l32.main()
     cfgd = dict(CONFIGS[args.config])
     if args.ratio is not None:
         cfgd["ratio"] = args.ratio

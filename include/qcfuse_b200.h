@@ -85,7 +85,9 @@ typedef struct {
  * fused_v[l][off_c + i] = chunk_v[l][i]                (bit copy)
  * fused_*[l][0]         = bos_*[l]                     (BOS row, position 0)
  * `chunks` is a DEVICE array of n_chunks descriptors. cos/sin tables are float64
- * [n_pos][D/2] built on the host exactly as model.py:264-280 builds the angles. */
+ * [n_pos][D/2] built on the host exactly as model.py:264-280 builds the angles.
+ * fused_v may be NULL: K only (the f32 critical-layer keys of the fp32
+ * scoring mode); bos_v and the descriptors' v are then not read. */
 int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
                  const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
                  int64_t fused_layer_stride, int n_layers, int hkv, int d,

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
   constexpr bool kBf16 = sizeof(T) == 2;
   const int layer = layer0 + blockIdx.y;
   const int vpr = row_elems / V;
+  const bool has_v = fv != nullptr;   // K only (fp32 scoring keys) when null
   const int half = d >> 1;
   __shared__ qcf_chunk_desc sc;
   __shared__ int64_t s_delta;
@@ -81,7 +82,8 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
       if (row == 0) {
         for (int i = threadIdx.x; i < vpr; i += blockDim.x) {
           reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(bos_k + (int64_t)layer * row_elems)[i];
-          reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems)[i];
+          if (has_v)
+            reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(bos_v + (int64_t)layer * row_elems)[i];
         }
         continue;
       }
@@ -113,14 +115,14 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
           const int i = i0 + u * blockDim.x;
           if (i < vpr) {
             kv[u] = __ldg(sk + i);
-            vv[u] = __ldg(sv + i);
+            if (has_v) vv[u] = __ldg(sv + i);
           }
         }
 #pragma unroll
         for (int u = 0; u < ASM_UNROLL; ++u) {
           const int i = i0 + u * blockDim.x;
           if (i < vpr) {
-            reinterpret_cast<uint4*>(dv)[i] = vv[u];
+            if (has_v) reinterpret_cast<uint4*>(dv)[i] = vv[u];
             const int j0 = ((i * V) % d) >> 1;
             if constexpr (kBf16) {
               const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&kv[u]);
@@ -172,7 +174,7 @@ static int assemble_impl(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx, 
                          const void* bos_v, void* fused_k, void* fused_v, int64_t fused_layer_stride, int layer0,
                          int n_layers, int hkv, int d, const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
                          const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
-  QCF_REQUIRE(chunks && bos_k && bos_v && fused_k && fused_v && cos_tbl && sin_tbl, QCF_EINVAL,
+  QCF_REQUIRE(chunks && bos_k && fused_k && cos_tbl && sin_tbl && (!fused_v || bos_v), QCF_EINVAL,
               "qcf_assemble: null pointer");
   QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1 && layer0 >= 0, QCF_EINVAL,
               "qcf_assemble: bad sizes");

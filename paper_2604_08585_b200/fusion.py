@@ -425,6 +425,17 @@ class _Bufs:
         self.logits = torch.empty((B, cfg.vocab_size), dtype=torch.float32, device=dev)
         self.sc_probe = eng.ex.scratch(B * q, key=("probe", id(self)))
         self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
+        self.fp32 = eng.fp32_scoring and plan.policy == "QCFuse" and n_sel > 0
+        if self.fp32:
+            # fp32 scoring mode: float32 probe prefix, Q_c and fused critical-layer keys
+            f32 = torch.float32
+            self.pk32 = torch.empty((c, B * P, Hkv, D), dtype=f32, device=dev)
+            self.pv32 = torch.empty_like(self.pk32)
+            self.qc32 = torch.empty((B * q, H, D), dtype=f32, device=dev)
+            self.kc32 = torch.empty((B * (1 + n_ctx), Hkv, D), dtype=f32, device=dev)
+            self.adesc32 = torch.empty_like(self.adesc)
+            self.kdesc32 = torch.empty_like(self.desc)
+            self.sc_probe32 = eng.ex32.scratch(B * q, key=("probe32", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
         self.rope_key: tuple | None = None   # RoPE table pointers the graph baked in
         self.h_staged: list[torch.Tensor] | None = None   # pinned host mirrors of staged()
@@ -433,7 +444,8 @@ class _Bufs:
     def staged(self) -> list[torch.Tensor]:
         """The device tensors a batch's host inputs are staged into (swapped
         between graph replays)."""
-        return [self.desc, self.tok, self.anchor_rows, self.adesc, self.adelta]
+        extra = [self.adesc32, self.kdesc32] if self.fp32 else []
+        return [self.desc, self.tok, self.anchor_rows, self.adesc, self.adelta] + extra
 
 
 class FusionEngine:
@@ -454,6 +466,20 @@ class FusionEngine:
         bos = torch.tensor([BOS_ID], dtype=torch.int32, device=self.device)
         bk, bv, _ = self.ex.forward_full(bos, 0)
         self._bos_k, self._bos_v = bk[:, 0].contiguous(), bv[:, 0].contiguous()
+        # fp32 scoring mode (SURVEY §7 hard parts): a bf16 engine whose store keeps
+        # float32 critical-layer keys and anchor rows, and whose weights carry
+        # float32 copies of layers 1..c: the probe (FFMA GEMMs, float64 RoPE) and
+        # the float64 scoring run in float32 end to end, so the selected index set
+        # is the reference's bit for bit; the recompute stays bf16 on tcgen05
+        self.fp32_scoring = getattr(store, "keep_f32_probe", False)
+        self.ex32 = None
+        if self.fp32_scoring:
+            if weights.probe32 is None:
+                raise ValueError("store is in fp32 scoring mode: build the weights with scoring='fp32'")
+            self.ex32 = _executor_for(weights.probe32)
+            c = self.config.critical_layer
+            bk32, bv32, _ = self.ex32.forward_full(bos, 0, layers=range(c))
+            self._bos_k32, self._bos_v32 = bk32[:, 0].contiguous(), bv32[:, 0].contiguous()
         self._bufs: "OrderedDict[tuple, _Bufs]" = OrderedDict()
         self.max_shapes = int(os.environ.get("QCF_MAX_SHAPES", "8"))
         self._oracle_cache: dict = {}
@@ -509,6 +535,31 @@ class FusionEngine:
             arr[i].n_tok = na
             arr[i].offset = row
             row += na
+        return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
+
+    def _anchor_desc32_bytes(self, recs) -> torch.Tensor:
+        """Descriptors of the float32 anchor rows (layers 1..c) of each chunk."""
+        arr = (ChunkDesc * len(recs))()
+        row = 1
+        for i, r in enumerate(recs):
+            na = int(r.anchor_indices.size)
+            arr[i].k = r.anchor_k32.data_ptr()
+            arr[i].v = r.anchor_v32.data_ptr()
+            arr[i].layer_stride = r.anchor_k32.stride(0) if na else 0
+            arr[i].n_tok = na
+            arr[i].offset = row
+            row += na
+        return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
+
+    def _kcrit32_desc_bytes(self, recs, offs) -> torch.Tensor:
+        """Descriptors of the float32 critical-layer keys (one layer, K only)."""
+        arr = (ChunkDesc * len(recs))()
+        for i, (r, o) in enumerate(zip(recs, offs)):
+            arr[i].k = r.k_crit32.data_ptr()
+            arr[i].v = r.k_crit32.data_ptr()
+            arr[i].layer_stride = 0
+            arr[i].n_tok = r.n_tokens
+            arr[i].offset = o
         return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
 
     def _assemble_range(self, recs, n_ctx, fk, fv, desc_dev, layer0, n_layers, stream=None, layer_stride=None):
@@ -818,10 +869,13 @@ class FusionEngine:
     def _stage(self, plans: list[_Plan], b: _Bufs, queries, stream=None) -> dict:
         """Host -> device copies of the batch's inputs (chunk descriptors,
         token tables, probe rows). Returns the byte counts."""
-        descs, toks, rows, adescs, adeltas = [], [], [], [], []
+        descs, toks, rows, adescs, adeltas, a32, k32 = [], [], [], [], [], [], []
         for plan, qt in zip(plans, queries):
             descs.append(self._desc_bytes(plan.records, plan.offsets))
             adescs.append(self._anchor_desc_bytes(plan.records, plan.offsets))
+            if b.fp32:
+                a32.append(self._anchor_desc32_bytes(plan.records))
+                k32.append(self._kcrit32_desc_bytes(plan.records, plan.offsets))
             adeltas.append(np.asarray(plan.offsets, np.int32))
             t = np.zeros(b.R, np.int32)
             body = np.concatenate([[BOS_ID], *[r.token_ids for r in plan.records], np.asarray(qt, np.int64)])
@@ -835,6 +889,9 @@ class FusionEngine:
         adelta = np.concatenate(adeltas)
         host = [desc, torch.from_numpy(tok), torch.from_numpy(rows), adesc, torch.from_numpy(adelta)]
         dev = [b.desc, b.tok, b.anchor_rows[:rows.size], b.adesc, b.adelta]
+        if b.fp32:
+            host += [torch.cat(a32), torch.cat(k32)]
+            dev += [b.adesc32, b.kdesc32]
         if b.h_staged is None:   # persistent pinned staging buffers (no per-call pinned allocation)
             b.h_staged = [torch.empty(t.numel() * t.element_size(), dtype=torch.uint8, pin_memory=True)
                           for t in host]
@@ -913,7 +970,9 @@ class FusionEngine:
             e = layer_ready.pop(li, None)
             if e is not None:
                 main.wait_event(e)
-        if probe:
+        if probe and b.fp32:
+            self._probe_score_fp32(plan, b, stream)
+        elif probe:
             for r in range(B):   # K2: probe prefix rows of request r from the chunks' anchor rows
                 call("qcf_assemble_rot", b.adesc.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k.data_ptr(),
                      self._bos_v.data_ptr(), b.pk.data_ptr() + r * b.P * row_elems * esz,
@@ -931,6 +990,7 @@ class FusionEngine:
             # K4: scoring of the whole batch (request r's keys at rows r*R+1.. of layer c)
             self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream, n_req=B,
                             k_req_stride=b.R * row_elems)
+        if probe:
             # K5: Top-N of every request (ascending positions -> rc_pos, table rows -> rc_dst)
             call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
                  b.rc_dst.data_ptr(), b.R, s)
@@ -950,6 +1010,40 @@ class FusionEngine:
         if last is not None:   # join the side stream (every range is complete by now anyway)
             main.wait_event(last)
         ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
+
+    def _probe_score_fp32(self, plan: _Plan, b: _Bufs, stream=None) -> None:
+        """K2-K4 of the fp32 scoring mode: the probe prefix from the float32
+        anchor rows (fusion.py:281-303), the probe's layers 1..c-1 plus layer c's
+        Q on the float32 weights (FFMA GEMMs, float64 RoPE; model.py:345-388),
+        the float32 fused critical-layer keys assembled from each chunk's float32
+        K_c (fusion.py:234-263), and the float64 scoring of fusion.py:313-326."""
+        cfg, ex32 = self.config, self.ex32
+        c, q, n_ctx, B = cfg.critical_layer, plan.q, plan.n_ctx, b.B
+        s = cuda_stream(stream)
+        row_elems = cfg.n_kv_heads * cfg.d_head
+        nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
+        n_ch = len(plan.records)
+        rope = ex32.rope
+        for r in range(B):
+            call("qcf_assemble_rot", b.adesc32.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k32.data_ptr(),
+                 self._bos_v32.data_ptr(), b.pk32.data_ptr() + r * b.P * row_elems * 4,
+                 b.pv32.data_ptr() + r * b.P * row_elems * 4, b.pk32.stride(0), c, cfg.n_kv_heads, cfg.d_head,
+                 rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, b.adelta.data_ptr() + r * n_ch * 4,
+                 b.max_delta, _lib.QCF_F32, s)
+            kc = b.kc32.data_ptr() + r * (1 + n_ctx) * row_elems * 4
+            call("qcf_assemble", b.kdesc32.data_ptr() + r * nd, n_ch, n_ctx, self._bos_k32[c - 1].data_ptr(), None,
+                 kc, None, (1 + n_ctx) * row_elems, 1, cfg.n_kv_heads, cfg.d_head, rope.cos.data_ptr(),
+                 rope.sin.data_ptr(), rope.n_pos, _lib.QCF_F32, s)
+        sc = b.sc_probe32
+        ex32.embed(sc, B * q, b.tok, rows=b.p_tok, stream=stream)
+        for li in range(c - 1):
+            ex32.layer(li, sc, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[li], b.pv32[li], stream=stream, n_req=B)
+        ex32.layer(c - 1, sc, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[c - 1], b.pv32[c - 1],
+                   q_only=True, q_out=b.qc32, stream=stream, n_req=B)
+        call("qcf_score_batched", _lib.QCF_F32, b.qc32.data_ptr(), b.kc32[1:].data_ptr(),
+             (1 + n_ctx) * row_elems, n_ctx, q, B, cfg.n_heads, cfg.n_kv_heads, cfg.d_head,
+             1.0 / math.sqrt(cfg.d_head), 1 if self.options.query_agg == "last" else 0, 1,
+             b.scores.data_ptr(), b.score_ws.data_ptr(), b.score_ws.numel(), s)
 
     # ------------------------------------------------------------------
     # host-pool variant: layer-pipelined chunk-KV streaming (SURVEY §8f rank 3)
@@ -985,7 +1079,11 @@ class FusionEngine:
             return torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(dev)
 
         keep = []   # device descriptor arrays must outlive the launches
-        if plan.policy == "QCFuse" and n_sel > 0:
+        if b.fp32:   # fp32 scoring: its inputs (float32 anchors, K_c) are HBM-resident
+            self._probe_score_fp32(plan, b)
+            call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
+                 b.rc_dst.data_ptr(), b.R, s)
+        elif plan.policy == "QCFuse" and n_sel > 0:
             for r, pl in enumerate(plans):
                 # probe prefix rows [BOS | anchors of chunk 0 | ...] of layers < c, K rotated by off_c
                 fields, deltas, row = [], [], 1
@@ -1104,6 +1202,8 @@ class FusionEngine:
         b = self._buffers(plans, extra_rows)
         self._stage(plans, b, queries, stream)
         self.ex.rope.ensure(b.rows + 2)
+        if self.ex32 is not None:
+            self.ex32.rope.ensure(b.rows + 2)
         if any(r.on_host for pl in plans for r in pl.records):
             if not all(r.on_host for pl in plans for r in pl.records):
                 raise ValueError("a batch must draw all its chunks from one pool placement")
@@ -1112,8 +1212,8 @@ class FusionEngine:
         if not use_graph:
             self._launch(plans, b, stream)
             return plans, b
-        rope = self.ex.rope
-        rope_key = (rope.cos.data_ptr(), rope.sin.data_ptr(), rope.cs32.data_ptr(), rope.n_pos)
+        rope_key = tuple((r.cos.data_ptr(), r.sin.data_ptr(), r.cs32.data_ptr(), r.n_pos)
+                         for r in (self.ex.rope, self.ex32.rope if self.ex32 is not None else None) if r is not None)
         if b.graph is not None and b.rope_key != rope_key:
             b.graph = None      # the RoPE table grew (moved) since capture: re-capture
         if b.graph is None:

@@ -157,6 +157,9 @@ class ModelWeights:
     ln_f_bias: torch.Tensor
     device: torch.device = field(default_factory=lambda: torch.device("cuda"))
     b_layout: int = _lib.B_ROWMAJOR   # projection weights tile-major (B_TILE64) in bf16 mode
+    # fp32 scoring mode: float32 copies of layers 1..c (the probe that produces
+    # Q_c runs on them, so selection is the reference's bit for bit)
+    probe32: "ModelWeights | None" = None
 
     @property
     def qcf_dtype(self) -> int:
@@ -172,9 +175,15 @@ class ModelWeights:
 
     @classmethod
     def from_host(cls, config: ModelConfig, token_embedding, layers, dtype="bf16",
-                  device="cuda") -> "ModelWeights":
+                  device="cuda", scoring: str = "native") -> "ModelWeights":
         """From host arrays in the reference layout: layers is a sequence of
-        objects with wq wk wv wo w1 w2 ([d_in][d_out]) and ln gains/biases."""
+        objects with wq wk wv wo w1 w2 ([d_in][d_out]) and ln gains/biases.
+        scoring="fp32" (bf16 weights) also keeps float32 copies of layers 1..c."""
+        if scoring not in ("native", "fp32"):
+            raise ValueError(f"unknown scoring mode: {scoring}")
+        probe32 = None
+        if scoring == "fp32" and dtype == "bf16":
+            probe32 = cls.from_host(config, token_embedding, list(layers)[:config.critical_layer], "f32", device)
         dev = torch.device(device)
         tdt = DTYPES[dtype][1]
 
@@ -194,7 +203,7 @@ class ModelWeights:
         tiled = use_tiled_weights(config, dtype)
         _tile_layers(dl, tiled)
         return cls(config, dtype, t(token_embedding, torch.float32), dl, ones, torch.zeros_like(ones), dev,
-                   _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR)
+                   _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR, probe32)
 
 
 def tile64(w: torch.Tensor) -> torch.Tensor:
@@ -230,11 +239,15 @@ def _get(obj, *names):
 
 
 def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
-                 layers: int | None = None) -> ModelWeights:
+                 layers: int | None = None, scoring: str = "native") -> ModelWeights:
     """GPU restatement of init_weights (model.py:225-257): stream order
     embedding, then per layer wq wk wv wo w1 w2, each row-major. GQA: wk/wv are
-    [d][Hkv*D] in the same stream order (reduces to the reference at Hkv == H)."""
+    [d][Hkv*D] in the same stream order (reduces to the reference at Hkv == H).
+    scoring="fp32" with bf16 weights also draws float32 copies of layers 1..c
+    (`probe32`, the fp32 scoring mode's probe weights)."""
     config.validate()
+    if scoring not in ("native", "fp32"):
+        raise ValueError(f"unknown scoring mode: {scoring}")
     dev = torch.device(device)
     qdt, tdt = DTYPES[dtype]
     d, f, V = config.d_model, config.d_ff, config.vocab_size
@@ -270,8 +283,11 @@ def init_weights(config: ModelConfig, dtype: str = "bf16", device="cuda",
         _tile_layers([layer], tiled)
         dl.append(layer)
     ones = torch.ones(d, dtype=torch.float32, device=dev)
+    probe32 = None
+    if scoring == "fp32" and dtype == "bf16":
+        probe32 = init_weights(config, "f32", device, layers=min(n_build, config.critical_layer))
     return ModelWeights(config, dtype, emb, dl, ones, torch.zeros_like(ones), dev,
-                        _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR)
+                        _lib.B_TILE64 if tiled else _lib.B_ROWMAJOR, probe32)
 
 
 class RopeTable:

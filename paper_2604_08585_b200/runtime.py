@@ -183,13 +183,13 @@ class Executor:
              self.w.emb.data_ptr(), cfg.vocab_size, out.data_ptr(), cuda_stream(stream))
 
     # ------------------------------------------------------------------
-    def new_table(self, n_rows: int) -> tuple[torch.Tensor, torch.Tensor]:
+    def new_table(self, n_rows: int, n_layers: int | None = None) -> tuple[torch.Tensor, torch.Tensor]:
         cfg = self.cfg
-        shape = (cfg.n_layers, n_rows, cfg.n_kv_heads, cfg.d_head)
+        shape = (cfg.n_layers if n_layers is None else n_layers, n_rows, cfg.n_kv_heads, cfg.d_head)
         return (torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device),
                 torch.empty(shape, dtype=self.w.torch_dtype, device=self.w.device))
 
-    def forward_full_batch(self, tokens: torch.Tensor, stream=None):
+    def forward_full_batch(self, tokens: torch.Tensor, stream=None, layers: range | None = None):
         """forward_full of B equal-length sequences at once: tokens [B][m] ->
         tables [L][B*m][Hkv][D] (sequence b owns rows b*m..), one layer stack
         with the batched attention (n_req = B). Every row's arithmetic is the
@@ -198,26 +198,27 @@ class Executor:
         B, m = tokens.shape
         self.rope.ensure(m + 1)
         dev = self.w.device
-        tk, tv = self.new_table(B * m)
+        tk, tv = self.new_table(B * m, None if layers is None else len(layers))
         ar = torch.arange(m, dtype=torch.int32, device=dev)
         pos = ar.repeat(B)
         dst = torch.arange(B * m, dtype=torch.int32, device=dev)
         sc = self.scratch(B * m, key=("full_batch", B * m))
         self.embed(sc, B * m, tokens.reshape(-1), stream=stream)
-        self.stack(sc, B * m, pos, dst, pos, tk, tv, stream=stream, n_req=B)
+        self.stack(sc, B * m, pos, dst, pos, tk, tv, stream=stream, n_req=B, layers=layers)
         return tk, tv
 
     def forward_full(self, tokens: torch.Tensor, start: int = 0, tab=None, want_logits_rows=None,
-                     stream=None):
+                     stream=None, layers: range | None = None):
         """Full causal forward of `tokens` at positions start.. (model.py:391-400).
-        Returns (table K, table V, x scratch). Table row i = token i."""
+        Returns (table K, table V, x scratch). Table row i = token i.
+        `layers` = range(n) runs layers 1..n only (tables hold n layers)."""
         m = tokens.numel()
         self.rope.ensure(start + m + 1)
         dev = self.w.device
-        tk, tv = tab if tab is not None else self.new_table(m)
+        tk, tv = tab if tab is not None else self.new_table(m, None if layers is None else len(layers))
         ar = torch.arange(m, dtype=torch.int32, device=dev)
         pos = ar + start
         sc = self.scratch(m, key=("full", m))
         self.embed(sc, m, tokens, stream=stream)
-        self.stack(sc, m, pos, ar, ar, tk, tv, stream=stream)
+        self.stack(sc, m, pos, ar, ar, tk, tv, stream=stream, layers=layers)
         return tk, tv, sc
