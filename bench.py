@@ -35,6 +35,13 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# the CPU legs (cpu_baseline, --impl reference) use every host core for BLAS, stated in the line
+try:
+    _N_CORES = len(os.sched_getaffinity(0))
+except Exception:
+    _N_CORES = os.cpu_count() or 1
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, str(_N_CORES))
 
 CONFIGS = {
     "llama3-8b": dict(n_layers=32, n_heads=32, d_model=4096, d_head=128, d_ff=14336,
@@ -118,7 +125,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle port on a bounded layer sample
 # ---------------------------------------------------------------------------
-def cpu_sample(cfgd: dict, chunk_kv_host, chunk_tokens, anchors, query, sample_layers: int) -> dict:
+def cpu_sample(cfgd: dict, chunk_kv_host, chunk_tokens, anchors, query, sample_layers: int, w=None) -> dict:
     """Time the oracle's fused path at full width over `sample_layers` layers
     and extrapolate each phase to the full stack (labelled as such)."""
     from oracle import qcfuse_oracle as O
@@ -127,7 +134,7 @@ def cpu_sample(cfgd: dict, chunk_kv_host, chunk_tokens, anchors, query, sample_l
                   d_model=cfgd["d_model"],
                   d_head=cfgd["d_head"], d_ff=cfgd["d_ff"], seed=1234,
                   critical_layer=2 if max(4, sample_layers) >= 4 else None)
-    w = O.init_weights(oc, layers=sample_layers)
+    w = w if w is not None else O.init_weights(oc, layers=sample_layers)
     chunks = [O.Chunk(np.asarray(t), [O.KV(k[li], v[li], np.arange(k.shape[1])) for li in range(sample_layers)],
                       np.zeros(len(t), np.float32), np.asarray(a)) for t, (k, v), a in
               zip(chunk_tokens, chunk_kv_host, anchors)]
@@ -223,6 +230,16 @@ def timed(fn, steps, warmup, stream):
     return e0.elapsed_time(e1)
 
 
+def launch_cmd(n: int, argv: list[str]) -> list[str]:
+    """The torchrun command line `--gpus n` re-executes itself under."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -252,6 +269,11 @@ def main():
 
     rank, world, local = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1),
                                                                    ("LOCAL_RANK", 0)))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N`: re-launch as N ranks (one process per GPU)
+        return os.execv(sys.executable, launch_cmd(args.gpus, sys.argv[1:]))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks for --gpus N")
     if args.impl == "reference":
         return run_reference(args, cfgd, rank)
 
@@ -264,14 +286,30 @@ def main():
     local = local % max(n_dev, 1)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if n_dev < world and not os.environ.get("QCF_BENCH_DEVICES"):
+        raise SystemExit(f"bench.py: {world} ranks but only {n_dev} visible GPU(s)")
+    dist_info = {"backend": None, "world_size": world}
     if world > 1:
         backend = os.environ.get("QCF_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=device)
+            dist.barrier()   # forces communicator creation (eager with device_id)
+            dist_info["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
         else:
             dist.init_process_group(backend)
+        dist_info["backend"] = backend
+        if rank == 0:
+            print(f"[bench] process group up: backend={backend} world={world}", file=sys.stderr)
+    devs = [torch.cuda.current_device()]
+    if world > 1:
+        got = [None] * world
+        dist.all_gather_object(got, (rank, torch.cuda.get_device_properties(device).uuid.__str__()))
+        devs = sorted({u for _, u in got})
+    dist_info["gpus_active"] = len(devs)
     from paper_2604_08585_b200 import _lib
     from paper_2604_08585_b200.dist import gather_rows, max_over_ranks
+    if args.dtype == "bf16":   # speed mode: a bf16 call leaving the tcgen05 kernels is an error
+        _lib.lib.qcf_set_strict_tc(1)
 
     Q, cfg, w, store, eng, pool_ids, chunk_toks = build_engine(cfgd, args.dtype, device, pool)
     q, ratio, B = cfgd["q"], cfgd["ratio"], args.batch
@@ -455,13 +493,14 @@ def main():
         del fb.graph
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:   # other ranks wait at the final barrier
         cpu = cpu_baseline_block(cfgd, store, pool_ids[:cfgd["n_chunks"]], np.asarray(batches[0][0][1]),
                                  sample_layers=2)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
+            "gpus_active": dist_info["gpus_active"], "dist": dist_info,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "ttft_ms": ttft_ms, "ttft_e2e_ms": ttft_e2e_ms, "batch_latency_ms": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype,
@@ -473,11 +512,14 @@ def main():
                        "model": f"{args.config} shape (L{cfg.n_layers} H{cfg.n_heads} Hkv{cfg.n_kv_heads} "
                                 f"D{cfg.d_head} F{cfg.d_ff}, reference arch: LayerNorm, ReLU FFN, tied byte vocab)",
                        "n_ctx": n_ctx, "n_selected": n_sel, "anchors": int(plans[0].anchor_rows.size - 1),
-                       "requests_per_step_per_gpu": B, "parallelism": f"request sharding x{world} (replicas)",
+                       "requests_per_step_per_gpu": B,
+                       "parallelism": "request sharding, one process per GPU, no data-path collective "
+                                      "(NCCL all-gather of results only)",
                        "l2": "inputs larger than L2 (11.8 GB weights + chunk pool + per-request fused KV)"},
             "e2e": {"value": world * B * 1e3 / e2e_ms, "unit": "requests/s", "ms_per_batch": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,
+            "simt_fallbacks": int(_lib.lib.qcf_simt_fallbacks()),
             "roofline": roofline,
             "phases_ms": {k: round(v, 4) for k, v in sorted(phases.items(), key=lambda x: -x[1])},
             "phases_ms_single_request": {k: round(v, 4) for k, v in sorted(phases_single.items(), key=lambda x: -x[1])},
@@ -490,6 +532,7 @@ def main():
         }
         print(json.dumps(out))
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -511,49 +554,79 @@ def cpu_baseline_block(cfgd, store, ids, query, sample_layers):
             "wall_s": round(time.perf_counter() - t0, 2)}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def run_reference(args, cfgd, rank):
-    """CPU oracle port timed on the host (BASELINE.md §2 plan); rank 0 only."""
+    """The reference's CPU path on the host (BASELINE.md §2 plan): the oracle
+    port of the fused path (assemble, anchor probe, score, Top-N, recompute,
+    query forward) at FULL width over a 4-layer stack (critical layer 2), one
+    request per step. `ms_per_step` is that measured 4-layer sample; `value`
+    converts it to requests/s of the full-depth request by scaling each phase
+    to the full stack (assembly/recompute/query x L/4, probe x (c-1)) --
+    labelled "extrapolated". Rank 0 only; BLAS threads = all host cores."""
     if rank != 0:
         return
     from oracle import qcfuse_oracle as O
     L = cfgd["n_layers"]
-    sample_layers = 1
-    # chunk KV for the sample layers from the oracle itself (no GPU on this arm)
+    sample_layers = min(4, L)
     oc = O.Config(n_layers=4, n_heads=cfgd["n_heads"], n_kv_heads=cfgd.get("n_kv_heads"), d_model=cfgd["d_model"],
-                  d_head=cfgd["d_head"],
-                  d_ff=cfgd["d_ff"], seed=1234)
-    w1 = O.init_weights(oc, layers=sample_layers)
+                  d_head=cfgd["d_head"], d_ff=cfgd["d_ff"], seed=1234)
+    t_init = time.perf_counter()
+    w4 = O.init_weights(oc, layers=sample_layers)
+    # chunk KV for the sample layers from the oracle itself (no GPU on this arm)
     toks = [np.random.default_rng(i).integers(0, 256, cfgd["chunk_len"]) for i in range(cfgd["n_chunks"])]
     kv, anchors = [], []
     for t in toks:
-        tr = O.forward(w1, t, np.arange(t.size), None, layers=sample_layers)
+        tr = O.forward(w4, t, np.arange(t.size), None, layers=sample_layers)
         k = np.stack([x.keys for x in tr.kv])
         v = np.stack([x.values for x in tr.kv])
-        norms = np.linalg.norm(k[0], axis=2).mean(axis=1)
+        norms = np.linalg.norm(k[oc.critical_layer - 1], axis=2).mean(axis=1)
         kv.append((k, v))
         anchors.append(O.extract_anchors(norms, 0.05))
+    setup_s = time.perf_counter() - t_init
     # the whole arm stays within a few minutes: once the time budget is spent the
     # remaining steps are not sampled and the line says how many were
     budget = float(os.environ.get("QCF_REF_BUDGET_S", "150"))
     t_start = time.perf_counter()
-    times = []
+    samples, extrap = [], []
     for i in range(args.warmup + args.steps):
         if i > args.warmup and time.perf_counter() - t_start > budget:
             break
         qt = np.random.default_rng(10_000 + i).integers(0, 256, cfgd["q"])
-        r = cpu_sample(cfgd, kv, toks, anchors, qt, sample_layers)
+        r = cpu_sample(cfgd, kv, toks, anchors, qt, sample_layers, w=w4)
         if i >= args.warmup:
-            times.append(r["extrapolated_request_s"])
-    per = float(np.mean(times))
+            samples.append(r["sample_s"])
+            extrap.append(r["extrapolated_request_s"])
+    per = float(np.mean(extrap))
+    sample_ms = float(np.mean(samples)) * 1e3
+    cores = cpu_cores()
     out = {"metric": METRIC, "impl": "reference", "value": 1.0 / per, "unit": "requests/s", "n_gpus": 1,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "ttft_ms": per * 1e3,
+           "steps": len(samples), "steps_requested": args.steps, "warmup": args.warmup,
+           "ms_per_step": sample_ms, "ttft_ms": per * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic", "config": {"workload": f"{args.config}: {cfgd['n_chunks']}x{cfgd['chunk_len']}, "
                                                        f"q={cfgd['q']}, recompute {cfgd['ratio']:.0%}, QCFuse"},
-           "cpu_baseline": {"value": 1.0 / per, "unit": "requests/s", "cores": cpu_cores(), "kind": "port",
-                            "sample": f"oracle numpy port, full width, {sample_layers} of {L} layers per phase, "
-                                      f"extrapolated to {L} layers; {len(times)} of {args.steps} steps sampled "
-                                      f"within the {budget:.0f} s budget"},
+           "measured": {"layers": sample_layers, "ms_per_request_sample": sample_ms,
+                        "what": f"one request's fused path at full width over {sample_layers} layers "
+                                f"(critical layer {oc.critical_layer}), measured"},
+           "extrapolated": {"layers": L, "ms_per_request": per * 1e3,
+                            "what": f"per-phase measured times scaled to {L} layers (probe to layer {math.ceil(L / 2) - 1})"},
+           "host": {"cpu_model": cpu_model(), "cores": cores,
+                    "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", str(cores)), "setup_s": round(setup_s, 1)},
+           "cpu_baseline": {"value": 1.0 / per, "unit": "requests/s", "cores": cores, "kind": "port",
+                            "sample": f"oracle numpy port (threaded BLAS matmul; the reference's einsum is "
+                                      f"unthreaded), full width, {sample_layers} of {L} layers measured per step, "
+                                      f"extrapolated to {L}; {len(samples)} of {args.steps} steps sampled "
+                                      f"within the {budget:.0f} s budget; one request at a time (the "
+                                      f"reference has no batching)"},
            "e2e": {"value": 1.0 / per, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

@@ -199,6 +199,13 @@ int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int64_t ldb, in
 /* ---- location-aware attention: fusion.py:194-208 -> model.py:326-338 -------
  * out[i,h] = sum_{j<=kmax[i]} softmax_j(q[i,h].k[j,h/(H/Hkv)] / float(sqrt(D))) v[j]
  * q/out [M][H][D], k/v table [n_keys][Hkv][D]; kmax inclusive, < n_keys. */
+/* Arbitrary visibility (the public sparse_attention, fusion.py:194-208):
+ * key j visible to row i iff j <= kmax[i] and bit (j & 31) of
+ * mask[i*mask_words + j/32] is set; every row needs one visible key. SIMT
+ * (FFMA) kernel, float32 softmax; q/out [M][H][D], k/v [n_keys][Hkv][D]. */
+int qcf_attention_masked(int dtype, const void* q, const void* k, const void* v, const int32_t* kmax,
+                         const uint32_t* mask, int64_t mask_words, int64_t m, int h, int hkv, int d,
+                         int64_t n_keys, void* out, qcf_stream_t stream);
 int qcf_attention(int dtype, const void* q, const void* k, const void* v,
                   const int32_t* kmax, int64_t m, int h, int hkv, int d,
                   int64_t n_keys, void* out, qcf_stream_t stream);

@@ -66,6 +66,7 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_gemm_qkv_rope": (_I, [_P, _I64, _P, _I64, _I, _I64, _I64, _I, _I, _I, _P, _P, _P, _I64, _P, _P, _P, _P,
                                _SZ, _P]),
     "qcf_attention": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I64, _P, _P]),
+    "qcf_attention_masked": (_I, [_I, _P, _P, _P, _P, _P, _I64, _I64, _I, _I, _I, _I64, _P, _P]),
     "qcf_attention_batched": (_I, [_I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _I64, _P, _P]),
     "qcf_attention_workspace": (_SZ, [_I64, _I, _I, _I64]),
     "qcf_attention_split": (_I, [_I64, _I, _I, _I64]),

@@ -4,6 +4,9 @@
 // divided by float32(sqrt(D)) and max-subtracted softmax as model.py:326-338.
 // A CTA owns 32 query rows x one head; K/V tiles of 32 keys stream through
 // shared memory and are reused by all 32 rows; online softmax in fp32.
+// An optional bit mask [m][mask_words] (bit j of row i = key j visible) narrows
+// the visible set further: the public sparse_attention's arbitrary `visible`
+// masks (fusion.py:194-208, test_fusion.py:205-248).
 #include <math.h>
 
 #include "attention.cuh"
@@ -18,7 +21,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
                                                         const T* __restrict__ v,
                                                         const int32_t* __restrict__ kmax, int64_t m,
                                                         int h, int hkv, int64_t n_keys,
-                                                        T* __restrict__ out) {
+                                                        T* __restrict__ out,
+                                                        const uint32_t* __restrict__ mask, int64_t mask_words) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float sm[];
@@ -90,6 +94,9 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
       for (int c = 0; c < D; ++c) acc = fmaf(Qs[row * (D + 1) + c], Ks[j * (D + 1) + c], acc);
       acc = acc / inv_scale_div;
       if (k0 + j > my_kmax) acc = -INFINITY;
+      if (mask != nullptr && r0 + row < m && k0 + j < n_keys &&
+          !((mask[(req * m + r0 + row) * mask_words + ((k0 + j) >> 5)] >> ((k0 + j) & 31)) & 1u))
+        acc = -INFINITY;
       s[jj] = acc;
       tmax = fmaxf(tmax, acc);
     }
@@ -134,7 +141,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
 
 template <typename T, int D>
 static int launch_simt(const void* q, const void* k, const void* v, const int32_t* kmax, int64_t m,
-                       int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
+                       int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req,
+                       const uint32_t* mask, int64_t mask_words) {
   const size_t smem = sizeof(float) * (AQ * (D + 1) + AK * (D + 1) + AK * D + AQ * (AK + 1));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(attn_simt_kernel<T, D>,
@@ -143,20 +151,21 @@ static int launch_simt(const void* q, const void* k, const void* v, const int32_
   }
   dim3 grid(ceil_div(m, AQ), h, n_req);
   QCF_LAUNCH("attn_simt_kernel", attn_simt_kernel<T, D>, dim3(grid), dim3(128), smem, s, (const T*)q, (const T*)k, (const T*)v, kmax, m, h,
-                                                 hkv, n_keys, (T*)out);
+                                                 hkv, n_keys, (T*)out, mask, mask_words);
   QCF_LAUNCH_CHECK("qcf_attention(simt)");
   return QCF_OK;
 }
 
 template <typename T>
 static int dispatch_d(int d, const void* q, const void* k, const void* v, const int32_t* kmax,
-                      int64_t m, int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req) {
+                      int64_t m, int h, int hkv, int64_t n_keys, void* out, cudaStream_t s, int n_req,
+                      const uint32_t* mask, int64_t mw) {
   switch (d) {
-    case 8: return launch_simt<T, 8>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
-    case 16: return launch_simt<T, 16>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
-    case 32: return launch_simt<T, 32>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
-    case 64: return launch_simt<T, 64>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
-    case 128: return launch_simt<T, 128>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+    case 8: return launch_simt<T, 8>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mw);
+    case 16: return launch_simt<T, 16>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mw);
+    case 32: return launch_simt<T, 32>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mw);
+    case 64: return launch_simt<T, 64>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mw);
+    case 128: return launch_simt<T, 128>(q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mw);
     default: break;
   }
   set_error("qcf_attention: unsupported d_head %d (8/16/32/64/128)", d);
@@ -165,9 +174,21 @@ static int dispatch_d(int d, const void* q, const void* k, const void* v, const 
 
 int attention_simt_launch(int dtype, const void* q, const void* k, const void* v,
                           const int32_t* kmax, int64_t m, int h, int hkv, int d, int64_t n_keys,
-                          void* out, cudaStream_t s, int n_req) {
-  if (dtype == QCF_F32) return dispatch_d<float>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
-  return dispatch_d<__nv_bfloat16>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req);
+                          void* out, cudaStream_t s, int n_req, const uint32_t* mask, int64_t mask_words) {
+  if (dtype == QCF_F32) return dispatch_d<float>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mask_words);
+  return dispatch_d<__nv_bfloat16>(d, q, k, v, kmax, m, h, hkv, n_keys, out, s, n_req, mask, mask_words);
 }
 
 }  // namespace qcf
+
+extern "C" int qcf_attention_masked(int dtype, const void* q, const void* k, const void* v, const int32_t* kmax,
+                                    const uint32_t* mask, int64_t mask_words, int64_t m, int h, int hkv, int d,
+                                    int64_t n_keys, void* out, qcf_stream_t stream) {
+  QCF_REQUIRE(q && k && v && kmax && mask && out, QCF_EINVAL, "qcf_attention_masked: null pointer");
+  QCF_REQUIRE(h > 0 && hkv > 0 && h % hkv == 0 && n_keys > 0 && m >= 0, QCF_EINVAL, "qcf_attention_masked: bad shape");
+  QCF_REQUIRE(mask_words >= (n_keys + 31) / 32, QCF_ESHAPE, "qcf_attention_masked: mask rows too short");
+  QCF_REQUIRE(dtype == QCF_F32 || dtype == QCF_BF16, QCF_EINVAL, "qcf_attention_masked: bad dtype");
+  if (m == 0) return QCF_OK;
+  return qcf::attention_simt_launch(dtype, q, k, v, kmax, m, h, hkv, d, n_keys, out, qcf::as_stream(stream), 1, mask,
+                                    mask_words);
+}

@@ -330,9 +330,11 @@ def random_select(seed: int, n_ctx: int, ratio: float) -> SelectionResult:
 
 
 def sparse_attention(q, positions, keys, values, visible) -> np.ndarray:
-    """Attention of scattered rows over a KV table (fusion.py:194-208), on the
-    device. The location-aware kernel covers prefix-visibility masks (row i
-    sees keys 0..kmax[i], the only masks the fused path produces)."""
+    """Attention of scattered rows over a KV table (fusion.py:194-208) on the
+    device, for ANY visibility mask: prefix masks (row i sees keys 0..kmax[i],
+    what the fused path produces) run on the location-aware kernel, other masks
+    on `qcf_attention_masked` with the mask packed to bits. Same errors as the
+    reference (ValueError on a shape mismatch or a row with no visible key)."""
     q = np.asarray(q, np.float32)
     keys = np.asarray(keys, np.float32)
     values = np.asarray(values, np.float32)
@@ -341,20 +343,27 @@ def sparse_attention(q, positions, keys, values, visible) -> np.ndarray:
         raise ValueError("visibility mask shape mismatch")
     if not visible.any(axis=1).all():
         raise ValueError("every query row needs at least one visible key")
-    kmax = visible.shape[1] - 1 - np.argmax(visible[:, ::-1], axis=1)
-    prefix = np.arange(visible.shape[1])[None, :] <= kmax[:, None]
-    if not np.array_equal(prefix, visible):
-        raise NotImplementedError("sparse_attention: only prefix (causal-by-position) masks are "
-                                  "built on the device")
     m, H, D = q.shape
+    n = keys.shape[0]
+    kmax = n - 1 - np.argmax(visible[:, ::-1], axis=1)
+    prefix = np.arange(n)[None, :] <= kmax[:, None]
     dev = torch.device("cuda")
     tq = torch.as_tensor(q, device=dev)
     tk = torch.as_tensor(keys, device=dev)
     tv = torch.as_tensor(values, device=dev)
     out = torch.empty_like(tq)
-    call("qcf_attention", _lib.QCF_F32, tq.data_ptr(), tk.data_ptr(), tv.data_ptr(),
-         _i32(kmax, dev).data_ptr(), m, H, keys.shape[1], D, keys.shape[0], out.data_ptr(),
-         cuda_stream())
+    if np.array_equal(prefix, visible):
+        call("qcf_attention", _lib.QCF_F32, tq.data_ptr(), tk.data_ptr(), tv.data_ptr(),
+             _i32(kmax, dev).data_ptr(), m, H, keys.shape[1], D, n, out.data_ptr(), cuda_stream())
+    else:
+        words = (n + 31) // 32
+        bits = np.zeros((m, words * 32), bool)
+        bits[:, :n] = visible
+        packed = np.packbits(bits.reshape(m, words, 4, 8), axis=3, bitorder="little").reshape(m, words * 4)
+        mask = torch.as_tensor(np.ascontiguousarray(packed).view(np.uint32), device=dev)
+        call("qcf_attention_masked", _lib.QCF_F32, tq.data_ptr(), tk.data_ptr(), tv.data_ptr(),
+             _i32(kmax, dev).data_ptr(), mask.data_ptr(), words, m, H, keys.shape[1], D, n, out.data_ptr(),
+             cuda_stream())
     return out.cpu().numpy()
 
 

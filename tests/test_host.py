@@ -205,13 +205,16 @@ def test_oracle_gqa_equals_mha_with_repeated_kv_weights():
     assert np.array_equal(np.repeat(a.kv[2].keys, 2, axis=1), b.kv[2].keys)
 
 
-def _bench_reference(env_extra):
+def _bench_reference(env_extra, extra_args=(), drop=()):
     import os
     import subprocess
     import sys
     env = dict(os.environ, **env_extra)
+    for k in drop:
+        env.pop(k, None)
     return subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "tiny",
-                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True, env=env, timeout=300)
+                           "--steps", "1", "--warmup", "1", *extra_args], capture_output=True, text=True, env=env,
+                          timeout=300)
 
 
 def test_bench_reference_arm_contract():
@@ -228,5 +231,36 @@ def test_bench_reference_arm_contract():
 
 
 def test_bench_reference_arm_other_ranks_exit_silently():
-    p = _bench_reference({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    p = _bench_reference({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, ["--gpus", "2"])
     assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+def test_bench_reference_arm_reports_measured_and_extrapolated():
+    p = _bench_reference({"RANK": "0", "WORLD_SIZE": "1"})
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    assert d["measured"]["layers"] == 4 and d["extrapolated"]["layers"] == 4
+    # a step is the measured sample: steps x ms_per_step is time actually spent
+    assert abs(d["ms_per_step"] - d["measured"]["ms_per_request_sample"]) < 1e-9
+    assert d["host"]["cores"] >= 1 and d["host"]["cpu_model"]
+
+
+def test_bench_gpus_flag_must_match_world():
+    """--gpus N under a launcher with another WORLD_SIZE is an error, never a
+    mislabelled line."""
+    p = _bench_reference({"RANK": "0", "WORLD_SIZE": "1"}, ["--gpus", "2"])
+    assert p.returncode != 0 and "WORLD_SIZE" in (p.stderr + p.stdout)
+
+
+def test_bench_gpus_self_launches_n_ranks():
+    """`python bench.py --gpus 2` (no launcher) re-executes itself under
+    torch.distributed.run with 2 ranks on 127.0.0.1: rank 0 prints the line,
+    rank 1 stays silent (the reference arm needs no GPU, so the spawn is
+    exercised end to end on CPU)."""
+    import bench
+    cmd = bench.launch_cmd(2, ["--gpus", "2", "--steps", "1"])
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=2" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and cmd[-4:] == ["--gpus", "2", "--steps", "1"]
+    p = _bench_reference({}, ["--gpus", "2"], drop=("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"))
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
