@@ -580,8 +580,21 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 // (4% padding) instead of 4 x 256 rows (28%). TMEM lanes = output columns, TMEM
 // columns = activation rows, so the epilogue thread of lane n writes column n
 // of 32 consecutive rows per tcgen05.ld (warp-coalesced along the row).
-// Unit u -> (weight pair u / n_act, activation tile u % n_act): the clusters
-// running one weight pair's activation tiles side by side share it in L2.
+// Unit u -> (weight pair, activation tile) in bands of `gw` weight pairs: inside
+// a band the weight pair runs fastest, so one wave of clusters covers a compact
+// gw x (clusters / gw) block and every operand tile it reads is shared by the
+// clusters of that wave through L2. gw = 1 is the plain order (activation tile
+// fastest: each wave re-reads the WHOLE activation matrix from DRAM -- at the
+// batch shape M = 6400, K = 14336 that is 183 MB per wave, 3.4x the
+// algorithmic bytes, profiles/gemm_traffic.json).
+__device__ __forceinline__ void swap_unit(int u, int n_wp, int n_act, int gw, int& wt, int& at) {
+  const int per_band = gw * n_act;
+  const int band = u / per_band, rem = u - band * per_band;
+  const int bw = min(gw, n_wp - band * gw);   // the last band may be narrower
+  wt = band * gw + rem % bw;
+  at = rem / bw;
+}
+
 constexpr int SW_STAGES = 6;
 constexpr int SW_A_BYTES = 128 * TC_BK * 2;  // this CTA's 128 weight rows
 constexpr int SW_B_BYTES = 128 * TC_BK * 2;  // up to 128 activation rows (BNA / 2)
@@ -590,7 +603,8 @@ constexpr int SW_SMEM = SW_STAGES * SW_STAGE + 1024 + 256 + 4 * 32 * 33 * 4;  //
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                 void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int bna, int n_act) {
+                 void* __restrict__ C, int64_t ldc, int M, int N, int K, const EpiArgs ea, int bna, int n_act,
+                 int gw) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                // weights [stage]
@@ -629,8 +643,10 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
       const uint32_t stage_tx = 2 * (SW_A_BYTES + (uint32_t)xrows * 128);
       uint32_t it = 0;
       for (int u = cluster; u < n_units; u += n_clusters) {
-        const int wrow = (u / n_act) * 256 + rank * 128;
-        const int xrow = (u % n_act) * bna + rank * xrows;
+        int wt, at;
+        swap_unit(u, n_wp, n_act, gw, wt, at);
+        const int wrow = wt * 256 + rank * 128;
+        const int xrow = at * bna + rank * xrows;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % SW_STAGES;
           const uint32_t ph = (it / SW_STAGES) & 1;
@@ -680,8 +696,10 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
     uint32_t t = 0;
     for (int u = cluster; u < n_units; u += n_clusters, ++t) {
       const int acc = t & 1;
-      const int col0 = (u / n_act) * 256 + rank * 128 + g * 32;
-      const int row0 = (u % n_act) * bna;
+      int wt, at;
+      swap_unit(u, n_wp, n_act, gw, wt, at);
+      const int col0 = wt * 256 + rank * 128 + g * 32;
+      const int row0 = at * bna;
       const int rows = min(bna, M - row0);
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -1166,7 +1184,24 @@ static int launch_swap(const void* a, int64_t lda, const void* w, int64_t ldb, v
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2s_kernel, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea, bna, n_act);
+  // band width: about sqrt(clusters) weight pairs (8 on 74 clusters); QCF_SWAP_GROUP overrides (1 = plain order)
+  static int g_swap_group = -1;
+  if (g_swap_group < 0) {
+    const char* env = getenv("QCF_SWAP_GROUP");
+    g_swap_group = env ? std::max(1, atoi(env)) : 0;
+  }
+  const int n_wp = (int)((n + 255) / 256);
+  // activations that fit in L2 with room to spare (one request's ~800 rows) keep the plain
+  // order: every wave then shares the whole activation matrix from L2 (banding measured
+  // +1% TTFT there); the batch's 6400-row operands are banded
+  const bool big = (double)m * (double)k * 2.0 > 48e6;
+  int gw = g_swap_group > 0 ? g_swap_group : (big ? (int)std::lround(std::sqrt((double)clusters)) : 1);
+  gw = std::max(1, std::min(gw, n_wp));
+  // (L2 priority hints -- evict_last on the band's weights, evict_first on the
+  // activations -- were measured WORSE: 1909 vs 1047 MB at W2, since the wave's
+  // clusters share each activation k-slab through L2; tools/gemm_hint_ab.sh)
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2s_kernel, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea, bna, n_act,
+                                     gw);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 swapped pair)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 swapped pair)");
   return QCF_OK;
