@@ -388,67 +388,104 @@ class _Plan:
 
 
 class _Bufs:
-    """Device buffers for a homogeneous batch of B requests of one shape
-    (fixed addresses -> graph replay). Request b owns rows [b*R, (b+1)*R) of
-    every layer's fused table, [b*P, (b+1)*P) of the probe table and
-    [b*Mr, (b+1)*Mr) of the recompute rows; positions/kmax are per request."""
+    """Device buffers for a batch of B requests (fixed addresses -> graph
+    replay). Request b owns rows [b*R, (b+1)*R) of every layer's fused table,
+    [b*P, (b+1)*P) of the probe table, [b*Q, (b+1)*Q) of the probe rows and
+    [b*Mr, (b+1)*Mr) of the recompute rows; positions/kmax are per request.
 
-    def __init__(self, eng: "FusionEngine", plan: "_Plan", n_req: int, extra_rows: int = 0):
+    Ragged batches (requests with different chunk lengths, query lengths or
+    selection sizes) share ONE layer stack: every request's block
+    is padded to the batch maximum (R, P, Q, Mr = S + Q with S the largest
+    selection), a request's recompute rows are laid out [selected | pad |
+    query | pad], and the pad rows run at position 0 attending to BOS only and
+    write their K/V into the block's spare last row, which no real row ever
+    sees. A homogeneous batch has no pad rows and the exact layout it always
+    had."""
+
+    def __init__(self, eng: "FusionEngine", plans: list["_Plan"], extra_rows: int = 0):
         cfg, dev = eng.config, eng.device
         L, H, Hkv, D = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.d_head
         dt = eng.weights.torch_dtype
         c = cfg.critical_layer
-        n_ctx, q, n_sel, n_pre = plan.n_ctx, plan.q, plan.n_sel, plan.anchor_rows.size
-        B = self.B = n_req
-        self.R = R = 1 + n_ctx + q + extra_rows
-        self.P = P = n_pre + q
-        self.Mr = Mr = n_sel + q
-        self.n_pre = n_pre
+        B = self.B = len(plans)
+        self.n_ctx_r = [p.n_ctx for p in plans]
+        self.q_r = [p.q for p in plans]
+        self.n_sel_r = [p.n_sel for p in plans]
+        self.n_pre_r = [int(p.anchor_rows.size) for p in plans]
+        self.n_ch_r = [len(p.records) for p in plans]
+        self.ragged = len({p.shape_key() for p in plans}) > 1
+        spare = 1 if self.ragged else 0
+        self.R = R = max(1 + n + q for n, q in zip(self.n_ctx_r, self.q_r)) + extra_rows + spare
+        self.P = P = max(a + q for a, q in zip(self.n_pre_r, self.q_r)) + spare
+        self.Q = Q = max(self.q_r)
+        self.S = S = max(self.n_sel_r)
+        self.Mr = Mr = S + Q
+        self.n_ctx_max = n_ctx_max = max(self.n_ctx_r)
+        self.n_pre = self.n_pre_r[0]
         self.rows = R
+        dsz = ctypes.sizeof(ChunkDesc)
+        self.desc_off = [dsz * sum(self.n_ch_r[:r]) for r in range(B)]       # bytes into desc / adesc
+        self.delta_off = [4 * sum(self.n_ch_r[:r]) for r in range(B)]        # bytes into adelta
+        n_desc = sum(self.n_ch_r)
         self.fk = torch.empty((L, B * R, Hkv, D), dtype=dt, device=dev)
         self.fv = torch.empty_like(self.fk)
-        self.desc = torch.empty(B * len(plan.records) * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
+        self.desc = torch.empty(n_desc * dsz, dtype=torch.uint8, device=dev)
         self.tok = torch.empty(B * R, dtype=torch.int32, device=dev)
-        self.anchor_rows = torch.empty(B * max(n_pre, 1), dtype=torch.int32, device=dev)
+        self.anchor_rows = torch.empty(max(sum(self.n_pre_r), 1), dtype=torch.int32, device=dev)
         # probe prefix straight from each chunk's anchor rows (K rotated by the chunk offset)
-        self.adesc = torch.empty(B * len(plan.records) * ctypes.sizeof(ChunkDesc), dtype=torch.uint8, device=dev)
-        self.adelta = torch.empty(B * len(plan.records), dtype=torch.int32, device=dev)
-        self.max_delta = n_ctx
+        self.adesc = torch.empty(n_desc * dsz, dtype=torch.uint8, device=dev)
+        self.adelta = torch.empty(n_desc, dtype=torch.int32, device=dev)
+        self.max_delta = n_ctx_max
         self.pk = torch.empty((c, B * P, Hkv, D), dtype=dt, device=dev)
         self.pv = torch.empty_like(self.pk)
-        ar = torch.arange(q, dtype=torch.int32, device=dev)
-        rb = torch.arange(B, dtype=torch.int32, device=dev)[:, None]
-        self.p_pos = (ar + (n_ctx + 1)).repeat(B)                       # probe positions n_ctx+1..
-        self.p_kmax = (ar + n_pre).repeat(B)                            # rows in the request's probe table
-        self.p_dst = (rb * P + (ar + n_pre)[None, :]).reshape(-1).contiguous()
-        self.p_tok = (rb * R + (ar + n_ctx + 1)[None, :]).reshape(-1).contiguous()
-        self.qc = torch.empty((1, B * q, H, D), dtype=dt, device=dev)
-        self.scores = torch.empty(B * n_ctx, dtype=torch.float32, device=dev)
-        self.score_ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(n_ctx, q, B, H, Hkv)),
+        p_pos, p_kmax, p_dst, p_tok = (np.zeros(B * Q, np.int32) for _ in range(4))
+        rc_pos, rc_dst = np.zeros(B * Mr, np.int32), np.zeros(B * Mr, np.int32)
+        for r in range(B):
+            n, q, a = self.n_ctx_r[r], self.q_r[r], self.n_pre_r[r]
+            sl = slice(r * Q, (r + 1) * Q)
+            i = np.arange(Q)
+            live = i < q
+            p_pos[sl] = np.where(live, n + 1 + i, 0)                 # probe positions n_ctx+1..
+            p_kmax[sl] = np.where(live, a + i, 0)                    # rows in the request's probe table
+            p_dst[sl] = r * P + np.where(live, a + i, P - 1)
+            p_tok[sl] = r * R + np.where(live, n + 1 + i, R - 1)
+            pos = np.zeros(Mr, np.int32)                            # [selected | pad | query | pad]
+            dst = np.full(Mr, r * R + R - 1, np.int32)
+            pos[S:S + q] = n + 1 + np.arange(q)
+            dst[S:S + q] = r * R + n + 1 + np.arange(q)
+            rc_pos[r * Mr:(r + 1) * Mr] = pos
+            rc_dst[r * Mr:(r + 1) * Mr] = dst
+        t32 = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
+        self.p_pos, self.p_kmax, self.p_dst, self.p_tok = t32(p_pos), t32(p_kmax), t32(p_dst), t32(p_tok)
+        self.qc = torch.empty((1, B * Q, H, D), dtype=dt, device=dev)
+        self.scores = torch.empty(B * n_ctx_max, dtype=torch.float32, device=dev)
+        self.score_ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(n_ctx_max, Q, B, H, Hkv)),
                                     dtype=torch.uint8, device=dev)
-        self.rc_pos = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # per-request positions == kmax
-        self.rc_pos.view(B, Mr)[:, n_sel:] = ar + (n_ctx + 1)
-        self.rc_dst = torch.empty(B * Mr, dtype=torch.int32, device=dev)   # rows in the batch table
-        self.rc_dst.copy_((self.rc_pos.view(B, Mr) + rb * R).reshape(-1))
-        self.last_row = (rb[:, 0] * Mr + (Mr - 1)).contiguous()
+        self.rc_pos = t32(rc_pos)   # per-request positions == kmax (selected slots filled by Top-N)
+        self.rc_dst = t32(rc_dst)   # rows in the batch table
+        self.last_row = t32(np.asarray([r * Mr + S + self.q_r[r] - 1 for r in range(B)], np.int32))
         self.logits = torch.empty((B, cfg.vocab_size), dtype=torch.float32, device=dev)
-        self.sc_probe = eng.ex.scratch(B * q, key=("probe", id(self)))
+        self.sc_probe = eng.ex.scratch(B * Q, key=("probe", id(self)))
         self.sc_rc = eng.ex.scratch(B * Mr, key=("rc", id(self)))
-        self.fp32 = eng.fp32_scoring and plan.policy == "QCFuse" and n_sel > 0
+        self.fp32 = eng.fp32_scoring and plans[0].policy == "QCFuse" and S > 0
         if self.fp32:
             # fp32 scoring mode: float32 probe prefix, Q_c and fused critical-layer keys
             f32 = torch.float32
             self.pk32 = torch.empty((c, B * P, Hkv, D), dtype=f32, device=dev)
             self.pv32 = torch.empty_like(self.pk32)
-            self.qc32 = torch.empty((B * q, H, D), dtype=f32, device=dev)
-            self.kc32 = torch.empty((B * (1 + n_ctx), Hkv, D), dtype=f32, device=dev)
+            self.qc32 = torch.empty((B * Q, H, D), dtype=f32, device=dev)
+            self.kc32 = torch.empty((B * (1 + n_ctx_max), Hkv, D), dtype=f32, device=dev)
             self.adesc32 = torch.empty_like(self.adesc)
             self.kdesc32 = torch.empty_like(self.desc)
-            self.sc_probe32 = eng.ex32.scratch(B * q, key=("probe32", id(self)))
+            self.sc_probe32 = eng.ex32.scratch(B * Q, key=("probe32", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
         self.rope_key: tuple | None = None   # RoPE table pointers the graph baked in
         self.h_staged: list[torch.Tensor] | None = None   # pinned host mirrors of staged()
         self.h_done: torch.cuda.Event | None = None
+
+    def selection(self, r: int) -> torch.Tensor:
+        """Request r's selected positions (device, ascending)."""
+        return self.rc_pos[r * self.Mr: r * self.Mr + self.n_sel_r[r]]
 
     def staged(self) -> list[torch.Tensor]:
         """The device tensors a batch's host inputs are staged into (swapped
@@ -860,12 +897,12 @@ class FusionEngine:
     def _buffers(self, plans: list[_Plan], extra_rows: int = 0) -> _Bufs:
         """Per-shape buffers + graph, least-recently-used first out: at most
         `max_shapes` shapes stay resident (each holds a full fused table)."""
-        key = (plans[0].shape_key(), len(plans), extra_rows)
+        key = (tuple(p.shape_key() for p in plans), extra_rows)
         b = self._bufs.pop(key, None)
         if b is None:
             while len(self._bufs) >= max(1, self.max_shapes):
                 self._evict(next(iter(self._bufs)))
-            b = _Bufs(self, plans[0], len(plans), extra_rows)
+            b = _Bufs(self, plans, extra_rows)
         self._bufs[key] = b      # most recently used last
         return b
 
@@ -916,15 +953,15 @@ class FusionEngine:
         return {"h2d": sum(h.numel() * h.element_size() for h in host)}
 
     def _launch(self, plans: list[_Plan], b: _Bufs, stream=None) -> None:
-        """Every kernel of one (batched) fused prefill, in order (module docstring)."""
+        """Every kernel of one (batched) fused prefill, in order (module docstring).
+        Ragged batches run the same launches over the padded blocks (_Bufs);
+        only scoring and Top-N go request by request there."""
         cfg, ex, plan = self.config, self.ex, plans[0]
-        c, q, n_ctx, n_sel, B = cfg.critical_layer, plan.q, plan.n_ctx, plan.n_sel, b.B
+        c, B, Q = cfg.critical_layer, b.B, b.Q
         s = cuda_stream(stream)
         row_elems = cfg.n_kv_heads * cfg.d_head
         esz = b.fk.element_size()
-        nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
-        n_ch = len(plan.records)
-        probe = plan.policy == "QCFuse" and n_sel > 0
+        probe = plan.policy == "QCFuse" and b.S > 0
         main = stream or torch.cuda.current_stream()
         # K1 (assembly, HBM-bound on the chunk pool) runs on a side stream, layer range
         # by layer range: the critical layer first (scoring reads it, overlapping the
@@ -941,8 +978,8 @@ class FusionEngine:
             nonlocal last
             for l0, nl in rngs:
                 for r in range(B):   # request r's slice of the batch table, layers [l0, l0+nl)
-                    self._assemble_range(plan.records, n_ctx, _view_rows(b.fk, r * b.R),
-                                         _view_rows(b.fv, r * b.R), _DescView(b.desc, r * nd), l0, nl, aux,
+                    self._assemble_range(plans[r].records, plans[r].n_ctx, _view_rows(b.fk, r * b.R),
+                                         _view_rows(b.fv, r * b.R), _DescView(b.desc, b.desc_off[r]), l0, nl, aux,
                                          layer_stride=b.fk.stride(0))
                 e = torch.cuda.Event()
                 e.record(aux)
@@ -950,7 +987,7 @@ class FusionEngine:
                 for l in range(l0, l0 + nl):
                     layer_ready[l] = e
 
-        if B * n_ch > 0:
+        if sum(b.n_ch_r) > 0:
             if self._aux is None:
                 self._aux = torch.cuda.Stream(device=self.device)
             aux = self._aux if self.pipeline_asm else main
@@ -980,33 +1017,36 @@ class FusionEngine:
             if e is not None:
                 main.wait_event(e)
         if probe and b.fp32:
-            self._probe_score_fp32(plan, b, stream)
+            self._probe_score_fp32(plans, b, stream)
         elif probe:
             for r in range(B):   # K2: probe prefix rows of request r from the chunks' anchor rows
-                call("qcf_assemble_rot", b.adesc.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k.data_ptr(),
-                     self._bos_v.data_ptr(), b.pk.data_ptr() + r * b.P * row_elems * esz,
+                call("qcf_assemble_rot", b.adesc.data_ptr() + b.desc_off[r], b.n_ch_r[r], b.n_pre_r[r] - 1,
+                     self._bos_k.data_ptr(), self._bos_v.data_ptr(), b.pk.data_ptr() + r * b.P * row_elems * esz,
                      b.pv.data_ptr() + r * b.P * row_elems * esz, b.pk.stride(0), c, cfg.n_kv_heads, cfg.d_head,
                      self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(), self.ex.rope.n_pos,
-                     b.adelta.data_ptr() + r * n_ch * 4, b.max_delta, self.weights.qcf_dtype, s)
-            # K3: probe layers 1..c-1 + layer c's Q, all B*q rows at once
-            ex.embed(b.sc_probe, B * q, b.tok, rows=b.p_tok, stream=stream)
+                     b.adelta.data_ptr() + b.delta_off[r], b.max_delta, self.weights.qcf_dtype, s)
+            # K3: probe layers 1..c-1 + layer c's Q, all B*Q rows at once
+            ex.embed(b.sc_probe, B * Q, b.tok, rows=b.p_tok, stream=stream)
             for li in range(c - 1):
-                ex.layer(li, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[li], b.pv[li], stream=stream,
+                ex.layer(li, b.sc_probe, B * Q, b.p_pos, b.p_dst, b.p_kmax, b.pk[li], b.pv[li], stream=stream,
                          n_req=B)
-            ex.layer(c - 1, b.sc_probe, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
+            ex.layer(c - 1, b.sc_probe, B * Q, b.p_pos, b.p_dst, b.p_kmax, b.pk[c - 1], b.pv[c - 1],
                      q_only=True, q_out=b.qc[0], stream=stream, n_req=B)
             wait_layer(c - 1)
-            # K4: scoring of the whole batch (request r's keys at rows r*R+1.. of layer c)
-            self._score_dev(b.qc[0], b.fk[c - 1, 1:], n_ctx, b.scores, b.score_ws, stream, n_req=B,
-                            k_req_stride=b.R * row_elems)
+            # K4: scoring (request r's keys at rows r*R+1.. of layer c)
+            if not b.ragged:
+                self._score_dev(b.qc[0], b.fk[c - 1, 1:], b.n_ctx_max, b.scores, b.score_ws, stream, n_req=B,
+                                k_req_stride=b.R * row_elems)
+            else:
+                for r in range(B):
+                    self._score_dev(b.qc[0, r * Q: r * Q + b.q_r[r]], b.fk[c - 1, r * b.R + 1:], b.n_ctx_r[r],
+                                    b.scores[r * b.n_ctx_max:], b.score_ws, stream)
         if probe:
-            # K5: Top-N of every request (ascending positions -> rc_pos, table rows -> rc_dst)
-            call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
-                 b.rc_dst.data_ptr(), b.R, s)
+            self._topn_all(b, s)
         elif plan.policy == "FullCompute":
             for r in range(B):
-                call("qcf_iota", n_sel, 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
-                call("qcf_iota", n_sel, 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+                call("qcf_iota", b.n_sel_r[r], 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
+                call("qcf_iota", b.n_sel_r[r], 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
         if pending:   # the remaining layers' assembly starts with the recompute
             ev = torch.cuda.Event()
             ev.record(main)
@@ -1020,39 +1060,58 @@ class FusionEngine:
             main.wait_event(last)
         ex.lm_head(b.sc_rc, b.last_row, b.logits, stream=stream)
 
-    def _probe_score_fp32(self, plan: _Plan, b: _Bufs, stream=None) -> None:
+    @staticmethod
+    def _topn_all(b: _Bufs, s) -> None:
+        """K5: Top-N of every request (ascending positions -> rc_pos, table rows
+        -> rc_dst): one launch for a homogeneous batch; per request otherwise
+        (its own context length and N; rc_dst = positions + the block's base)."""
+        if not b.ragged:
+            call("qcf_topn_batched", b.scores.data_ptr(), b.n_ctx_max, b.B, b.S, 1, b.rc_pos.data_ptr(), b.Mr,
+                 b.rc_dst.data_ptr(), b.R, s)
+            return
+        for r in range(b.B):
+            if b.n_sel_r[r] == 0:
+                continue
+            pos = b.rc_pos.data_ptr() + r * b.Mr * 4
+            call("qcf_topn_batched", b.scores.data_ptr() + r * b.n_ctx_max * 4, b.n_ctx_r[r], 1, b.n_sel_r[r], 1,
+                 pos, b.n_sel_r[r], None, 0, s)
+            call("qcf_iota_add", pos, b.n_sel_r[r], r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
+
+    def _probe_score_fp32(self, plans: list[_Plan], b: _Bufs, stream=None) -> None:
         """K2-K4 of the fp32 scoring mode: the probe prefix from the float32
         anchor rows (fusion.py:281-303), the probe's layers 1..c-1 plus layer c's
         Q on the float32 weights (FFMA GEMMs, float64 RoPE; model.py:345-388),
         the float32 fused critical-layer keys assembled from each chunk's float32
         K_c (fusion.py:234-263), and the float64 scoring of fusion.py:313-326."""
         cfg, ex32 = self.config, self.ex32
-        c, q, n_ctx, B = cfg.critical_layer, plan.q, plan.n_ctx, b.B
+        c, B, Q = cfg.critical_layer, b.B, b.Q
         s = cuda_stream(stream)
         row_elems = cfg.n_kv_heads * cfg.d_head
-        nd = len(plan.records) * ctypes.sizeof(ChunkDesc)
-        n_ch = len(plan.records)
         rope = ex32.rope
+        kstride = (1 + b.n_ctx_max) * row_elems
         for r in range(B):
-            call("qcf_assemble_rot", b.adesc32.data_ptr() + r * nd, n_ch, b.n_pre - 1, self._bos_k32.data_ptr(),
-                 self._bos_v32.data_ptr(), b.pk32.data_ptr() + r * b.P * row_elems * 4,
+            call("qcf_assemble_rot", b.adesc32.data_ptr() + b.desc_off[r], b.n_ch_r[r], b.n_pre_r[r] - 1,
+                 self._bos_k32.data_ptr(), self._bos_v32.data_ptr(), b.pk32.data_ptr() + r * b.P * row_elems * 4,
                  b.pv32.data_ptr() + r * b.P * row_elems * 4, b.pk32.stride(0), c, cfg.n_kv_heads, cfg.d_head,
-                 rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, b.adelta.data_ptr() + r * n_ch * 4,
+                 rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, b.adelta.data_ptr() + b.delta_off[r],
                  b.max_delta, _lib.QCF_F32, s)
-            kc = b.kc32.data_ptr() + r * (1 + n_ctx) * row_elems * 4
-            call("qcf_assemble", b.kdesc32.data_ptr() + r * nd, n_ch, n_ctx, self._bos_k32[c - 1].data_ptr(), None,
-                 kc, None, (1 + n_ctx) * row_elems, 1, cfg.n_kv_heads, cfg.d_head, rope.cos.data_ptr(),
-                 rope.sin.data_ptr(), rope.n_pos, _lib.QCF_F32, s)
+            call("qcf_assemble", b.kdesc32.data_ptr() + b.desc_off[r], b.n_ch_r[r], b.n_ctx_r[r],
+                 self._bos_k32[c - 1].data_ptr(), None, b.kc32.data_ptr() + r * kstride * 4, None, kstride, 1,
+                 cfg.n_kv_heads, cfg.d_head, rope.cos.data_ptr(), rope.sin.data_ptr(), rope.n_pos, _lib.QCF_F32, s)
         sc = b.sc_probe32
-        ex32.embed(sc, B * q, b.tok, rows=b.p_tok, stream=stream)
+        ex32.embed(sc, B * Q, b.tok, rows=b.p_tok, stream=stream)
         for li in range(c - 1):
-            ex32.layer(li, sc, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[li], b.pv32[li], stream=stream, n_req=B)
-        ex32.layer(c - 1, sc, B * q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[c - 1], b.pv32[c - 1],
+            ex32.layer(li, sc, B * Q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[li], b.pv32[li], stream=stream, n_req=B)
+        ex32.layer(c - 1, sc, B * Q, b.p_pos, b.p_dst, b.p_kmax, b.pk32[c - 1], b.pv32[c - 1],
                    q_only=True, q_out=b.qc32, stream=stream, n_req=B)
-        call("qcf_score_batched", _lib.QCF_F32, b.qc32.data_ptr(), b.kc32[1:].data_ptr(),
-             (1 + n_ctx) * row_elems, n_ctx, q, B, cfg.n_heads, cfg.n_kv_heads, cfg.d_head,
-             1.0 / math.sqrt(cfg.d_head), 1 if self.options.query_agg == "last" else 0, 1,
-             b.scores.data_ptr(), b.score_ws.data_ptr(), b.score_ws.numel(), s)
+        agg = 1 if self.options.query_agg == "last" else 0
+        scale = 1.0 / math.sqrt(cfg.d_head)
+        groups = [(0, B, b.n_ctx_max, Q)] if not b.ragged else [(r, 1, b.n_ctx_r[r], b.q_r[r]) for r in range(B)]
+        for r0, nr, n_ctx, q in groups:
+            call("qcf_score_batched", _lib.QCF_F32, b.qc32[r0 * Q:].data_ptr(),
+                 b.kc32[r0 * (1 + b.n_ctx_max) + 1:].data_ptr(), kstride, n_ctx, q, nr, cfg.n_heads,
+                 cfg.n_kv_heads, cfg.d_head, scale, agg, 1, b.scores[r0 * b.n_ctx_max:].data_ptr(),
+                 b.score_ws.data_ptr(), b.score_ws.numel(), s)
 
     # ------------------------------------------------------------------
     # host-pool variant: layer-pipelined chunk-KV streaming (SURVEY §8f rank 3)
@@ -1089,7 +1148,7 @@ class FusionEngine:
 
         keep = []   # device descriptor arrays must outlive the launches
         if b.fp32:   # fp32 scoring: its inputs (float32 anchors, K_c) are HBM-resident
-            self._probe_score_fp32(plan, b)
+            self._probe_score_fp32(plans, b)
             call("qcf_topn_batched", b.scores.data_ptr(), n_ctx, B, n_sel, 1, b.rc_pos.data_ptr(), b.Mr,
                  b.rc_dst.data_ptr(), b.R, s)
         elif plan.policy == "QCFuse" and n_sel > 0:
@@ -1201,13 +1260,13 @@ class FusionEngine:
     @_serialized
     def prefill_batch(self, policy: str, ratio: float, chunk_lists, queries, use_graph: bool = True,
                       extra_rows: int = 0, stream=None):
-        """Device-side fused prefill of a homogeneous batch (same chunk lengths,
-        query length and selection size) up to first-token logits.
-        Returns (plans, buffers): logits b.logits[r], selection of request r in
-        b.rc_pos[r*b.Mr : r*b.Mr + n_sel]."""
+        """Device-side fused prefill of a batch of requests (any mix of chunk
+        lengths, query lengths and selection sizes: ragged batches are padded,
+        see _Bufs) up to first-token logits. Returns (plans, buffers): logits
+        b.logits[r], selection of request r in b.selection(r)."""
         plans = [self._plan(policy, ratio, ids, qt) for ids, qt in zip(chunk_lists, queries)]
-        if any(p.shape_key() != plans[0].shape_key() for p in plans):
-            raise ValueError("prefill_batch needs requests of one shape (chunk lengths, query length)")
+        if not plans:
+            raise ValueError("empty batch")
         b = self._buffers(plans, extra_rows)
         self._stage(plans, b, queries, stream)
         self.ex.rope.ensure(b.rows + 2)
@@ -1216,6 +1275,8 @@ class FusionEngine:
         if any(r.on_host for pl in plans for r in pl.records):
             if not all(r.on_host for pl in plans for r in pl.records):
                 raise ValueError("a batch must draw all its chunks from one pool placement")
+            if b.ragged:
+                raise NotImplementedError("host-pool batches need requests of one shape")
             self._launch_host(plans, b)   # eager: two streams, per-layer events
             return plans, b
         if not use_graph:
@@ -1251,15 +1312,14 @@ class FusionEngine:
     @_serialized
     def fuse_batch(self, queries, chunk_lists, ratio: float = 0.15):
         """Batched north-star entry (BASELINE config 3): one fused prefill for
-        a homogeneous batch of RAG requests. Returns (logits [B][V] numpy,
+        a batch of RAG requests (ragged allowed). Returns (logits [B][V] numpy,
         list of selected-position arrays)."""
         qts = [byte_tokens(q) if isinstance(q, (str, bytes)) else list(q) for q in queries]
         if not qts or any(not q for q in qts):
             raise ValueError("query must be non-empty")
         plans, b = self.prefill_batch("QCFuse", ratio, chunk_lists, qts)
-        n = plans[0].n_sel
-        sel = b.rc_pos.view(b.B, b.Mr)[:, :n].cpu().numpy().astype(np.int64)
-        return b.logits.cpu().numpy(), [sel[r] for r in range(b.B)]
+        pos = b.rc_pos.view(b.B, b.Mr).cpu().numpy().astype(np.int64)
+        return b.logits.cpu().numpy(), [pos[r, :b.n_sel_r[r]] for r in range(b.B)]
 
     @_serialized
     def fuse(self, query, chunk_ids, ratio: float = 0.15):

@@ -228,3 +228,49 @@ def baseline_fixtures():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "baselines":
     baseline_fixtures()
+
+
+def calibration_fixtures():
+    """The reference's calibrate_layer (bench.py:118-144) on a 6-layer config
+    (candidate layers 2..5) over text chunks it retrieves itself
+    (cases.retrieve): records the chunk token lists each query retrieved, the
+    per-layer mean overlaps and the recommended layer -> calibrate.npz."""
+    model, store_mod, fusion = _import_reference()
+    import qcfuse.bench as bench  # noqa: E402
+    import qcfuse.cases as cases  # noqa: E402
+    cfg = model.ModelConfig(n_layers=6, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=4321)
+    w = model.init_weights(cfg)
+    texts = ["the quick brown fox jumps over the lazy dog near the river bank",
+             "a fused cache keeps the keys and values of every retrieved chunk",
+             "rotary position embeddings rotate pairs of key dimensions by angle",
+             "selective recompute refreshes the tokens the query attends to most",
+             "the river bank was flooded after the storm and the fox swam across",
+             "values are copied while keys are re-rotated to their fused offsets"]
+    queries = ["which tokens does the query attend to", "where did the fox swim", "how are keys rotated"]
+    tmp = Path(tempfile.mkdtemp(prefix="qcf-golden-"))
+    out = {"cfg": json.dumps(cfg.to_dict()), "ratio": 0.2, "top_k": 3, "n_queries": len(queries)}
+    try:
+        st = store_mod.ChunkStore(tmp / "store", cfg)
+        eng = fusion.FusionEngine(w, st)
+        for i, t in enumerate(texts):
+            toks = [int(b) for b in t.encode("utf-8")]
+            st.precompute(w, toks, 0.05, f"t{i}")
+            out[f"text{i}_tokens"] = np.asarray(toks, np.int64)
+        out["n_texts"] = len(texts)
+        res = bench.calibrate_layer(eng, queries, ratio=0.2, top_k=3)
+        for qi, q in enumerate(queries):
+            out[f"query{qi}"] = np.asarray(list(q.encode("utf-8")), np.int64)
+            ids = cases.retrieve(st, q, 3)
+            for ci, cid in enumerate(ids):
+                out[f"query{qi}_chunk{ci}_tokens"] = np.asarray(st.load_meta(cid).token_ids, np.int64)
+        out["recommended"] = int(res["recommended"])
+        out["layers"] = np.asarray(sorted(res["mean_overlap"]), np.int64)
+        out["mean_overlap"] = np.asarray([res["mean_overlap"][k] for k in sorted(res["mean_overlap"])], np.float64)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    np.savez_compressed(HERE / "calibrate.npz", **out)
+    print("wrote", HERE / "calibrate.npz", out["recommended"], out["mean_overlap"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "calibrate":
+    calibration_fixtures()

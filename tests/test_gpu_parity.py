@@ -837,3 +837,69 @@ def test_ratio_one_oracle_equivalence_20_seeds(tmp_path):
         assert np.abs(res.first_logits - cpu).max() < 1e-4, f"case {case}: vs CPU oracle"
     elapsed = time.time() - started
     assert elapsed < 60.0, f"took {elapsed:.1f} s"
+
+
+def test_calibrate_layer_matches_reference_golden(golden_dir, tmp_path):
+    """calibrate_layer (reference bench.py:118-144) on the chunks the reference
+    retrieved for each query (tests/golden/calibrate.npz, made by running the
+    reference): same per-layer mean overlaps and the same recommended layer."""
+    import json
+
+    import paper_2604_08585_b200 as Q
+    from paper_2604_08585_b200.calibrate import calibrate_layer
+    z = np.load(golden_dir / "calibrate.npz")
+    d = json.loads(str(z["cfg"]))
+    cfg = Q.ModelConfig(**{k: d[k] for k in ("n_layers", "n_heads", "d_model", "d_head", "d_ff", "rope_theta",
+                                              "ln_eps", "seed", "critical_layer")})
+    w = Q.init_weights(cfg, dtype="f32")
+    store = Q.ChunkStore(tmp_path, cfg, dtype="f32", persist=False)
+    for i in range(int(z["n_texts"])):
+        store.precompute(w, z[f"text{i}_tokens"], 0.05, f"t{i}")
+    eng = Q.FusionEngine(w, store)
+    lists, queries = [], []
+    for qi in range(int(z["n_queries"])):
+        lists.append([Q.chunk_hash(z[f"query{qi}_chunk{ci}_tokens"]) for ci in range(int(z["top_k"]))])
+        queries.append(z[f"query{qi}"].tolist())
+    res = calibrate_layer(eng, lists, queries, ratio=float(z["ratio"]))
+    got = np.asarray([res["mean_overlap"][int(l)] for l in z["layers"]])
+    assert np.allclose(got, z["mean_overlap"], atol=1e-12), (got, z["mean_overlap"])
+    assert res["recommended"] == int(z["recommended"])
+
+
+@pytest.mark.parametrize("dtype,scoring", [("f32", "native"), ("bf16", "native"), ("bf16", "fp32")])
+def test_ragged_batch_equals_single_requests(tmp_path, dtype, scoring):
+    """A RAGGED batch (different chunk counts and lengths, query lengths and
+    hence selection sizes) runs as one padded layer stack and gives
+    every request what it gets alone: f32 bit-exact; bf16 against the oracle
+    within the stated tolerance is covered per request by
+    test_gpu_bf16_parity.py, here selection and logits track the single-request
+    run (the fp32-scoring selection bit-exactly)."""
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=98)
+    w = Q.init_weights(cfg, dtype=dtype, scoring=scoring)
+    store = Q.ChunkStore(tmp_path / "s", cfg, dtype=dtype, persist=False, scoring=scoring)
+    eng = Q.FusionEngine(w, store)
+    lens = [96, 64, 130, 96, 48, 200, 96]
+    pool = [store.precompute(w, np.random.default_rng(i).integers(0, 256, n), 0.05).chunk_id
+            for i, n in enumerate(lens)]
+    rng = np.random.default_rng(4)
+    reqs = [[pool[j] for j in rng.permutation(len(pool))[:k]] for k in (3, 1, 4, 2, 3)]
+    queries = [rng.integers(0, 256, n).tolist() for n in (12, 5, 20, 1, 12)]
+    for use_graph in (False, True):
+        plans, b = eng.prefill_batch("QCFuse", 0.2, reqs, queries, use_graph=use_graph)
+        assert b.ragged
+        for r in range(len(reqs)):
+            logits, sel = eng.fuse(queries[r], reqs[r], 0.2)
+            bsel = b.selection(r).cpu().numpy()
+            blog = b.logits[r].cpu().numpy()
+            assert bsel.size == plans[r].n_sel
+            if dtype == "f32" or scoring == "fp32":
+                assert np.array_equal(bsel, sel), r
+            if dtype == "f32":
+                assert np.array_equal(blog, logits), r
+            else:
+                assert len(set(bsel.tolist()) & set(sel.tolist())) >= 0.95 * sel.size
+                assert np.abs(blog - logits).max() < 2e-2 * np.abs(logits).max()
+    # the public batched entry returns each request's own selection
+    lg, sels = eng.fuse_batch(queries, reqs, 0.2)
+    assert [s.size for s in sels] == [p.n_sel for p in plans]
