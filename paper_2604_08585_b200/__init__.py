@@ -10,5 +10,6 @@ from .fusion import (POLICIES, PROBE_ANCHORS, PROBE_FULL, PROBE_NONE, FusedConte
                      sparse_attention, top_n_positions)
 from .pipeline import CostModel
 from .calibrate import calibrate_layer, layer_overlaps
+from .serving import BatchingFrontend
 
 __all__ = [n for n in dir() if not n.startswith("_")]

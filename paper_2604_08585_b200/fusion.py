@@ -480,6 +480,7 @@ class _Bufs:
             self.sc_probe32 = eng.ex32.scratch(B * Q, key=("probe32", id(self)))
         self.graph: torch.cuda.CUDAGraph | None = None
         self.rope_key: tuple | None = None   # RoPE table pointers the graph baked in
+        self.uses = 0
         self.h_staged: list[torch.Tensor] | None = None   # pinned host mirrors of staged()
         self.h_done: torch.cuda.Event | None = None
 
@@ -1279,7 +1280,10 @@ class FusionEngine:
                 raise NotImplementedError("host-pool batches need requests of one shape")
             self._launch_host(plans, b)   # eager: two streams, per-layer events
             return plans, b
-        if not use_graph:
+        b.uses += 1
+        if not use_graph or (b.ragged and b.uses < 2):
+            # a ragged batch composition is captured only once it repeats (a serving
+            # loop's compositions mostly do not; capture costs more than one launch)
             self._launch(plans, b, stream)
             return plans, b
         rope_key = tuple((r.cos.data_ptr(), r.sin.data_ptr(), r.cs32.data_ptr(), r.n_pos)

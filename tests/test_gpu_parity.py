@@ -903,3 +903,32 @@ def test_ragged_batch_equals_single_requests(tmp_path, dtype, scoring):
     # the public batched entry returns each request's own selection
     lg, sels = eng.fuse_batch(queries, reqs, 0.2)
     assert [s.size for s in sels] == [p.n_sel for p in plans]
+
+
+def test_batching_frontend_concurrent_threads(tmp_path):
+    """Concurrent Python threads (the reference's FastAPI pattern) submit to the
+    dynamic batcher: requests of different shapes are served in shared ragged
+    batches, and each caller gets exactly what fuse() gives its request alone
+    (f32 parity mode: bit-exact)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2604_08585_b200 as Q
+    cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=64, d_head=32, d_ff=128, seed=21)
+    w = Q.init_weights(cfg, dtype="f32")
+    store = Q.ChunkStore(tmp_path / "s", cfg, dtype="f32", persist=False)
+    eng = Q.FusionEngine(w, store)
+    pool = [store.precompute(w, np.random.default_rng(i).integers(0, 256, 24 + 8 * i), 0.1).chunk_id
+            for i in range(6)]
+    rng = np.random.default_rng(7)
+    reqs = [([pool[j] for j in rng.permutation(6)[:int(rng.integers(1, 4))]],
+             rng.integers(0, 256, int(rng.integers(2, 9))).tolist()) for _ in range(16)]
+    alone = [eng.fuse(q, ids, 0.25) for ids, q in reqs]
+    with Q.BatchingFrontend(eng, max_batch=8, max_wait_ms=20.0) as fe:
+        with ThreadPoolExecutor(16) as pool_ex:
+            futs = [pool_ex.submit(fe.fuse, q, ids, 0.25) for ids, q in reqs]
+            got = [f.result() for f in futs]
+        assert sum(fe.batches) == 16 and len(fe.batches) < 16
+        with pytest.raises(KeyError):
+            fe.submit([1, 2], ["ab" * 32])
+    for (l0, s0), (l1, s1) in zip(alone, got):
+        assert np.array_equal(s0, s1) and np.array_equal(l0, l1)

@@ -264,3 +264,43 @@ def test_bench_gpus_self_launches_n_ranks():
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [ln for ln in p.stdout.strip().splitlines() if ln.startswith("{")]
     assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
+
+
+def test_batching_frontend_groups_and_routes_results():
+    """Host logic of the dynamic batcher with a stand-in engine: concurrent
+    submissions are grouped into batches of <= max_batch (split by ratio), each
+    Future gets its own request's row, and a failing batch fails its callers."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2604_08585_b200.serving import BatchingFrontend
+
+    class FakeEngine:
+        def __init__(self):
+            self.store = {"a", "b", "c"}
+            self.calls = []
+            self.lock = threading.Lock()
+
+        def fuse_batch(self, queries, chunk_lists, ratio):
+            with self.lock:
+                self.calls.append((len(queries), ratio))
+            if any(q[0] == 255 for q in queries):
+                raise ValueError("boom")
+            return (np.asarray([[sum(q), ratio] for q in queries]),
+                    [np.asarray([len(c)]) for c in chunk_lists])
+
+    eng = FakeEngine()
+    with BatchingFrontend(eng, max_batch=4, max_wait_ms=50.0) as fe:
+        with ThreadPoolExecutor(10) as ex:
+            futs = [ex.submit(fe.fuse, [i, 1], ["a"] * (1 + i % 3), 0.1 if i % 2 else 0.2) for i in range(10)]
+            res = [f.result() for f in futs]
+        for i, (lg, sel) in enumerate(res):
+            assert lg.tolist() == [i + 1, 0.1 if i % 2 else 0.2] and sel.tolist() == [1 + i % 3]
+        assert all(n <= 4 for n, _ in eng.calls) and sum(n for n, _ in eng.calls) == 10
+        bad = fe.submit([255], ["a"])
+        with pytest.raises(ValueError):
+            bad.result(timeout=10)
+        with pytest.raises(KeyError):
+            fe.submit([1], ["zz"])
+        with pytest.raises(ValueError):
+            fe.submit([], ["a"])
