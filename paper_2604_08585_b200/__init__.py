@@ -11,5 +11,6 @@ from .fusion import (POLICIES, PROBE_ANCHORS, PROBE_FULL, PROBE_NONE, FusedConte
 from .pipeline import CostModel
 from .calibrate import calibrate_layer, layer_overlaps
 from .serving import BatchingFrontend
+from .sharded import ShardedChunkStore
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -9,6 +9,7 @@ The second half restates the reference's own test_fusion.py cases against the
 B200 engine (same assertions, same tolerances)."""
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -932,3 +933,32 @@ def test_batching_frontend_concurrent_threads(tmp_path):
             fe.submit([1, 2], ["ab" * 32])
     for (l0, s0), (l1, s1) in zip(alone, got):
         assert np.array_equal(s0, s1) and np.array_equal(l0, l1)
+
+
+def test_sharded_pool_p2p(tmp_path):
+    """ShardedChunkStore: two ranks each own half of the
+    chunk pool and map the other's through CUDA IPC; fused prefills that draw
+    chunks from both shards read the peer's HBM in place and equal a local pool
+    bit for bit, and the oracle on the same chunk KV (selection bit-exact,
+    logits 1e-4). Both ranks share this box's one GPU here (the same IPC path
+    a multi-GPU node uses over NVLink)."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    worker = str(Path(__file__).resolve().parent / "sharded_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), "2", str(port), str(tmp_path)],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-3000:]
+    for r in range(2):
+        rep = json.loads((tmp_path / f"rank{r}.json").read_text())
+        assert rep["remote"] > 0 and rep["owners"] == [0, 1]
+        assert any(c["remote_chunks"] > 0 for c in rep["cases"])
+        for c in rep["cases"]:
+            assert c["equal_local"] and c["sel_equal_oracle"] and c["logit_err"] < 1e-4, c
+        assert rep["batch_equal_local"]

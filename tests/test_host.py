@@ -304,3 +304,61 @@ def test_batching_frontend_groups_and_routes_results():
             fe.submit([1], ["zz"])
         with pytest.raises(ValueError):
             fe.submit([], ["a"])
+
+
+def _sharded_worker(rank, world, port, root, q):
+    import os
+    import torch.distributed as dist
+    import paper_2604_08585_b200 as Q
+    from paper_2604_08585_b200.sharded import ShardedChunkStore
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64)
+    st = ShardedChunkStore(Path(root) / f"r{rank}", cfg, dtype="f32", device="cpu")
+    toks = [np.arange(5 + i) for i in range(10)]
+    ids = []
+    for t in toks:   # each rank registers only the chunks it owns (CPU tensors stand in for HBM)
+        cid = Q.chunk_hash(t)
+        ids.append(cid)
+        if st.owner(cid) == rank:
+            k = torch.full((4, t.size, 2, 16), float(int(cid[:4], 16)))
+            st.add_record(t, k, -k, np.ones(t.size, np.float32), np.asarray([0]))
+    st.exchange()
+    res = []
+    for cid in ids:
+        rec = st.get_record(cid)
+        res.append((cid, st.owner(cid), st.is_remote(cid), float(rec.k[0, 0, 0, 0]), float(rec.v[1, 0, 1, 2]),
+                    tuple(rec.anchor_k.shape), rec.n_tokens))
+    q.put((rank, res, sorted(st.chunk_ids()) == sorted(ids)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_store_exchange_two_ranks_gloo(tmp_path):
+    """ShardedChunkStore host logic over a 2-rank gloo group: every chunk has
+    one owner, the exchange maps every peer chunk (metadata + shared tensors)
+    into every rank, and a remote record reads the owner's values."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, str(tmp_path), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get() for _ in range(2)]
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    by_rank = {r: res for r, res, _ in got}
+    assert all(ok for _, _, ok in got)
+    owners = {c[1] for c in by_rank[0]}
+    assert owners == {0, 1}
+    for rank, res in by_rank.items():
+        for cid, owner, remote, kval, vval, ashape, n in res:
+            assert remote == (owner != rank)
+            assert kval == float(int(cid[:4], 16)) and vval == -kval
+            assert ashape == (4, 1, 2, 16)
