@@ -12,6 +12,7 @@ can be captured into a CUDA graph.
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 
@@ -48,6 +49,7 @@ class Executor:
         # request at a time runs through them (the reference engine is re-entrant,
         # fusion.py:211-216, so concurrent Python threads must be safe)
         self.lock = threading.RLock()
+        self.residual_in_epilogue = os.environ.get("QCF_RESID_EPI", "0") == "1"
         # fused QKV+RoPE epilogue: bf16 on a tcgen05 device, head dim a multiple of 32
         self.fused_qkv = (weights.dtype == "bf16" and self.cfg.d_head % 32 == 0
                           and torch.cuda.is_available() and bool(_lib.lib.qcf_tc_available()))
@@ -118,6 +120,23 @@ class Executor:
         call("qcf_gemm_ws", self.w.qcf_dtype, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), ldc,
              m, n, k, epi, out_dt, self.w.b_layout, sc.ws.data_ptr(), sc.ws.numel(), s)
 
+    def _project(self, sc: Scratch, a, lda, w, m: int, k: int, s) -> None:
+        """x += a @ w (model.py:375-376). The residual add runs in the GEMM
+        epilogue (read-modify-write of x, one f32 add per element: the same
+        arithmetic as adding it later), so the LayerNorm that follows reads x
+        alone (6 instead of 14 bytes per element) -- residual_in_epilogue
+        (QCF_RESID_EPI=1). Measured (r2g, two A/B pairs): LayerNorm 1.16 ->
+        0.94 ms per request and 4.38 -> 3.03 ms per batch, but the GEMM epilogue's
+        read of x sits on the kernels' tails: TTFT 13.8 -> 14.4 ms and 88.4 ->
+        87.4 req/s. Default: the projection goes to `delta` and the add folds
+        into the next LayerNorm."""
+        d = self.cfg.d_model
+        if self.residual_in_epilogue:
+            self.gemm(sc, a, lda, w, lda, sc.x, d, m, d, k, EPI_ADD_F32, QCF_F32, s)
+        else:
+            self.gemm(sc, a, lda, w, lda, sc.delta, d, m, d, k, EPI_STORE, QCF_F32, s)
+            sc.pending = True
+
     def layer(self, li: int, sc: Scratch, m: int, pos: torch.Tensor, dst: torch.Tensor,
               kmax: torch.Tensor, tab_k: torch.Tensor, tab_v: torch.Tensor,
               q_only: bool = False, q_out: torch.Tensor | None = None, stream=None,
@@ -154,12 +173,10 @@ class Executor:
         call("qcf_attention_batched_ws", dt, qdst.data_ptr(), tab_k.data_ptr(), tab_v.data_ptr(),
              kmax.data_ptr(), m // n_req, n_req, H, Hkv, D, tab_k.shape[0] // n_req, sc.o.data_ptr(),
              aws.data_ptr() if aws is not None else None, aws.numel() if aws is not None else 0, s)
-        self.gemm(sc, sc.o, H * D, lw.wo, H * D, sc.delta, d, m, d, H * D, EPI_STORE, QCF_F32, s)
-        sc.pending = True
+        self._project(sc, sc.o, H * D, lw.wo, m, H * D, s)
         self._norm(sc, m, lw.ln2_g, lw.ln2_b, s)
         self.gemm(sc, sc.a, d, lw.w1, d, sc.hid, F, m, F, d, EPI_RELU, dt, s)
-        self.gemm(sc, sc.hid, F, lw.w2, F, sc.delta, d, m, d, F, EPI_STORE, QCF_F32, s)
-        sc.pending = True
+        self._project(sc, sc.hid, F, lw.w2, m, F, s)
 
     def stack(self, sc: Scratch, m: int, pos, dst, kmax, tab_k: torch.Tensor, tab_v: torch.Tensor,
               layers: range | None = None, q_store: torch.Tensor | None = None, stream=None,
