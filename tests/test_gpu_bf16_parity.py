@@ -234,3 +234,29 @@ def test_fp32_scoring_precompute_and_qcfk_reload(tmp_path):
     store2 = Q.ChunkStore(tmp_path, cfg, dtype="bf16", persist=True, scoring="fp32")
     _, sel2 = Q.FusionEngine(w, store2).fuse(query, ids, 0.3)
     assert np.array_equal(sel2, sel)
+
+
+# ------------------------------------------- GQA (configs[3] shape family), small
+CFG_GQA = O.Config(n_layers=4, n_heads=8, n_kv_heads=2, d_model=1024, d_head=128, d_ff=2048)
+
+
+@pytest.fixture(scope="module")
+def gqa_case(tmp_path_factory):
+    ow = O.init_weights(CFG_GQA)
+    chunks = [O.precompute_chunk(ow, np.random.default_rng(50 + i).integers(0, 256, 256), 0.05) for i in range(4)]
+    query = np.random.default_rng(10_050).integers(0, 256, 24)
+    return Case(tmp_path_factory.mktemp("gqa"), CFG_GQA, ow, chunks, query, 0.15)
+
+
+def test_gqa_bf16_within_stated_tolerance(gqa_case):
+    """GQA-4 (H 8, Hkv 2, D 128: tcgen05 GQA attention and scoring) under the
+    same stated tolerance; parity anchored on the oracle's GQA restatement,
+    which reduces to the reference at Hkv == H."""
+    import paper_2604_08585_b200 as Q
+    before = Q._lib.lib.qcf_simt_fallbacks()
+    _check_bf16(gqa_case, "gqa/L4")
+    assert Q._lib.lib.qcf_simt_fallbacks() == before
+
+
+def test_gqa_fp32_scoring_selection_bit_exact(gqa_case):
+    _check_fp32_scoring(gqa_case, "gqa/L4")

@@ -962,3 +962,93 @@ def test_sharded_pool_p2p(tmp_path):
         for c in rep["cases"]:
             assert c["equal_local"] and c["sel_equal_oracle"] and c["logit_err"] < 1e-4, c
         assert rep["batch_equal_local"]
+
+
+class TestFetchLayer:
+    """The reference's TestFetchLayer (test_store.py:149-199) against the B200
+    store (f32 pool: the returned HostLayerKV is the device pool read back)."""
+
+    @staticmethod
+    def _store(tmp_path, **kw):
+        import paper_2604_08585_b200 as Q
+        cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+        return Q, cfg, Q.init_weights(cfg, dtype="f32"), Q.ChunkStore(tmp_path / "s", cfg, dtype="f32", **kw)
+
+    def test_duration_formula(self, tmp_path):
+        import paper_2604_08585_b200 as Q
+        cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=16, d_head=8, d_ff=32, seed=3)
+        store = Q.ChunkStore(tmp_path / "s", cfg, dtype="f32",
+                             tier=Q.TierConfig(ssd_base_latency=0.001, ssd_bandwidth=1e6))
+        rec = store.precompute(Q.init_weights(cfg, dtype="f32"), list(range(8)))
+        _, duration = store.fetch_layer(rec.chunk_id, 1)
+        assert duration == pytest.approx(0.001 + 1024 / 1e6)
+
+    def test_counters_and_determinism(self, tmp_path):
+        Q, cfg, w, store = self._store(tmp_path)
+        rec = store.precompute(w, [5, 6, 7, 8])
+        f0, b0 = store.manifest.layers_fetched, store.manifest.bytes_fetched
+        kv1, _ = store.fetch_layer(rec.chunk_id, 2)
+        kv2, _ = store.fetch_layer(rec.chunk_id, 2)
+        assert np.array_equal(kv1.keys, kv2.keys)
+        assert store.manifest.layers_fetched - f0 == 2
+        assert store.manifest.bytes_fetched - b0 == 2 * (2 * 4 * 2 * 16 * 4)
+        # the layer is the device pool's layer (and the oracle's precompute to fp32 rounding)
+        ow = O.init_weights(O.Config(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234))
+        ref = O.precompute_chunk(ow, [5, 6, 7, 8], 0.05)
+        assert np.array_equal(kv1.keys, rec.k[1].cpu().numpy())
+        assert np.abs(kv1.keys - ref.kv[1].keys).max() < 1e-5
+        assert np.abs(kv1.values - ref.kv[1].values).max() < 1e-5
+
+    def test_clock_advances(self, tmp_path):
+        import paper_2604_08585_b200 as Q
+        clock = Q.store.VirtualClock()
+        cfg = Q.ModelConfig(n_layers=4, n_heads=2, d_model=32, d_head=16, d_ff=64, seed=1234)
+        store = Q.ChunkStore(tmp_path / "s", cfg, dtype="f32", clock=clock)
+        rec = store.precompute(Q.init_weights(cfg, dtype="f32"), [1])
+        _, d = store.fetch_layer(rec.chunk_id, 1)
+        assert clock.now == pytest.approx(d)
+
+    def test_layer_out_of_range_and_unknown(self, tmp_path):
+        Q, cfg, w, store = self._store(tmp_path)
+        rec = store.precompute(w, [1, 2])
+        for bad in (0, 5):
+            with pytest.raises(KeyError):
+                store.fetch_layer(rec.chunk_id, bad)
+        with pytest.raises(KeyError):
+            store.fetch_layer("ff" * 32, 1)
+
+    def test_anchor_rows_free_when_resident(self, tmp_path):
+        Q, cfg, w, store = self._store(tmp_path)
+        rec = store.precompute(w, list(range(30)), anchor_ratio=0.2)
+        k, v, idx, duration = store.fetch_anchor_rows(rec.chunk_id, 1)
+        assert duration == 0.0
+        assert np.array_equal(idx, rec.anchor_indices)
+        assert np.array_equal(k, rec.layer_kv[0].keys[idx]) and np.array_equal(v, rec.layer_kv[0].values[idx])
+
+    def test_anchor_rows_charged_when_not_resident(self, tmp_path):
+        Q, cfg, w, store = self._store(tmp_path, tier=None)
+        store.tier = Q.TierConfig(anchors_resident=False)
+        rec = store.precompute(w, list(range(30)), anchor_ratio=0.2)
+        *_, duration = store.fetch_anchor_rows(rec.chunk_id, 1)
+        assert duration > 0
+
+
+def test_host_pool_matches_oracle(tmp_path):
+    """The pinned-host pool's layer-pipelined prefill against the ORACLE (not
+    only against the HBM pool): f32 parity mode, chunks from the oracle's
+    precompute; selection bit-exact, first-token logits within 1e-4."""
+    import paper_2604_08585_b200 as Q
+    from tests.gpu_util import device_weights
+    oc = O.Config(n_layers=4, n_heads=2, d_model=64, d_head=32, d_ff=128, seed=44)
+    ow = O.init_weights(oc)
+    rng = np.random.default_rng(8)
+    chunks = [O.precompute_chunk(ow, rng.integers(0, 256, 40), 0.1) for _ in range(3)]
+    query = rng.integers(0, 256, 7).tolist()
+    ref = O.run(ow, chunks, query, 0.25)
+    w = device_weights(ow, "f32")
+    host = Q.ChunkStore(tmp_path / "h", w.config, dtype="f32", persist=False, pool="host")
+    ids = load_oracle_chunks(host, chunks)
+    assert host.get_record(ids[0]).on_host
+    lg, sel = Q.FusionEngine(w, host).fuse(query, ids, 0.25)
+    assert np.array_equal(sel, ref.selection)
+    assert np.abs(lg - ref.first_logits).max() < 1e-4
