@@ -761,8 +761,33 @@ class FusionEngine:
     # selection policies (fusion.py:352-440)
     # ------------------------------------------------------------------
     def qcfuse_select(self, query_tokens, fused: FusedContext, ratio: float) -> SelectionResult:
+        if self.fp32_scoring:   # the float32 probe + scoring of the fast path (bit-exact selection)
+            return self._qcfuse_select_fp32(query_tokens, fused, ratio)
         probe = self.probe_query(query_tokens, fused, PROBE_ANCHORS, layers=self.config.critical_layer)
         return select_topn(self.score_critical(probe, fused), ratio, "QCFuse")
+
+    @_serialized
+    def _qcfuse_select_fp32(self, query_tokens, fused: FusedContext, ratio: float) -> SelectionResult:
+        """fusion.py:394-397 in the fp32 scoring mode: the same K2-K5 launches the
+        fast path runs (float32 anchor prefix and probe, float32 K_c, float64
+        scoring, Top-N), on a one-request buffer set."""
+        qt = [int(t) for t in np.asarray(query_tokens, np.int64)]
+        if not qt:
+            raise ValueError("query must be non-empty")
+        n_select(ratio, fused.n_ctx)   # ratio validation (ValueError)
+        plans = [self._plan("QCFuse", ratio, fused.chunk_ids, qt)]
+        b = self._buffers(plans)
+        self._stage(plans, b, [qt])
+        self.ex32.rope.ensure(b.rows + 2)
+        n = plans[0].n_sel
+        if n:
+            self._probe_score_fp32(plans, b)
+            self._topn_all(b, cuda_stream())
+            idx = b.selection(0).cpu().numpy().astype(np.int64)
+        else:
+            idx = np.zeros(0, np.int64)
+        scores = b.scores[:fused.n_ctx].cpu().numpy().copy() if n else np.zeros(fused.n_ctx, np.float32)
+        return SelectionResult("QCFuse", ratio, idx, scores)
 
     def qclast_select(self, query_tokens, fused, ratio) -> SelectionResult:
         probe = self.probe_query(query_tokens, fused, PROBE_NONE)

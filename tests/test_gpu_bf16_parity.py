@@ -260,3 +260,15 @@ def test_gqa_bf16_within_stated_tolerance(gqa_case):
 
 def test_gqa_fp32_scoring_selection_bit_exact(gqa_case):
     _check_fp32_scoring(gqa_case, "gqa/L4")
+
+
+def test_fp32_scoring_api_select_matches_fast_path(config1):
+    """The API-level select("QCFuse") of an fp32-scoring engine runs the same
+    float32 probe + scoring as the fast path: the reference's selection."""
+    case = config1[0]
+    eng, ids = case.engines["fp32"]
+    fused = eng.assemble_context(ids)
+    sel = eng.select("QCFuse", case.ratio, fused, case.query.tolist())
+    assert np.array_equal(sel.indices, case.ref.selection)
+    res = eng.run("QCFuse", case.ratio, ids, case.query.tolist(), max_new=2)
+    assert np.array_equal(res.selection.indices, case.ref.selection)
