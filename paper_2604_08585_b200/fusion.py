@@ -532,7 +532,8 @@ class FusionEngine:
         self._oracle_cache: dict = {}
         # assembly || probe on two streams (see _launch); measured neutral on B200 at the
         # Llama-3-8B shape (tools/concurrency_check.py: both phases are HBM-bound), off by default
-        self.concurrent = False   # True: the whole assembly may also overlap the probe (both HBM-bound)
+        # True: the whole assembly may also overlap the probe (both HBM-bound); QCF_ASM_CONCURRENT=1
+        self.concurrent = os.environ.get("QCF_ASM_CONCURRENT", "0") == "1"
         self.asm_group = 4        # layers per side-stream assembly launch
         # False: assembly on the main stream, in order (instrumented passes; QCF_PIPELINE_ASM=0)
         self.pipeline_asm = os.environ.get("QCF_PIPELINE_ASM", "1") != "0"
