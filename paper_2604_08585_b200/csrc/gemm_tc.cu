@@ -708,6 +708,37 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
         uint32_t r[32];
         tmem_ld32(tmem_base + acc * 256 + c0 + ((uint32_t)(g * 32) << 16), r);
         tmem_ld_wait();
+        if (ea.kind != QCF_EPI_ROPE_QKV) {
+          // store / ReLU / residual add: lane n holds column col0 + n of 32 consecutive
+          // rows, so the warp writes each row's 32 columns in one coalesced access --
+          // no shared-memory transpose (same per-element arithmetic: bit-identical)
+          const int col = col0 + lane, nr = min(32, rows - c0);
+          if (col < N) {
+            if (ea.out_dtype == QCF_F32) {
+              float* cp = reinterpret_cast<float*>(C) + (int64_t)(row0 + c0) * ldc + col;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j < nr) {
+                  float v = __uint_as_float(r[j]);
+                  if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
+                  else if (ea.kind == QCF_EPI_ADD_F32) v += cp[(int64_t)j * ldc];
+                  cp[(int64_t)j * ldc] = v;
+                }
+              }
+            } else {
+              __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)(row0 + c0) * ldc + col;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j < nr) {
+                  float v = __uint_as_float(r[j]);
+                  if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
+                  cp[(int64_t)j * ldc] = __float2bfloat16_rn(v);
+                }
+              }
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) stage[j * 33 + lane] = __uint_as_float(r[j]);
         __syncwarp();

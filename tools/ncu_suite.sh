@@ -12,10 +12,10 @@ ncu --nvtx --nvtx-include "profile_step/" --metrics gpu__time_duration.sum --clo
     --log-file $OUT/launches_b8.csv python tools/profile_step.py llama3-8b QCFuse 8 > $OUT/launches_b8.log 2>&1
 ncu --nvtx --nvtx-include "profile_step/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_b1.csv python tools/profile_step.py llama3-8b QCFuse 1 > $OUT/launches_b1.log 2>&1
-for shape in "6400 12288 4096 9" "6400 4096 4096 2" "6400 14336 4096 1" "6400 4096 14336 2" \
-             "256 12288 4096 0" "256 4096 4096 2" "256 14336 4096 1" "256 4096 14336 2" \
-             "800 12288 4096 9" "800 4096 4096 2" "800 14336 4096 1" "800 4096 14336 2" \
-             "32 12288 4096 9" "32 4096 4096 2" "32 14336 4096 1" "32 4096 14336 2"; do
+for shape in "6400 12288 4096 9" "6400 4096 4096 0" "6400 14336 4096 1" "6400 4096 14336 0" \
+             "256 12288 4096 0" "256 4096 4096 0" "256 14336 4096 1" "256 4096 14336 0" \
+             "800 12288 4096 9" "800 4096 4096 0" "800 14336 4096 1" "800 4096 14336 0" \
+             "32 12288 4096 9" "32 4096 4096 0" "32 14336 4096 1" "32 4096 14336 0"; do
   set -- $shape
   ncu --set full --clock-control none -k regex:"gemm_tc|gemm_skc|splitk" -s 2 -c 2 --csv --page raw \
       python tools/one_gemm.py $1 $2 $3 $4 > $OUT/gemm_$1x$2x$3.csv 2> /dev/null
