@@ -555,6 +555,357 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// v4: two CTAs per SM, 64-key tiles. The single-tile kernel's per key tile period
+// (~2100 cycles traced) is one softmax latency chain with every softmax warp in the
+// same phase, plus ~5 us of per-CTA setup / epilogue with the tensor core idle.
+// Here one CTA (128 query rows, one head) needs only 256 TMEM columns
+// (S double-buffered at 64 keys + O) and ~97 KB of shared memory, so two CTAs
+// share an SM: one CTA's softmax, setup and epilogue run while the other's MMAs
+// keep the tensor core busy (the hardware interleaves them; no ping-pong code).
+//   warp 0      TMA: lane 0 streams Q then K tiles (2-stage ring), lane 1 V tiles
+//   warp 1      MMA: S_0, S_1, then per key tile j: P_j.V_j, S_{j+2} into P_j's
+//               buffer (tcgen05 ops of one thread execute in order: S_{j+2} cannot
+//               overwrite P_j before P_j.V_j has read it)
+//   warps 2..   softmax: SW = 4 -> one full 64-key row per thread (no cross-warp
+//               max exchange); SW = 8 -> half rows, max exchanged through smem.
+//               Row sums in registers (FADD2), lazy reference max (rescale O only
+//               when the running max grows by > 2^8), epilogue O / l.
+// ---------------------------------------------------------------------------
+constexpr int A4_BN = 64;
+constexpr int A4_KT = A4_BN * AT_D * 2;  // 16 KB: one 64-key K or V tile (two 8 KB SW128 atoms)
+constexpr int A4_KS = 2, A4_VS = 2;
+constexpr int A4_SMEM = AT_TILE_BYTES + A4_KT * (A4_KS + A4_VS) + 1024 + 256;
+
+// MN-major SW128 descriptor for a 64-key V tile: 8-key groups 1024 B apart (SBO),
+// the two 64-dim atoms 8 KB apart (LBO)
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128_k64(const void* smem_tile) {
+  const uint32_t a = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+template <int SW, int EMU16>
+__global__ void __launch_bounds__(64 + SW * 32, 2)
+attn_tc4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
+                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int rshift) {
+  constexpr int NCH = SW / 4;          // warps sharing one row (column chunks)
+  constexpr int CW = A4_BN / NCH;      // S columns (keys) per softmax thread: 64 or 32
+  constexpr int OW = AT_D / NCH;       // output dims per softmax thread: 128 or 64
+  const int req = blockIdx.z;
+  kmax += (int64_t)req * M;
+  out += (int64_t)req * M * H * AT_D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + AT_TILE_BYTES;               // [A4_KS]
+  uint8_t* sV = sK + A4_KS * A4_KT;                 // [A4_VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + A4_VS * A4_KT);
+  uint64_t* q_full = bars + 0;
+  uint64_t* s_full = bars + 1;     // [2] S buffer b holds S_j, j = b mod 2
+  uint64_t* p_full = bars + 3;     // [2] P_j stored over S_j (SW arrives)
+  uint64_t* pv_done = bars + 5;    // [2] P_j.V_j complete
+  uint64_t* k_full = bars + 7;     // [A4_KS]
+  uint64_t* k_empty = k_full + A4_KS;
+  uint64_t* v_full = k_empty + A4_KS;   // [A4_VS]
+  uint64_t* v_empty = v_full + A4_VS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + A4_VS);
+  __shared__ float red[2][NCH][AT_BM];
+  __shared__ float red_l[NCH][AT_BM];
+  __shared__ int s_kend;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int qt = n_qt - 1 - blockIdx.y;   // longest tiles first
+  const int head = blockIdx.x;
+  const int kvh = head / (H / Hkv);
+  const int m0 = qt * AT_BM - rshift;
+#ifdef QCF_ATTN_TRACE
+  if (threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    QCF_TRACE(0, sm);
+    QCF_TRACE(1, gtimer());
+  }
+#endif
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], SW);
+      mbar_init(&pv_done[s], 1);
+    }
+    for (int s = 0; s < A4_KS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < A4_VS; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_barrier_init();
+    s_kend = 0;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 256);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {  // Q and K_0 in flight while the key range is scanned
+    mbar_expect_tx(q_full, AT_TILE_BYTES);
+    tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
+    tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
+    mbar_expect_tx(&k_full[0], A4_KT);
+    tma_load_3d(sK, &map_k, &k_full[0], kvh * AT_D, 0, req);
+    tma_load_3d(sK + A4_KT / 2, &map_k, &k_full[0], kvh * AT_D + 64, 0, req);
+  }
+  if (threadIdx.x < AT_BM) {
+    const int rr = m0 + (int)threadIdx.x;
+    int v = (rr >= 0 && rr < M) ? kmax[rr] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) atomicMax(&s_kend, max(1, min(v + 1, n_keys)));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tiles = (s_kend + A4_BN - 1) / A4_BN;
+  const uint32_t tS = tmem, tO = tmem + 128;   // S[2] (64 columns each) | O (128)
+#ifdef QCF_ATTN_TRACE
+  if (threadIdx.x == 0) { QCF_TRACE(2, gtimer()); QCF_TRACE(7, n_tiles); }
+#endif
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 1; j < n_tiles; ++j) {
+        const int st = j % A4_KS;
+        mbar_wait(&k_empty[st], ((j / A4_KS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], A4_KT);
+        uint8_t* k = sK + st * A4_KT;
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * A4_BN, req);
+        tma_load_3d(k + A4_KT / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * A4_BN, req);
+      }
+    } else if (lane == 1) {
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % A4_VS;
+        mbar_wait(&v_empty[st], ((j / A4_VS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], A4_KT);
+        uint8_t* v = sV + st * A4_KT;
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * A4_BN, req);
+        tma_load_3d(v + A4_KT / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * A4_BN, req);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, A4_BN);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);  // B (V) MN-major
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    auto issue_s = [&](int j) {
+      const int st = j % A4_KS, sb = j & 1;
+      mbar_wait(&k_full[st], (j / A4_KS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+        const uint64_t b = umma_desc_k_sw128(sK + st * A4_KT + (kk >> 2) * (A4_KT / 2)) + (uint64_t)((kk & 3) * 2);
+        mma_bf16_e(tS + sb * 64, a, b, idesc_s, kk != 0);
+      }
+      mma_commit_e(&s_full[sb]);
+      mma_commit_e(&k_empty[st]);
+      QCF_TRACE2(j, 5);
+    };
+    issue_s(0);
+    if (n_tiles > 1) issue_s(1);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j & 1, vs = j % A4_VS;
+      mbar_wait(&p_full[sb], (j >> 1) & 1);
+      QCF_TRACE2(j, 7);
+      mbar_wait(&v_full[vs], (j / A4_VS) & 1);
+      QCF_TRACE2(j, 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < A4_BN / 16; ++kk) {
+        // keys 16kk..16kk+15 = packed columns at the start of their owner's S columns
+        const uint32_t pa = tS + sb * 64 + (kk * 16 / CW) * CW + ((kk * 16) % CW) / 2;
+        const uint64_t b = umma_desc_mn_sw128_k64(sV + vs * A4_KT + kk * 16 * 128);
+        mma_bf16_ts_e(tO, pa, b, idesc_o, (j | kk) != 0);
+      }
+      QCF_TRACE2(j, 2);
+      mma_commit_e(&v_empty[vs]);
+      mma_commit_e(&pv_done[sb]);
+      QCF_TRACE2(j, 6);
+      if (j + 2 < n_tiles) issue_s(j + 2);
+    }
+  } else {
+    const int sw = warp - 2;
+    const int g = warp & 3;               // TMEM lane quarter -> rows 32g..32g+31
+    const int ch = sw >> 2;               // column chunk (SW = 8: keys / dims half)
+    const int r = g * 32 + lane;
+    const int row = m0 + r;
+    const int my_kmax = (row >= 0 && row < M) ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const uint64_t sc2 = f2(scale_log2, scale_log2);
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+#ifdef QCF_ATTN_TRACE
+      if (j == 0 && threadIdx.x == 64) QCF_TRACE(3, gtimer());
+      if (threadIdx.x == 64) QCF_TRACE2(j, 0);
+#endif
+      tc_fence_after();
+      uint32_t v[CW];
+      tmem_ld32(tS + sb * 64 + ch * CW + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      if constexpr (CW == 64) tmem_ld32(tS + sb * 64 + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      const int lim = my_kmax - j * A4_BN - ch * CW;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= CW - 1);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      float pmax = -INFINITY;
+      if (all_vis) {
+        float pm1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < CW; i += 4) {
+          pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          pm1 = fmax3(pm1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        }
+        pmax = fmaxf(pmax, pm1);
+      } else if (!none_vis) {
+#pragma unroll
+        for (int i = 0; i < CW; ++i) pmax = fmaxf(pmax, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
+      }
+      float tmax = pmax * scale_log2;
+      if constexpr (NCH > 1) {
+        red[sb][ch][r] = tmax;
+        named_bar(1 + g, 64);
+        tmax = fmaxf(red[sb][0][r], red[sb][1][r]);
+      }
+      const bool need = tmax > m_ref + 8.f;  // lazily move the reference max
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - tmax);
+        m_ref = tmax;
+        l *= alpha;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale O after P_{j-1}.V_{j-1}
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < OW / 32; ++hh) {
+          uint32_t o[32];
+          tmem_ld32(tO + ch * OW + hh * 32 + lane_off, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tO + ch * OW + hh * 32 + lane_off, o);
+        }
+      }
+      uint32_t pk[CW / 2];
+      if (none_vis) {
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) pk[i] = 0u;
+      } else if (all_vis) {
+        const uint64_t nm2 = f2(-m_ref, -m_ref);
+        uint64_t l2 = f2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < CW; i += 2) {
+          const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
+          uint64_t p2;
+          if (((((i >> 1) & 15) * 9) & 15) < EMU16) {
+            p2 = exp2_poly2(x2);
+          } else {
+            float a, b;
+            f2_split(x2, a, b);
+            p2 = f2(ex2_approx(a), ex2_approx(b));
+          }
+          l2 = fadd2(l2, p2);
+          float p0, p1;
+          f2_split(p2, p0, p1);
+          pk[i >> 1] = bf16x2_bits(p0, p1);
+        }
+        float la, lb;
+        f2_split(l2, la, lb);
+        l += la + lb;
+      } else {
+#pragma unroll
+        for (int i = 0; i < CW; i += 2) {
+          float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
+          float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
+          p0 = (i <= lim) ? p0 : 0.f;
+          p1 = (i + 1 <= lim) ? p1 : 0.f;
+          l += p0 + p1;
+          pk[i >> 1] = bf16x2_bits(p0, p1);
+        }
+      }
+#ifdef QCF_ATTN_TRACE
+      if (threadIdx.x == 64) QCF_TRACE2(j, 3);
+#endif
+      if constexpr (CW == 64) tmem_st32(tS + sb * 64 + lane_off, pk);
+      else tmem_st16(tS + sb * 64 + ch * CW + lane_off, pk);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[sb]);
+#ifdef QCF_ATTN_TRACE
+      if (threadIdx.x == 64) QCF_TRACE2(j, 4);
+#endif
+    }
+#ifdef QCF_ATTN_TRACE
+    if (threadIdx.x == 64) QCF_TRACE(4, gtimer());
+#endif
+    // epilogue: O / l
+    float lt = l;
+    if constexpr (NCH > 1) {
+      red_l[ch][r] = l;
+      named_bar(1 + g, 64);
+      lt = red_l[0][r] + red_l[1][r];
+    }
+    mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    tc_fence_after();
+#ifdef QCF_ATTN_TRACE
+    if (threadIdx.x == 64) QCF_TRACE(5, gtimer());
+#endif
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll
+    for (int hh = 0; hh < OW / 32; ++hh) {
+      uint32_t o[32];
+      tmem_ld32(tO + ch * OW + hh * 32 + lane_off, o);
+      tmem_ld_wait();
+      if (row >= 0 && row < M) {
+        __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + ch * OW + hh * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk4;
+          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv, __uint_as_float(o[i + 2 * u + 1]) * inv);
+          *reinterpret_cast<uint4*>(dst + i) = pk4;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+#ifdef QCF_ATTN_TRACE
+    if (lane == 0) QCF_TRACE(6, gtimer());
+#endif
+  }
+}
+
+// ---------------------------------------------------------------------------
 // v2: two query tiles per CTA (ping-pong) with P kept in tensor memory.
 //
 // One CTA = (two 128-row query tiles, one head). TMEM: S_t / P_t (cols 128t..)
@@ -1119,7 +1470,7 @@ static int g_attn_split = 2;  // v2 softmax layout: 2 = half rows (default), 1 =
 void set_attention_kernel(int v) {
   g_attn_split = (v == 3) ? 1 : 2;
   if (v == 3) v = 2;
-  g_attn_ver = (v == 1 || v == 2) ? v : 0;
+  g_attn_ver = (v == 1 || v == 2 || v == 4) ? v : 0;
 }
 
 static int g_attn_nsplit = -1;  // QCF_ATTN_SPLIT env / qcf_set_attention_split: split-KV factor (one-wave grids)
@@ -1163,7 +1514,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
   if (st != QCF_OK) return st;
   if (g_attn_ver < 0) {
     const char* e = getenv("QCF_ATTN");
-    g_attn_ver = (e && atoi(e) == 1) ? 1 : (e && atoi(e) == 2) ? 2 : 0;  // 0 = by grid size
+    g_attn_ver = (e && atoi(e) == 1) ? 1 : (e && atoi(e) == 2) ? 2 : (e && atoi(e) == 4) ? 4 : 0;  // 0 = by grid size
   }
   static bool attr = false;
   if (!attr) {
@@ -1172,6 +1523,9 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
       e = cudaFuncSetAttribute(attn_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
+if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc4_kernel<4, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, A4_SMEM);
+
     if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
     attr = true;
   }
@@ -1189,15 +1543,20 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
     n_split = attention_auto_split(m, n_req, h, n_keys);
     if (n_split > 1 && ws_bytes < attention_workspace(m, n_req, h, n_split)) n_split = 1;
   }
-  const int64_t grid_pairs = (int64_t)h * n_pairs * n_req;
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  // ping-pong pairs pay off for long row lists (full prefill 5152 rows: 236 vs 268 us,
-  // 32k Mistral: 1216 vs 1341 us); at the recompute shape (~800 rows per request) single
-  // tiles are as fast for MHA and 10% faster for GQA-8 (tools/attn_bench.py)
-  const int ver = g_attn_ver ? g_attn_ver : (((grid_pairs > sms && m > 2048) || n_split > 1) ? 2 : 1);
+  // auto (tools/attn_bench.py, profiles/r2s3_attn_bench.jsonl): v4 (two CTAs per SM over
+  // 64-key tiles) once the grid fills both CTA slots of every SM -- batch recompute 8 x 800
+  // rows: 337 vs 366 us, GQA-8 307 vs 381, full prefill 205 vs 232, Mistral 32k 1141 vs
+  // 1202 -- or fills one slot with short uniform key ranges (probe rows of 8 requests: 10
+  // vs 14 us); one request's 224 uneven tiles stay on the single-tile kernel (54 vs 72 us:
+  // the longest tiles would share SMs while others idle); split-KV grids on the pairs
+  const int64_t ctas = (int64_t)h * n_qt * n_req;
+  const int ver = g_attn_ver ? g_attn_ver
+                             : n_split > 1 ? 2
+                             : (ctas >= 2 * sms || (ctas > sms && n_keys <= 4 * AT_BN)) ? 4 : 1;
   if (ver == 2) {
     static int pair_mode = -1;  // QCF_ATTN_PAIR: 0 adjacent (default), 1 mirrored
     if (pair_mode == -1) {
@@ -1223,6 +1582,14 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
                  dim3(128), 0, s, (const float*)ws_o, (const float2*)ws_ml, (int)m, h, n_split, (__nv_bfloat16*)out,
                  rshift);
     }
+  } else if (ver == 4) {
+    CUtensorMap mk4, mv4;   // 64-key boxes
+    st = make_kmajor_map3(&mk4, k, n_keys, kw, kw, A4_BN, n_req, n_keys * kw);
+    if (st == QCF_OK) st = make_kmajor_map3(&mv4, v, n_keys, kw, kw, A4_BN, n_req, n_keys * kw);
+    if (st != QCF_OK) return st;
+    dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
+    QCF_LAUNCH("attn_tc4_kernel", (attn_tc4_kernel<4, 7>), dim3(grid), dim3(64 + 4 * 32), A4_SMEM, s, mq, mk4, mv4,
+               kmax, (int)m, h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, rshift);
   } else {
     dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
     QCF_LAUNCH("attn_tc_kernel", attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, s, mq, mk, mv, kmax, (int)m,

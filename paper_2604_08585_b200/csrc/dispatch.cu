@@ -170,7 +170,7 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
 }
 
 extern "C" int qcf_set_attention_kernel(int version) {
-  QCF_REQUIRE(version >= 0 && version <= 3, QCF_EINVAL, "qcf_set_attention_kernel: version 0 (auto), 1, 2 or 3");
+  QCF_REQUIRE(version >= 0 && version <= 4, QCF_EINVAL, "qcf_set_attention_kernel: version 0 (auto) or 1..4");
   qcf::set_attention_kernel(version);
   return QCF_OK;
 }

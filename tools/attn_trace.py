@@ -35,7 +35,7 @@ def run(name, m, n_keys, H, Hkv, n_req, kmax):
     out = torch.empty_like(q)
     n_cta = H * ((m + 127) // 128) * n_req
     buf = torch.zeros(n_cta * 8, dtype=torch.int64, device="cuda")
-    _lib.call("qcf_set_attention_kernel", 1)
+    _lib.call("qcf_set_attention_kernel", int(os.environ.get("QCF_TRACE_KNOB", "1")))
     f = lambda: _lib.call("qcf_attention_batched", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(), kmax.data_ptr(), m,
                           n_req, H, Hkv, D, n_keys, out.data_ptr(), S)
     for _ in range(3):
