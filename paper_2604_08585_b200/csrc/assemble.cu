@@ -3,6 +3,7 @@
 // fused table written once, with 16-byte vector accesses; the chunk offset
 // rotation uses a float64 cos/sin table built on the host exactly as the
 // reference builds its angles (model.py:278-281).
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace qcf {

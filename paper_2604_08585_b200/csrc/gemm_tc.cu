@@ -716,13 +716,24 @@ gemm_tc2s_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
           if (col < N) {
             if (ea.out_dtype == QCF_F32) {
               float* cp = reinterpret_cast<float*>(C) + (int64_t)(row0 + c0) * ldc + col;
+              if (ea.kind == QCF_EPI_ADD_F32) {
+                // all 32 residual loads first: interleaved with the stores they would be
+                // serialised (the compiler cannot rule out ldc == 0 aliasing), one L2
+                // round trip per row -- measured 119 us for W_o at M = 800 (ncu, 10% tensor)
+                float res[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (j < nr) {
-                  float v = __uint_as_float(r[j]);
-                  if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
-                  else if (ea.kind == QCF_EPI_ADD_F32) v += cp[(int64_t)j * ldc];
-                  cp[(int64_t)j * ldc] = v;
+                for (int j = 0; j < 32; ++j) res[j] = j < nr ? cp[(int64_t)j * ldc] : 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j < nr) cp[(int64_t)j * ldc] = __uint_as_float(r[j]) + res[j];
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  if (j < nr) {
+                    float v = __uint_as_float(r[j]);
+                    if (ea.kind == QCF_EPI_RELU) v = fmaxf(v, 0.f);
+                    cp[(int64_t)j * ldc] = v;
+                  }
                 }
               }
             } else {
@@ -1167,6 +1178,19 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 // at M = 256 the 64-wide plan measured slower than 1-CTA 128 x 64 tiles)
 static double swap_plan(int64_t m, int64_t n, int& bna, int& n_act, int min_w = 128) {
   const int64_t clusters = sm_count() / 2, wp = (n + 255) / 256;
+  static int force_na = -1;   // QCF_SWAP_NA: force the activation tile count (measurement)
+  if (force_na < 0) {
+    const char* e = getenv("QCF_SWAP_NA");
+    force_na = e ? std::max(0, atoi(e)) : 0;
+  }
+  if (force_na > 0) {
+    const int64_t w = ((m + force_na - 1) / force_na + 15) / 16 * 16;
+    if (w <= 256) {
+      bna = (int)w;
+      n_act = force_na;
+      return 0.0;
+    }
+  }
   double best = 1e30;
   for (int64_t na = (m + 255) / 256; na <= (m + 255) / 256 + 8; ++na) {
     const int64_t w = ((m + na - 1) / na + 15) / 16 * 16;

@@ -49,7 +49,7 @@ class Executor:
         # request at a time runs through them (the reference engine is re-entrant,
         # fusion.py:211-216, so concurrent Python threads must be safe)
         self.lock = threading.RLock()
-        self.residual_in_epilogue = os.environ.get("QCF_RESID_EPI", "0") == "1"
+        self.residual_in_epilogue = os.environ.get("QCF_RESID_EPI", "1") == "1"
         # fused QKV+RoPE epilogue: bf16 on a tcgen05 device, head dim a multiple of 32
         self.fused_qkv = (weights.dtype == "bf16" and self.cfg.d_head % 32 == 0
                           and torch.cuda.is_available() and bool(_lib.lib.qcf_tc_available()))
@@ -125,11 +125,13 @@ class Executor:
         epilogue (read-modify-write of x, one f32 add per element: the same
         arithmetic as adding it later), so the LayerNorm that follows reads x
         alone (6 instead of 14 bytes per element) -- residual_in_epilogue
-        (QCF_RESID_EPI=1). Measured (r2g, two A/B pairs): LayerNorm 1.16 ->
-        0.94 ms per request and 4.38 -> 3.03 ms per batch, but the GEMM epilogue's
-        read of x sits on the kernels' tails: TTFT 13.8 -> 14.4 ms and 88.4 ->
-        87.4 req/s. Default: the projection goes to `delta` and the add folds
-        into the next LayerNorm."""
+        (default; QCF_RESID_EPI=0 turns it off). The swapped kernel's epilogue
+        issues all 32 residual loads of a row group before its stores (they were
+        serialised: W_o at M = 800 took 119 us). A/B on one box (r2s3,
+        profiles/r2s3_resid_epi_ab.txt, two pairs): LayerNorm 4.39 -> 3.0-3.2 ms
+        per batch and 1.10 -> 0.95 ms per request, 88.4/89.3 -> 89.8/89.4 req/s,
+        TTFT 13.50/13.48 -> 13.42/13.44 ms. Off: the projection goes to `delta`
+        and the add folds into the next LayerNorm."""
         d = self.cfg.d_model
         if self.residual_in_epilogue:
             self.gemm(sc, a, lda, w, lda, sc.x, d, m, d, k, EPI_ADD_F32, QCF_F32, s)
