@@ -47,6 +47,7 @@ struct EpiArgs {
   void* k_tab;
   void* v_tab;
   int h, hkv, d;
+  int preload_w = 0;   // cluster split-K kernel: request the first weight k-blocks before the PDL wait
 };
 
 // fused epilogue for 32 consecutive columns of one output row
@@ -918,6 +919,19 @@ gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the weights do not depend on the previous kernel: the first ring's worth of weight
+  // k-blocks is requested before the PDL wait (only the activation rows wait for it)
+  const int npre = ea.preload_w ? min(SKC_STAGES, kb1 - kb0) : 0;
+  if (warp == 0 && lane == 0) {
+    for (int it = 0; it < npre; ++it) {
+      const int kb = kb0 + it;
+      mbar_expect_tx(&full[it], SKC_A + NM * 128);
+      if (ea.b_tiled)
+        tma_load_4d(sA + it * SKC_A, &map_w, &full[it], 0, 0, kb, tile * 2);
+      else
+        tma_load_2d(sA + it * SKC_A, &map_w, &full[it], kb * TC_BK, tile * 128);
+    }
+  }
   pdl_wait();
   pdl_trigger();
 
@@ -925,12 +939,14 @@ gemm_skc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant
     if (lane == 0) {  // ---------------- TMA producer
       for (int kb = kb0; kb < kb1; ++kb) {
         const int it = kb - kb0, s = it % SKC_STAGES;
-        mbar_wait(&empty[s], ((it / SKC_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&full[s], SKC_A + NM * 128);
-        if (ea.b_tiled)
-          tma_load_4d(sA + s * SKC_A, &map_w, &full[s], 0, 0, kb, tile * 2);
-        else
-          tma_load_2d(sA + s * SKC_A, &map_w, &full[s], kb * TC_BK, tile * 128);
+        if (it >= npre) {
+          mbar_wait(&empty[s], ((it / SKC_STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], SKC_A + NM * 128);
+          if (ea.b_tiled)
+            tma_load_4d(sA + s * SKC_A, &map_w, &full[s], 0, 0, kb, tile * 2);
+          else
+            tma_load_2d(sA + s * SKC_A, &map_w, &full[s], kb * TC_BK, tile * 128);
+        }
         tma_load_2d(sB + s * SKC_B, &map_x, &full[s], kb * TC_BK, 0);
       }
     }
@@ -1356,7 +1372,14 @@ static int launch_skc_nm(const CUtensorMap& mw, const void* a, int64_t lda, void
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_skc_kernel<NM>, mw, mx, c, ldc, (int)m, (int)n, (int)k, ea);
+  static int preload = -1;   // QCF_SKC_PRELOAD=0: no weight loads before the PDL wait
+  if (preload < 0) {
+    const char* e = getenv("QCF_SKC_PRELOAD");
+    preload = e ? atoi(e) : 1;
+  }
+  EpiArgs ep = ea;
+  ep.preload_w = preload;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_skc_kernel<NM>, mw, mx, c, ldc, (int)m, (int)n, (int)k, ep);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 cluster split-K)");
   QCF_LAUNCH_CHECK("qcf_gemm(tcgen05 cluster split-K)");
   return QCF_OK;
