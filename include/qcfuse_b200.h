@@ -229,9 +229,11 @@ int qcf_attention_batched_ws(int dtype, const void* q, const void* k, const void
 /* Tuning knob (process-wide): tcgen05 attention kernel 1 = one 128-row query
  * tile per CTA over 128-key tiles; 2 = two query tiles per CTA ping-ponging on
  * the tensor core (3 = the same with one thread per full row); 4 = one query
- * tile per CTA over 64-key tiles, two CTAs resident per SM; 0 (default) = 4 when
- * the grid fills both CTA slots of every SM (or one slot with key ranges of at
- * most 256 keys), split-KV pairs for one-wave grids, else 1. */
+ * tile per CTA over 64-key tiles, two CTAs resident per SM; 8 = one query tile
+ * per CTA, two softmax warp groups on alternate key tiles, three S buffers;
+ * 0 (default) = 4 when the grid fills both CTA slots of every SM (or one slot
+ * with key ranges of at most 256 keys), split-KV pairs for one-wave grids,
+ * else 1. */
 int qcf_set_attention_kernel(int version);
 /* Tuning knob (process-wide): tcgen05 GEMM tile plan for M > 32. 0 (default) =
  * wave-quantisation model; 1 = 2-CTA 256x256; 2 = 1-CTA 128x256; 3 = 128x128;

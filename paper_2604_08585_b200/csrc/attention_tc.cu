@@ -906,6 +906,367 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// v8: one 128-row query tile per CTA over 128-key tiles, with two softmax warp
+// groups taking alternate key tiles (group j & 1) and THREE S buffers. In v1 all
+// 16 softmax warps step through the same latency chain per tile; here one group
+// exponentiates tile j while the other already works on tile j+1, and S_{j+3}
+// goes into P_j's buffer right after P_j.V_j, so a group's next S is ready when it
+// finishes a tile. The groups share only the lazy reference max: the owner of
+// tile j publishes its per-row reference in shared memory (mref_ready[j & 1]) and
+// the owner of tile j+1 starts from it. TMEM: S[3] (128 each) | O (128) = 512
+// columns, so the row sums live in registers (each thread sums its 64 keys; the
+// four partials of a row -- 2 groups x 2 halves, each relative to its group's
+// last reference max -- are combined in the epilogue).
+// Measured (tools/attn_bench.py, tools/attn_trace.py knob 8): ~1780 cycles per key
+// tile vs ~2100 for v1; one request's 224 tiles 44 vs 48 us. The tile period is
+// now set by shared-memory bandwidth: per key and 128-row query tile the K and V
+// rows are written by TMA (512 B) and read by the MMAs (K + Q slab and V), about
+// 1 KB per 8 tensor-core cycles -- the SM's ~128 B/clk. (A variant with Q in TMEM
+// and two S buffers -- TS S-MMAs, 32 KB less smem traffic per tile -- measured
+// ~1820 cycles per tile: the MMA round trip P_j -> P_j.V_j -> S_{j+2} then sat on
+// each group's chain.)
+//   warp 0      TMA: lane 0 Q then the K ring, lane 1 the V ring
+//   warp 1      MMA: S_0 S_1 S_2, then per key tile j: P_j.V_j, S_{j+3} into
+//               P_j's buffer (j mod 3)
+//   warps 2..9  softmax group 0 (even tiles), 10..17 group 1 (odd tiles)
+// ---------------------------------------------------------------------------
+constexpr int A8_KS = 2, A8_VS = 3;
+constexpr int A8_THREADS = 576;
+constexpr int A8_SMEM = AT_TILE_BYTES * (1 + A8_KS + A8_VS) + 1024 + 256;
+
+__global__ void __launch_bounds__(A8_THREADS, 1)
+attn_tc8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const int32_t* __restrict__ kmax, int M, int H,
+                int Hkv, int n_keys, float scale_log2, __nv_bfloat16* __restrict__ out, int rshift) {
+  const int req = blockIdx.z;
+  kmax += (int64_t)req * M;
+  out += (int64_t)req * M * H * AT_D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + AT_TILE_BYTES;                   // [A8_KS]
+  uint8_t* sV = sK + A8_KS * AT_TILE_BYTES;             // [A8_VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + A8_VS * AT_TILE_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* o_full = bars + 1;      // every P.V done
+  uint64_t* s_full = bars + 2;      // [3]
+  uint64_t* p_full = bars + 5;      // [3] (the 8 warps of the owning group)
+  uint64_t* pv_done = bars + 8;     // [3]
+  uint64_t* mref_ready = bars + 11; // [2] reference max after tile j published (4 warps)
+  uint64_t* k_full = bars + 13;     // [A8_KS]
+  uint64_t* k_empty = k_full + A8_KS;
+  uint64_t* v_full = k_empty + A8_KS;  // [A8_VS]
+  uint64_t* v_empty = v_full + A8_VS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + A8_VS);
+  __shared__ float red[2][2][2][AT_BM]; // [group][group-tile parity][column half][row] partial row max
+  __shared__ float mref_buf[2][AT_BM];  // [tile parity][row] reference max after that tile
+  __shared__ float lsum[2][2][AT_BM];   // [group][half][row] row-sum partials (epilogue)
+  __shared__ float lref[2][AT_BM];      // [group][row] the reference those partials are relative to
+  __shared__ int s_kend;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (M + AT_BM - 1) / AT_BM;
+  const int qt = n_qt - 1 - blockIdx.y;  // longest tiles first
+  const int head = blockIdx.x;
+  const int kvh = head / (H / Hkv);
+  const int m0 = qt * AT_BM - rshift;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_k);
+    tma_prefetch_desc(&map_v);
+    mbar_init(q_full, 1);
+    mbar_init(o_full, 1);
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 8);
+      mbar_init(&pv_done[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) mbar_init(&mref_ready[s], 4);
+    for (int s = 0; s < A8_KS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < A8_VS; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_barrier_init();
+    s_kend = 0;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {  // Q and K_0 in flight while the key range is scanned
+    mbar_expect_tx(q_full, AT_TILE_BYTES);
+    tma_load_3d(sQ, &map_q, q_full, head * AT_D, m0, req);
+    tma_load_3d(sQ + AT_TILE_BYTES / 2, &map_q, q_full, head * AT_D + 64, m0, req);
+    mbar_expect_tx(&k_full[0], AT_TILE_BYTES);
+    tma_load_3d(sK, &map_k, &k_full[0], kvh * AT_D, 0, req);
+    tma_load_3d(sK + AT_TILE_BYTES / 2, &map_k, &k_full[0], kvh * AT_D + 64, 0, req);
+  }
+  if (threadIdx.x < AT_BM) {
+    const int rr = m0 + (int)threadIdx.x;
+    int v = (rr >= 0 && rr < M) ? kmax[rr] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) atomicMax(&s_kend, max(1, min(v + 1, n_keys)));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tiles = (s_kend + AT_BN - 1) / AT_BN;
+  const uint32_t tS0 = tmem, tO = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 1; j < n_tiles; ++j) {
+        const int st = j % A8_KS;
+        mbar_wait(&k_empty[st], ((j / A8_KS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], AT_TILE_BYTES);
+        uint8_t* k = sK + st * AT_TILE_BYTES;
+        tma_load_3d(k, &map_k, &k_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(k + AT_TILE_BYTES / 2, &map_k, &k_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      }
+    } else if (lane == 1) {
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % A8_VS;
+        mbar_wait(&v_empty[st], ((j / A8_VS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], AT_TILE_BYTES);
+        uint8_t* v = sV + st * AT_TILE_BYTES;
+        tma_load_3d(v, &map_v, &v_full[st], kvh * AT_D, j * AT_BN, req);
+        tma_load_3d(v + AT_TILE_BYTES / 2, &map_v, &v_full[st], kvh * AT_D + 64, j * AT_BN, req);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = idesc_bf16_f32(AT_BM, AT_BN);                  // K-major A (Q) and B (K)
+    constexpr uint32_t idesc_o = idesc_bf16_f32(AT_BM, AT_D) | (1u << 16);      // B (V) MN-major
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    auto issue_s = [&](int j) {
+      const int st = j % A8_KS;
+      mbar_wait(&k_full[st], (j / A8_KS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const uint64_t a = umma_desc_k_sw128(sQ + (kk >> 2) * (AT_TILE_BYTES / 2)) + (uint64_t)((kk & 3) * 2);
+        const uint64_t b = umma_desc_k_sw128(sK + st * AT_TILE_BYTES + (kk >> 2) * (AT_TILE_BYTES / 2)) +
+                           (uint64_t)((kk & 3) * 2);
+        mma_bf16_e(tS0 + (j % 3) * 128, a, b, idesc_s, kk != 0);
+      }
+      mma_commit_e(&s_full[j % 3]);
+      mma_commit_e(&k_empty[st]);
+      QCF_TRACE2(j, 5);
+    };
+    for (int j = 0; j < 3 && j < n_tiles; ++j) issue_s(j);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j % 3, vs = j % A8_VS;
+      mbar_wait(&p_full[sb], (j / 3) & 1);
+      QCF_TRACE2(j, 7);
+      mbar_wait(&v_full[vs], (j / A8_VS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < AT_BN / 16; ++kk) {   // keys 16kk.. : half kk/4, packed at 64*(kk/4) + 8*(kk%4)
+        const uint32_t pa = tS0 + sb * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
+        const uint64_t b = umma_desc_mn_sw128(sV + vs * AT_TILE_BYTES + kk * 16 * 128);
+        mma_bf16_ts_e(tO, pa, b, idesc_o, (j | kk) != 0);
+      }
+      QCF_TRACE2(j, 2);
+      mma_commit_e(&v_empty[vs]);
+      mma_commit_e(&pv_done[sb]);
+      QCF_TRACE2(j, 6);
+      if (j + 3 < n_tiles) issue_s(j + 3);
+    }
+    mma_commit_e(o_full);
+  } else {
+    const int sw = warp - 2;
+    const int grp = sw >> 3;              // softmax group: tiles j with j & 1 == grp
+    const int h = (sw >> 2) & 1;          // column half: keys 64h..64h+63 of a tile
+    const int g = warp & 3;               // TMEM lane quarter -> rows 32g..32g+31
+    const int r = g * 32 + lane;
+    const int row = m0 + r;
+    const int my_kmax = (row >= 0 && row < M) ? kmax[row] : -1;
+    const uint32_t lane_off = (uint32_t)(g * 32) << 16;
+    const uint64_t sc2 = f2(scale_log2, scale_log2);
+    float l = 0.f, m_mine = -INFINITY;   // this thread's row-sum partial, relative to m_mine
+    for (int j = grp; j < n_tiles; j += 2) {
+      const int sb = j % 3;
+      mbar_wait(&s_full[sb], (j / 3) & 1);
+#ifdef QCF_ATTN_TRACE
+      if (lane == 0 && (sw & 7) == 0) QCF_TRACE2(j, 0);
+#endif
+      tc_fence_after();
+      const int lim = my_kmax - j * AT_BN - 64 * h;  // columns <= lim are visible
+      const bool all_vis = __all_sync(0xffffffffu, lim >= 63);
+      const bool none_vis = __all_sync(0xffffffffu, lim < 0);
+      // pass 1: row max over this half's 64 columns, 32 at a time
+      float pmax = -INFINITY;
+      if (!none_vis) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tS0 + sb * 128 + 64 * h + 32 * c + lane_off, v);
+          tmem_ld_wait();
+          if (all_vis) {
+            float pm1 = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              pmax = fmax3(pmax, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+              pm1 = fmax3(pm1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+            }
+            pmax = fmaxf(pmax, pm1);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pmax = fmaxf(pmax, 32 * c + i <= lim ? __uint_as_float(v[i]) : -INFINITY);
+          }
+        }
+      }
+      const int rp = (j >> 1) & 1;      // a group's consecutive tiles alternate buffers
+      red[grp][rp][h][r] = pmax * scale_log2;
+      named_bar(1 + grp * 4 + g, 64);   // the two halves of these rows in this group
+      const float tmax = fmaxf(red[grp][rp][0][r], red[grp][rp][1][r]);
+      float m_prev = -INFINITY;         // reference max after tile j-1 (the other group's)
+      if (j > 0) {
+        mbar_wait(&mref_ready[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        m_prev = mref_buf[(j - 1) & 1][r];
+      }
+#ifdef QCF_ATTN_TRACE
+      if (lane == 0 && (sw & 7) == 0) QCF_TRACE2(j, 1);   // (slot 1 = reference max handed over)
+#endif
+      const bool need = tmax > m_prev + 8.f;  // lazily move the reference max
+      const float m_ref = need ? tmax : m_prev;
+      if (h == 0) {
+        mref_buf[j & 1][r] = m_ref;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&mref_ready[j & 1]);
+      }
+      if (m_ref > m_mine) {   // this thread's partial sum follows the reference (it only grows)
+        l = (m_mine == -INFINITY) ? 0.f : l * ex2_approx(m_mine - m_ref);
+        m_mine = m_ref;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale O after P_{j-1}.V_{j-1}
+        const float alpha = (m_prev == -INFINITY) ? 0.f : ex2_approx(m_prev - m_ref);
+        mbar_wait(&pv_done[(j - 1) % 3], ((j - 1) / 3) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int hh = 0; hh < 4; ++hh) {   // 16 columns at a time (register budget)
+          uint32_t o[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7]),
+                "=r"(o[8]), "=r"(o[9]), "=r"(o[10]), "=r"(o[11]), "=r"(o[12]), "=r"(o[13]), "=r"(o[14]), "=r"(o[15])
+              : "r"(tO + 64 * h + 16 * hh + lane_off));
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tO + 64 * h + 16 * hh + lane_off, o);
+        }
+      }
+      // pass 2: P = exp2(s*scale - m_ref), packed bf16, 32 keys (16 columns) at a time
+      // over the first 32 of this half's 64 S columns; row-sum partial in registers
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[16];
+        uint32_t v[32];
+        if (!none_vis) {
+          tmem_ld32(tS0 + sb * 128 + 64 * h + 32 * c + lane_off, v);
+          tmem_ld_wait();
+        }
+        if (none_vis) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        } else if (all_vis) {
+          const uint64_t nm2 = f2(-m_ref, -m_ref);
+          uint64_t l2 = f2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t x2 = ffma2(f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
+            uint64_t p2;
+            if (A2_EMU(i >> 1)) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float a, b;
+              f2_split(x2, a, b);
+              p2 = f2(ex2_approx(a), ex2_approx(b));
+            }
+            l2 = fadd2(l2, p2);
+            float p0, p1;
+            f2_split(p2, p0, p1);
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+          float la, lb;
+          f2_split(l2, la, lb);
+          l += la + lb;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const int e = 32 * c + i;
+            float p0 = ex2_approx(fmaf(__uint_as_float(v[i]), scale_log2, -m_ref));
+            float p1 = ex2_approx(fmaf(__uint_as_float(v[i + 1]), scale_log2, -m_ref));
+            p0 = (e <= lim) ? p0 : 0.f;
+            p1 = (e + 1 <= lim) ? p1 : 0.f;
+            l += p0 + p1;
+            pk[i >> 1] = bf16x2_bits(p0, p1);
+          }
+        }
+#ifdef QCF_ATTN_TRACE
+        if (c == 1 && lane == 0 && (sw & 7) == 0) QCF_TRACE2(j, 3);
+#endif
+        tmem_st16(tS0 + sb * 128 + 64 * h + 16 * c + lane_off, pk);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[sb]);
+#ifdef QCF_ATTN_TRACE
+      if (lane == 0 && (sw & 7) == 0) QCF_TRACE2(j, 4);
+#endif
+    }
+    // epilogue: combine the four row-sum partials (2 groups x 2 halves) at the final
+    // reference (the largest: references only grow), then O / l for 32 dims per warp
+    lsum[grp][h][r] = l;
+    if (h == 0) lref[grp][r] = m_mine;
+    named_bar(9, 512);                  // the 16 softmax warps
+    float lt = 0.f;
+    {
+      const float ma = lref[0][r], mb = lref[1][r];
+      const float mf = fmaxf(ma, mb);
+      if (mf != -INFINITY) {
+        if (ma != -INFINITY) lt += (lsum[0][0][r] + lsum[0][1][r]) * ex2_approx(ma - mf);
+        if (mb != -INFINITY) lt += (lsum[1][0][r] + lsum[1][1][r]) * ex2_approx(mb - mf);
+      }
+    }
+    const int cq = sw >> 2;   // dims 32cq..32cq+31
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    uint32_t o[32];
+    tmem_ld32(tO + cq * 32 + lane_off, o);
+    tmem_ld_wait();
+    if (row >= 0 && row < M) {
+      __nv_bfloat16* dst = out + ((int64_t)row * H + head) * AT_D + cq * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk4;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          p2[u] = __floats2bfloat162_rn(__uint_as_float(o[i + 2 * u]) * inv, __uint_as_float(o[i + 2 * u + 1]) * inv);
+        *reinterpret_cast<uint4*>(dst + i) = pk4;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // v2: two query tiles per CTA (ping-pong) with P kept in tensor memory.
 //
 // One CTA = (two 128-row query tiles, one head). TMEM: S_t / P_t (cols 128t..)
@@ -1470,7 +1831,7 @@ static int g_attn_split = 2;  // v2 softmax layout: 2 = half rows (default), 1 =
 void set_attention_kernel(int v) {
   g_attn_split = (v == 3) ? 1 : 2;
   if (v == 3) v = 2;
-  g_attn_ver = (v == 1 || v == 2 || v == 4) ? v : 0;
+  g_attn_ver = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
 }
 
 static int g_attn_nsplit = -1;  // QCF_ATTN_SPLIT env / qcf_set_attention_split: split-KV factor (one-wave grids)
@@ -1523,9 +1884,10 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
       e = cudaFuncSetAttribute(attn_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, A2_SMEM);
-if (e == cudaSuccess)
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_tc4_kernel<4, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, A4_SMEM);
-
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A8_SMEM);
     if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
     attr = true;
   }
@@ -1547,12 +1909,14 @@ if (e == cudaSuccess)
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  // auto (tools/attn_bench.py, profiles/r2s3_attn_bench.jsonl): v4 (two CTAs per SM over
-  // 64-key tiles) once the grid fills both CTA slots of every SM -- batch recompute 8 x 800
-  // rows: 337 vs 366 us, GQA-8 307 vs 381, full prefill 205 vs 232, Mistral 32k 1141 vs
-  // 1202 -- or fills one slot with short uniform key ranges (probe rows of 8 requests: 10
-  // vs 14 us); one request's 224 uneven tiles stay on the single-tile kernel (54 vs 72 us:
-  // the longest tiles would share SMs while others idle); split-KV grids on the pairs
+  // auto (tools/attn_bench.py, profiles/r2s3_attn_versions*.jsonl): v4 (two CTAs per SM
+  // over 64-key tiles) once the grid fills both CTA slots of every SM -- batch recompute
+  // 8 x 800 rows: 337 vs 366 us (v1), GQA-8 307 vs 381, full prefill 205 vs 232, Mistral
+  // 32k 1141 vs 1202 -- or fills one slot with short uniform key ranges (probe rows of 8
+  // requests: 10 vs 14 us); smaller grids of uneven tiles (one request: 224) run v1
+  // (72-76 us for v4: its longest tiles would share SMs while others idle; v8 is 44 vs
+  // 48 us alone but measured slower inside the step: TTFT 13.29 vs 13.0-13.2 ms);
+  // split-KV grids on the pairs
   const int64_t ctas = (int64_t)h * n_qt * n_req;
   const int ver = g_attn_ver ? g_attn_ver
                              : n_split > 1 ? 2
@@ -1582,6 +1946,10 @@ if (e == cudaSuccess)
                  dim3(128), 0, s, (const float*)ws_o, (const float2*)ws_ml, (int)m, h, n_split, (__nv_bfloat16*)out,
                  rshift);
     }
+  } else if (ver == 8) {
+    dim3 grid((unsigned)h, (unsigned)n_qt, (unsigned)n_req);
+    QCF_LAUNCH("attn_tc8_kernel", attn_tc8_kernel, dim3(grid), dim3(A8_THREADS), A8_SMEM, s, mq, mk, mv, kmax, (int)m,
+               h, hkv, (int)n_keys, scale_log2, (__nv_bfloat16*)out, rshift);
   } else if (ver == 4) {
     CUtensorMap mk4, mv4;   // 64-key boxes
     st = make_kmajor_map3(&mk4, k, n_keys, kw, kw, A4_BN, n_req, n_keys * kw);

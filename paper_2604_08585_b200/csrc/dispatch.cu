@@ -170,7 +170,8 @@ extern "C" int qcf_gemm_qkv_rope(const void* a, int64_t lda, const void* w, int6
 }
 
 extern "C" int qcf_set_attention_kernel(int version) {
-  QCF_REQUIRE(version >= 0 && version <= 4, QCF_EINVAL, "qcf_set_attention_kernel: version 0 (auto) or 1..4");
+  QCF_REQUIRE(version >= 0 && version <= 8 && version != 5 && version != 6 && version != 7, QCF_EINVAL,
+              "qcf_set_attention_kernel: version 0 (auto), 1, 2, 3, 4 or 8");
   qcf::set_attention_kernel(version);
   return QCF_OK;
 }

@@ -483,7 +483,7 @@ def _torch_attention_gqa(q, k, v, kmax):
     return torch_attention(q, k.repeat_interleave(H // Hkv, dim=1), v.repeat_interleave(H // Hkv, dim=1), kmax)
 
 
-@pytest.mark.parametrize("version", [1, 2, 3, 4, "auto+ws", "split3"])
+@pytest.mark.parametrize("version", [1, 2, 3, 4, 8, "auto+ws", "split3"])
 @pytest.mark.parametrize("m,n,H,Hkv,n_req,sort", [
     (800, 5153, 4, 4, 3, True), (130, 1000, 8, 2, 2, True), (64, 300, 2, 1, 1, True),
     (1000, 1200, 32, 8, 8, True), (256, 700, 2, 2, 1, False), (383, 900, 4, 4, 2, False)])
@@ -491,7 +491,8 @@ def test_attention_tc_batched_gqa_versions(L, version, m, n, H, Hkv, n_req, sort
     """The tcgen05 attention kernels (1: single tile, P via smem; 2: ping-pong
     tile pairs, P in TMEM, half rows per thread; 3: the same with one thread
     per full row; 4: two CTAs per SM over 64-key tiles, one full row per
-    thread; adjacent and mirrored pairings) on batched, GQA,
+    thread; 8: two softmax warp groups on alternate key tiles, three S buffers;
+    adjacent and mirrored pairings) on batched, GQA,
     ragged-M and unsorted-row inputs vs an fp32 torch reference (tol 2e-2)."""
     torch.manual_seed(m * 7 + n)
     D = 128

@@ -1,6 +1,7 @@
 """tcgen05 attention kernels at the fused-path shapes (CUDA events): 1 = one
 tile per CTA, 2 = ping-pong pairs with half-row softmax threads, 3 = ping-pong
-with full-row threads, 4 = two CTAs per SM over 64-key tiles (0 = auto).
+with full-row threads, 4 = two CTAs per SM over 64-key tiles, 8 = two softmax
+groups on alternate key tiles with three S buffers (0 = auto).
 QCF_ATTN_PAIR=0/1 forces adjacent/mirrored pairing.
 FLOPs counted on the exact visible keys: 4*H*D*sum(kmax+1)."""
 import sys
@@ -24,7 +25,7 @@ def bench(m, n_keys, H, Hkv, n_req, kmax, it=20):
     nb = int(_lib.lib.qcf_attention_workspace(m, n_req, H, n_keys))
     ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
     res["auto_split"] = int(_lib.lib.qcf_attention_split(m, n_req, H, n_keys))
-    order = [int(x) for x in __import__("os").environ.get("QCF_ATTN_ORDER", "1,2,4,0").split(",")]
+    order = [int(x) for x in __import__("os").environ.get("QCF_ATTN_ORDER", "1,4,8,0").split(",")]
     for ver in order:   # 0 = auto with workspace (split-KV for one-wave grids)
         _lib.call("qcf_set_attention_kernel", ver)
         f = lambda: _lib.call("qcf_attention_batched_ws", 1, q.data_ptr(), k.data_ptr(), v.data_ptr(),
