@@ -1888,6 +1888,7 @@ int attention_tc_launch(const void* q, const void* k, const void* v, const int32
       e = cudaFuncSetAttribute(attn_tc4_kernel<4, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, A4_SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_tc8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A8_SMEM);
+
     if (e != cudaSuccess) return cuda_status(e, "attn_tc attr");
     attr = true;
   }
