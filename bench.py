@@ -440,6 +440,9 @@ def main():
         elif name == "qcf_assemble_range":
             asm_ms += ms
             asm_b += 4.0 * a[9] * a[2] * a[10] * a[11] * esz
+        elif name == "qcf_assemble_range_skip":   # the selected rows are left out (the recompute writes them)
+            asm_ms += ms
+            asm_b += 4.0 * a[9] * (a[2] - n_sel_plan) * a[10] * a[11] * esz
         elif name == "qcf_add_layernorm":
             ln_ms += ms
             ln_b += a[2] * a[3] * ((4 + 4 + 4) if a[1] else 4) + a[2] * a[3] * (2 if a[8] == 1 else 4)

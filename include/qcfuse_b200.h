@@ -107,6 +107,20 @@ int qcf_assemble_range(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
                        int64_t fused_layer_stride, int layer0, int n_layers, int hkv, int d,
                        const double* cos_tbl, const double* sin_tbl, int64_t n_pos, int dtype,
                        qcf_stream_t stream);
+/* qcf_assemble_range that leaves out the fused rows whose bit is set in skip_rows
+ * (device bitmap, bit r of word r/32 = fused row r): the selected rows, which the
+ * recompute rewrites in every layer (fusion.py:477-478), so their chunk K/V are
+ * neither read nor written (the same final table, ~15% fewer assembly bytes). */
+int qcf_assemble_range_skip(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                            const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                            int64_t fused_layer_stride, int layer0, int n_layers, int hkv, int d,
+                            const double* cos_tbl, const double* sin_tbl, int64_t n_pos, int dtype,
+                            const uint32_t* skip_rows, qcf_stream_t stream);
+/* Bitmap of rows: for each of n_req requests, bit p of bitmap[r * words_per_req ..]
+ * is set for every pos[r * stride + i] > 0, i < n_per_req (the recompute rows'
+ * positions; BOS / padding entries are 0). */
+int qcf_rows_bitmap(const int32_t* pos, int64_t stride, int n_req, int64_t n_per_req, uint32_t* bitmap,
+                    int64_t words_per_req, qcf_stream_t stream);
 int qcf_assemble_rot(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
                      const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
                      int64_t fused_layer_stride, int n_layers, int hkv, int d,

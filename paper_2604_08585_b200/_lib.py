@@ -50,6 +50,8 @@ SIGNATURES: dict[str, tuple] = {
     "qcf_assemble": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _P, _I64, _I, _P]),
     "qcf_assemble_rot": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _P, _I64, _P, _I, _I, _P]),
     "qcf_assemble_range": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _P, _P, _I64, _I, _P]),
+    "qcf_assemble_range_skip": (_I, [_P, _I, _I, _P, _P, _P, _P, _I64, _I, _I, _I, _I, _P, _P, _I64, _I, _P, _P]),
+    "qcf_rows_bitmap": (_I, [_P, _I64, _I, _I64, _P, _I64, _P]),
     "qcf_gather_rows": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _I, _I64, _I, _P]),
     "qcf_embed": (_I, [_P, _P, _I32, _I64, _P, _I, _P, _P]),
     "qcf_layernorm": (_I, [_P, _I64, _I, _P, _P, _F, _P, _I, _P]),

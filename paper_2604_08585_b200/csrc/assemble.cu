@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
     const T* __restrict__ bos_k, const T* __restrict__ bos_v, T* __restrict__ fk,
     T* __restrict__ fv, int64_t fstride, int row_elems, int d,
     const double* __restrict__ ctab, const double* __restrict__ stab, const int32_t* __restrict__ deltas,
-    int layer0) {
+    int layer0, const uint32_t* __restrict__ skip) {
   pdl_wait();
   pdl_trigger();
   constexpr int V = Vec16<T>::N;
@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(ASM_THREADS) assemble_kernel(
   int c_lo = 1, c_hi = 0;                 // fused rows of the cached chunk: [c_lo, c_hi)
   for (int run = blockIdx.x * ASM_ROWS; run < n_rows; run += gridDim.x * ASM_ROWS) {
     for (int row = run; row < min(run + ASM_ROWS, n_rows); ++row) {
+      // rows the recompute rewrites in every layer (bit set) are not copied (CTA-uniform)
+      if (skip && ((__ldg(skip + (row >> 5)) >> (row & 31)) & 1u)) continue;
       T* dk = fk + layer * fstride + (int64_t)row * row_elems;
       T* dv = fv + layer * fstride + (int64_t)row * row_elems;
       if (row == 0) {
@@ -174,7 +176,8 @@ __global__ void gather_rows_kernel(const T* __restrict__ sk, const T* __restrict
 static int assemble_impl(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx, const void* bos_k,
                          const void* bos_v, void* fused_k, void* fused_v, int64_t fused_layer_stride, int layer0,
                          int n_layers, int hkv, int d, const double* cos_tbl, const double* sin_tbl, int64_t n_pos,
-                         const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream) {
+                         const int32_t* deltas, int max_delta, int dtype, qcf_stream_t stream,
+                         const uint32_t* skip = nullptr) {
   QCF_REQUIRE(chunks && bos_k && fused_k && cos_tbl && sin_tbl && (!fused_v || bos_v), QCF_EINVAL,
               "qcf_assemble: null pointer");
   QCF_REQUIRE(n_chunks >= 1 && n_ctx >= 1 && n_layers >= 1 && hkv >= 1 && layer0 >= 0, QCF_EINVAL,
@@ -193,11 +196,11 @@ static int assemble_impl(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx, 
   if (dtype == QCF_F32)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<float>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1, (const float*)bos_k,
         (const float*)bos_v, (float*)fused_k, (float*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl,
-        deltas, layer0);
+        deltas, layer0, skip);
   else if (dtype == QCF_BF16)
     QCF_LAUNCH("assemble_kernel", qcf::assemble_kernel<__nv_bfloat16>, dim3(grid), block, 0, s, chunks, n_chunks, n_ctx + 1,
         (const __nv_bfloat16*)bos_k, (const __nv_bfloat16*)bos_v, (__nv_bfloat16*)fused_k,
-        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas, layer0);
+        (__nv_bfloat16*)fused_v, fused_layer_stride, row_elems, d, cos_tbl, sin_tbl, deltas, layer0, skip);
   else
     QCF_REQUIRE(false, QCF_EINVAL, "qcf_assemble: bad dtype");
   QCF_LAUNCH_CHECK("qcf_assemble");
@@ -220,6 +223,43 @@ extern "C" int qcf_assemble_range(const qcf_chunk_desc* chunks, int n_chunks, in
                                   qcf_stream_t stream) {
   return assemble_impl(chunks, n_chunks, n_ctx, bos_k, bos_v, fused_k, fused_v, fused_layer_stride, layer0,
                        n_layers, hkv, d, cos_tbl, sin_tbl, n_pos, nullptr, 0, dtype, stream);
+}
+
+extern "C" int qcf_assemble_range_skip(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,
+                                       const void* bos_k, const void* bos_v, void* fused_k, void* fused_v,
+                                       int64_t fused_layer_stride, int layer0, int n_layers, int hkv, int d,
+                                       const double* cos_tbl, const double* sin_tbl, int64_t n_pos, int dtype,
+                                       const uint32_t* skip_rows, qcf_stream_t stream) {
+  return assemble_impl(chunks, n_chunks, n_ctx, bos_k, bos_v, fused_k, fused_v, fused_layer_stride, layer0,
+                       n_layers, hkv, d, cos_tbl, sin_tbl, n_pos, nullptr, 0, dtype, stream, skip_rows);
+}
+
+namespace qcf {
+// bitmap of the fused rows named in pos[r * stride + i] (i < n_per_req), one block
+// per request: cleared, then one atomicOr per row; rows <= 0 (BOS / padding) ignored
+__global__ void rows_bitmap_kernel(const int32_t* __restrict__ pos, int64_t stride, int64_t n_per_req,
+                                   uint32_t* __restrict__ bm, int64_t words) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x;
+  uint32_t* b = bm + (int64_t)r * words;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) b[i] = 0u;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n_per_req; i += blockDim.x) {
+    const int32_t p = pos[(int64_t)r * stride + i];
+    if (p > 0 && (p >> 5) < words) atomicOr(b + (p >> 5), 1u << (p & 31));
+  }
+}
+}  // namespace qcf
+
+extern "C" int qcf_rows_bitmap(const int32_t* pos, int64_t stride, int n_req, int64_t n_per_req, uint32_t* bitmap,
+                               int64_t words_per_req, qcf_stream_t stream) {
+  QCF_REQUIRE(pos && bitmap && n_req >= 1 && n_req <= 65535 && n_per_req >= 0 && words_per_req >= 1, QCF_EINVAL,
+              "qcf_rows_bitmap: bad arguments");
+  QCF_LAUNCH("rows_bitmap_kernel", qcf::rows_bitmap_kernel, dim3((unsigned)n_req), dim3(256), 0, qcf::as_stream(stream),
+             pos, stride, n_per_req, bitmap, words_per_req);
+  QCF_LAUNCH_CHECK("qcf_rows_bitmap");
+  return QCF_OK;
 }
 
 extern "C" int qcf_assemble(const qcf_chunk_desc* chunks, int n_chunks, int n_ctx,

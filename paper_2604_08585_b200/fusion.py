@@ -462,6 +462,8 @@ class _Bufs:
         self.score_ws = torch.empty(int(_lib.lib.qcf_score_batched_workspace(n_ctx_max, Q, B, H, Hkv)),
                                     dtype=torch.uint8, device=dev)
         self.rc_pos = t32(rc_pos)   # per-request positions == kmax (selected slots filled by Top-N)
+        self.skip_words = (R + 31) // 32   # per-request bitmap of the recompute rows (assembly skips them)
+        self.skip_bm = torch.empty(B * self.skip_words, dtype=torch.int32, device=dev)
         self.rc_dst = t32(rc_dst)   # rows in the batch table
         self.last_row = t32(np.asarray([r * Mr + S + self.q_r[r] - 1 for r in range(B)], np.int32))
         self.logits = torch.empty((B, cfg.vocab_size), dtype=torch.float32, device=dev)
@@ -534,6 +536,7 @@ class FusionEngine:
         # Llama-3-8B shape (tools/concurrency_check.py: both phases are HBM-bound), off by default
         # True: the whole assembly may also overlap the probe (both HBM-bound); QCF_ASM_CONCURRENT=1
         self.concurrent = os.environ.get("QCF_ASM_CONCURRENT", "0") == "1"
+        self.asm_skip = os.environ.get("QCF_ASM_SKIP", "1") != "0"
         self.asm_group = 4        # layers per side-stream assembly launch
         # False: assembly on the main stream, in order (instrumented passes; QCF_PIPELINE_ASM=0)
         self.pipeline_asm = os.environ.get("QCF_PIPELINE_ASM", "1") != "0"
@@ -610,14 +613,22 @@ class FusionEngine:
             arr[i].offset = o
         return torch.frombuffer(bytearray(arr), dtype=torch.uint8)
 
-    def _assemble_range(self, recs, n_ctx, fk, fv, desc_dev, layer0, n_layers, stream=None, layer_stride=None):
+    def _assemble_range(self, recs, n_ctx, fk, fv, desc_dev, layer0, n_layers, stream=None, layer_stride=None,
+                        skip_ptr: int | None = None):
+        """Layers [layer0, layer0 + n_layers) of assemble_context (fusion.py:234-263).
+        skip_ptr: device bitmap of fused rows the recompute rewrites in every layer
+        (the selection); those rows are neither read nor written."""
         cfg = self.config
         self.ex.rope.ensure(n_ctx + 2)
-        call("qcf_assemble_range", desc_dev.data_ptr(), len(recs), n_ctx, self._bos_k.data_ptr(),
-             self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(),
-             fk.stride(0) if layer_stride is None else layer_stride, layer0, n_layers,
-             cfg.n_kv_heads, cfg.d_head, self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(),
-             self.ex.rope.n_pos, self.weights.qcf_dtype, cuda_stream(stream))
+        args = (desc_dev.data_ptr(), len(recs), n_ctx, self._bos_k.data_ptr(),
+                self._bos_v.data_ptr(), fk.data_ptr(), fv.data_ptr(),
+                fk.stride(0) if layer_stride is None else layer_stride, layer0, n_layers,
+                cfg.n_kv_heads, cfg.d_head, self.ex.rope.cos.data_ptr(), self.ex.rope.sin.data_ptr(),
+                self.ex.rope.n_pos, self.weights.qcf_dtype)
+        if skip_ptr is None:
+            call("qcf_assemble_range", *args, cuda_stream(stream))
+        else:
+            call("qcf_assemble_range_skip", *args, skip_ptr, cuda_stream(stream))
 
     def _assemble_into(self, recs, offs, n_ctx, fk, fv, desc_dev, stream=None, layer_stride=None):
         cfg = self.config
@@ -1001,13 +1012,14 @@ class FusionEngine:
         aux = None
         last = None
 
-        def enqueue(rngs) -> None:
+        def enqueue(rngs, skip: bool = False) -> None:
             nonlocal last
             for l0, nl in rngs:
                 for r in range(B):   # request r's slice of the batch table, layers [l0, l0+nl)
+                    sp = b.skip_bm.data_ptr() + 4 * r * b.skip_words if skip else None
                     self._assemble_range(plans[r].records, plans[r].n_ctx, _view_rows(b.fk, r * b.R),
                                          _view_rows(b.fv, r * b.R), _DescView(b.desc, b.desc_off[r]), l0, nl, aux,
-                                         layer_stride=b.fk.stride(0))
+                                         layer_stride=b.fk.stride(0), skip_ptr=sp)
                 e = torch.cuda.Event()
                 e.record(aux)
                 last = e
@@ -1075,10 +1087,15 @@ class FusionEngine:
                 call("qcf_iota", b.n_sel_r[r], 1, b.rc_pos.data_ptr() + r * b.Mr * 4, s)
                 call("qcf_iota", b.n_sel_r[r], 1 + r * b.R, b.rc_dst.data_ptr() + r * b.Mr * 4, s)
         if pending:   # the remaining layers' assembly starts with the recompute
+            # the selection is known now: the rows the recompute rewrites in every layer
+            # are left out of the copy (QCF_ASM_SKIP=0 copies them too)
+            skip = probe and self.asm_skip
+            if skip:
+                call("qcf_rows_bitmap", b.rc_pos.data_ptr(), b.Mr, B, b.Mr, b.skip_bm.data_ptr(), b.skip_words, s)
             ev = torch.cuda.Event()
             ev.record(main)
             aux.wait_event(ev)
-            enqueue(pending)
+            enqueue(pending, skip=skip)
         m = B * b.Mr   # K6: recompute + query rows of the whole batch
         ex.embed(b.sc_rc, m, b.tok, rows=b.rc_dst, stream=stream)
         ex.stack(b.sc_rc, m, b.rc_pos, b.rc_dst, b.rc_pos, b.fk, b.fv, stream=stream, n_req=B,

@@ -737,3 +737,43 @@ def test_decode_advance_argmax_tie_rule(L):
     assert log.tolist() == [17, 3, -1, -1]
     assert int(tok.item()) == 3 and int(pos.item()) == 43 and int(step.item()) == 2
     assert int(np.argmax(lg[0].cpu().numpy())) == 3
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_assembly_skips_recomputed_rows(golden_dir, tmp_path, dtype):
+    """The side-stream assembly leaves out the selected rows (qcf_rows_bitmap +
+    qcf_assemble_range_skip: the recompute rewrites them in every layer), and the
+    final fused table and logits are bit-identical to a prefill that copies every
+    row; the skipped rows really are not written by the assembly."""
+    from tests.gpu_util import golden_setup
+    z, oc, ow, chunks, w, store, ids, eng = golden_setup(golden_dir, "small_case1", dtype, tmp_path)
+    query = [int(t) for t in z["query"]] if "query" in z else [1, 2, 3, 4, 5]
+    outs = []
+    for skip in (False, True):
+        eng.asm_skip = skip
+        eng._bufs.clear()
+        plan, b = eng.prefill("QCFuse", 0.25, ids, query, use_graph=False)
+        torch.cuda.synchronize()
+        n = plan.n_ctx
+        outs.append((b.fk[:, :n + 1].clone(), b.fv[:, :n + 1].clone(), b.logits.clone(),
+                     b.rc_pos[:plan.n_sel].clone()))
+    eng.asm_skip = True
+    for x, y in zip(outs[0], outs[1]):
+        assert torch.equal(x, y)
+    # the bitmap marks exactly the selected positions
+    sel = outs[1][3].long().cpu()
+    words = b.skip_bm[:b.skip_words].cpu().numpy().view(np.uint32)
+    bits = np.array([(words[p >> 5] >> (p & 31)) & 1 for p in range(1, n + 1)])
+    assert set(np.nonzero(bits)[0] + 1) == set(sel.tolist())
+    # and the skip kernel leaves those rows untouched
+    recs, offs, n_ctx = eng._records(ids)
+    desc = eng._desc_bytes(recs, offs).to(eng.device)
+    fk = torch.full_like(b.fk[:, :n_ctx + 1], 7.0).contiguous()
+    fv = torch.full_like(fk, 7.0)
+    eng._assemble_range(recs, n_ctx, fk, fv, desc, 0, oc.n_layers, skip_ptr=b.skip_bm.data_ptr())
+    torch.cuda.synchronize()
+    for p in sel.tolist():
+        assert (fk[:, p] == 7.0).all() and (fv[:, p] == 7.0).all()
+    keep = [p for p in range(n_ctx + 1) if p not in set(sel.tolist())]
+    full = eng.assemble_context(ids)
+    assert torch.equal(fk[:, keep], full.k[:, keep]) and torch.equal(fv[:, keep], full.v[:, keep])

@@ -20,7 +20,7 @@ for shape in "6400 12288 4096 9" "6400 4096 4096 0" "6400 14336 4096 1" "6400 40
   ncu --set full --clock-control none -k regex:"gemm_tc|gemm_skc|splitk" -s 2 -c 2 --csv --page raw \
       python tools/one_gemm.py $1 $2 $3 $4 > $OUT/gemm_$1x$2x$3.csv 2> /dev/null
 done
-for k in "attn:attn_tc_kernel:15:8" "score1:score_tc_kernel:0:8" "score2:score_tc_kernel:1:8" "layernorm:layernorm:40:8" \
+for k in "attn:attn_tc4_kernel:15:8" "score1:score_tc_kernel:0:8" "score2:score_tc_kernel:1:8" "layernorm:layernorm:40:8" \
          "assemble:assemble:0:8" "topn:topn:0:8" "attn_single:attn_tc_kernel:15:1"; do
   IFS=: read name regex skip batch <<< "$k"
   ncu --nvtx --nvtx-include "profile_step/" --set full --import-source on --clock-control none -k regex:$regex \
