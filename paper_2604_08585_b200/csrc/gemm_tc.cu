@@ -1188,10 +1188,23 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
 }
 
 // swapped 2-CTA kernel: activation tile width (multiple of 16, <= 256) and count
-// minimising waves x (width + per-unit overhead); returns that cost in the same
-// units as the normal 256 x 256 pair schedule (pair_cost)
+// minimising waves x (width + 256), the shared-memory traffic of a k-block in
+// 128-byte rows: per CTA the TMA writes and the MMA reads the 128 weight rows and
+// width/2 activation rows, 2 x (128 + width/2) rows against the SM's ~128 B/clk,
+// which exceeds the MMA's own 2 x width cycles for every width < 256 (ncu, M = 800:
+// the tensor pipe ~66% active; tools/mma_bench.cu). Same units as pair_cost.
+// (The former waves x (width + 24) model picked 6 x 144 rows for the M = 800 QKV
+// instead of 4 x 208.)
 // (tiles narrower than 128 activation rows stream too many weight bytes per flop:
 // at M = 256 the 64-wide plan measured slower than 1-CTA 128 x 64 tiles)
+static double swap_overhead() {   // QCF_SWAP_OVH: the model's per-k-block constant (measurement)
+  static int ovh = -1;
+  if (ovh < 0) {
+    const char* e = getenv("QCF_SWAP_OVH");
+    ovh = e ? std::max(0, atoi(e)) : 256;
+  }
+  return (double)ovh;
+}
 static double swap_plan(int64_t m, int64_t n, int& bna, int& n_act, int min_w = 128) {
   const int64_t clusters = sm_count() / 2, wp = (n + 255) / 256;
   static int force_na = -1;   // QCF_SWAP_NA: force the activation tile count (measurement)
@@ -1212,7 +1225,7 @@ static double swap_plan(int64_t m, int64_t n, int& bna, int& n_act, int min_w = 
     const int64_t w = ((m + na - 1) / na + 15) / 16 * 16;
     if (w > 256 || w < std::min<int64_t>(min_w, (m + 15) / 16 * 16)) continue;
     const int64_t units = wp * na;
-    const double cost = (double)((units + clusters - 1) / clusters) * (double)(w + 24);
+    const double cost = (double)((units + clusters - 1) / clusters) * (double)(w + swap_overhead());
     if (cost < best - 1e-9) {
       best = cost;
       bna = (int)w;
@@ -1223,7 +1236,7 @@ static double swap_plan(int64_t m, int64_t n, int& bna, int& n_act, int min_w = 
 }
 static double pair_cost(int64_t m, int64_t n) {
   const int64_t clusters = sm_count() / 2, units = ((m + 255) / 256) * ((n + 255) / 256);
-  return (double)((units + clusters - 1) / clusters) * (256.0 + 24.0);
+  return (double)((units + clusters - 1) / clusters) * (256.0 + swap_overhead());
 }
 
 static int launch_swap(const void* a, int64_t lda, const void* w, int64_t ldb, void* c, int64_t ldc, int64_t m,
