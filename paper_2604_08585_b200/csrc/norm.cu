@@ -178,47 +178,6 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(float* __restrict
   }
 }
 
-// One warp per row (bf16 output, x already holding the residual sum): d/128 float4
-// per lane in registers, both reductions by warp shuffles -- no block barriers, so a
-// few-hundred-row LayerNorm (one request's 800 recompute rows, the probe's 32) pays
-// one load round trip instead of the block kernel's load + 2 barrier phases.
-template <int NV>
-__global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __restrict__ x, int64_t m, int d,
-                                                             const float* __restrict__ g,
-                                                             const float* __restrict__ b, float eps,
-                                                             __nv_bfloat16* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= m) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * d);
-  float4 v[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  const float mean = warp_sum(s) / d;
-  float qs = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
-    qs += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
-  }
-  const float sd = sqrtf(warp_sum(qs) / d + eps);  // numpy: (x - mean) / sqrt(var + eps) * g + b (model.py:308)
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(b);
-  __nv_bfloat16* orow = out + row * d;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int e = lane + 32 * i;
-    const float4 gv = __ldg(g4 + e), bv = __ldg(b4 + e);
-    store4<__nv_bfloat16>(orow + 4 * e, ((v[i].x - mean) / sd) * gv.x + bv.x, ((v[i].y - mean) / sd) * gv.y + bv.y,
-                          ((v[i].z - mean) / sd) * gv.z + bv.z, ((v[i].w - mean) / sd) * gv.w + bv.w);
-  }
-}
-
 // rows per CTA: 2 for one request's ~800 rows (18.4 -> 14.5 us), 1 for the probe's
 // 32 / 256 rows (256: 10.2 vs 12.3 us) and the batch's 6400 (63.5 vs 65.6 us); 4 rows
 // per CTA was slower everywhere (tools/ln_bench.py). QCF_LN_ROWS=1/2 forces it.
@@ -244,31 +203,6 @@ static int launch_ln_vec(float* x, const float* delta, int64_t m, int d, const f
   if (g_ln_rows < 0) {
     const char* e = getenv("QCF_LN_ROWS");
     g_ln_rows = e ? ((atoi(e) == 2) ? 2 : 1) : 0;  // 0 = by row count
-  }
-  static int warp_rows = -1;   // QCF_LN_WARP=0: block kernels only
-  if (warp_rows < 0) {
-    const char* e = getenv("QCF_LN_WARP");
-    warp_rows = e ? atoi(e) : 1;
-  }
-  if constexpr (sizeof(T) == 2) {
-    if (warp_rows && !delta && m <= 2048 && d % 128 == 0) {
-      const unsigned grid = (unsigned)((m + 7) / 8);
-      switch (d / 128) {
-        case 32:
-          QCF_LAUNCH("layernorm_warp_kernel", layernorm_warp_kernel<32>, dim3(grid), dim3(256), 0, s, x, m, d, g, b, eps,
-                     (__nv_bfloat16*)out);
-          return QCF_OK;
-        case 8:
-          QCF_LAUNCH("layernorm_warp_kernel", layernorm_warp_kernel<8>, dim3(grid), dim3(256), 0, s, x, m, d, g, b, eps,
-                     (__nv_bfloat16*)out);
-          return QCF_OK;
-        case 2:
-          QCF_LAUNCH("layernorm_warp_kernel", layernorm_warp_kernel<2>, dim3(grid), dim3(256), 0, s, x, m, d, g, b, eps,
-                     (__nv_bfloat16*)out);
-          return QCF_OK;
-        default: break;
-      }
-    }
   }
   const bool two = g_ln_rows == 2 || (g_ln_rows == 0 && m >= 512 && m <= 2048);
   if (two && d / 4 <= 4 * LN_THREADS) return launch_ln_rows<T, 2>(x, delta, m, d, g, b, eps, out, s);
