@@ -1177,9 +1177,17 @@ static int launch_pair(const CUtensorMap& ma, const void* b, int64_t ldb, void* 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  // raster band of m pairs (QCF_GEMM_GROUP); default = all m pairs (m fastest). Bands
-  // of 4-12 were within run-to-run noise at the fused-path shapes (tools/group_sweep.sh)
-  const int group_m = g_group_m > 0 ? g_group_m : (int)((m + PM - 1) / PM);
+  // raster band of m pairs (QCF_GEMM_GROUP overrides): the fewest equal bands whose A
+  // rows (PM x K bf16 per pair) stay under 32 MB, so a band's activations remain in L2
+  // while every weight tile streams past them once per band -- the batch QKV / W1 (25
+  // pairs, K = 4096) run as 13 + 12: DRAM reads 518 -> 291 MB and 493 -> 312 MB per
+  // launch, 453 -> 436 and 509 -> 492 us (ncu, profiles/r2s3_gemm_group_ab.txt). With
+  // all 25 pairs in one band the 157-183 MB of outputs pushed the 52 MB of A out of
+  // L2 between waves.
+  const int64_t m_pairs = (m + PM - 1) / PM;
+  const int64_t max_g = std::max<int64_t>(1, (int64_t)(32e6 / ((double)PM * (double)k * 2.0)));
+  const int64_t bands = (m_pairs + max_g - 1) / max_g;
+  const int group_m = g_group_m > 0 ? g_group_m : (int)((m_pairs + bands - 1) / bands);
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, PM>, ma_pair, mb, c, ldc, (int)m, (int)n, (int)k, ea, sk, sk_flags,
                                      sk_part, group_m);
   if (e != cudaSuccess) return cuda_status(e, "qcf_gemm(tcgen05 pair)");
