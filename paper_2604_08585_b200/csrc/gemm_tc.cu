@@ -1287,7 +1287,11 @@ static int launch_swap(const void* a, int64_t lda, const void* w, int64_t ldb, v
   // order: every wave then shares the whole activation matrix from L2 (banding measured
   // +1% TTFT there); the batch's 6400-row operands are banded
   const bool big = (double)m * (double)k * 2.0 > 48e6;
-  int gw = g_swap_group > 0 ? g_swap_group : (big ? (int)std::lround(std::sqrt((double)clusters)) : 1);
+  // all weight pairs in one band when the whole weight matrix fits in L2 beside the wave's
+  // activation slabs (the batch W_o, 4096 x 4096: DRAM 253 -> 223 MB per launch, ncu)
+  const bool w_fits = (double)n * (double)k * 2.0 <= 40e6;
+  int gw = g_swap_group > 0 ? g_swap_group
+                            : (big ? (w_fits ? n_wp : (int)std::lround(std::sqrt((double)clusters))) : 1);
   gw = std::max(1, std::min(gw, n_wp));
   // (L2 priority hints -- evict_last on the band's weights, evict_first on the
   // activations -- were measured WORSE: 1909 vs 1047 MB at W2, since the wave's
