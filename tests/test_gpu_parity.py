@@ -431,6 +431,37 @@ def test_batched_prefill_equals_single_requests(tmp_path, dtype):
             assert np.abs(blog - logits).max() < 5e-2 * np.abs(logits).max()
 
 
+@pytest.mark.parametrize("knob", [4, 8])
+def test_batched_prefill_attention_kernels(tmp_path, knob):
+    """The batch's attention kernels inside the engine: a bf16 batch run with the
+    two-CTAs-per-SM kernel (knob 4, the auto choice for the benchmarked batch) or
+    the two-softmax-group kernel (knob 8) tracks each request's single-request run
+    (single-tile kernel) within the bf16 tolerance of the batched test above."""
+    import paper_2604_08585_b200 as Q
+    from paper_2604_08585_b200 import _lib
+    cfg = Q.ModelConfig(n_layers=4, n_heads=4, d_model=512, d_head=128, d_ff=1024, seed=97)
+    w = Q.init_weights(cfg, dtype="bf16")
+    store = Q.ChunkStore(tmp_path / "s", cfg, dtype="bf16", persist=False)
+    eng = Q.FusionEngine(w, store)
+    pool = [store.precompute(w, np.random.default_rng(i).integers(0, 256, 256), 0.05).chunk_id for i in range(6)]
+    rng = np.random.default_rng(7)
+    reqs = [[pool[j] for j in rng.permutation(6)[:4]] for _ in range(4)]
+    queries = [rng.integers(0, 256, 16).tolist() for _ in range(4)]
+    singles = [eng.fuse(queries[r], reqs[r], 0.2) for r in range(4)]
+    _lib.call("qcf_set_attention_kernel", knob)
+    try:
+        plans, b = eng.prefill_batch("QCFuse", 0.2, reqs, queries, use_graph=False)
+        torch.cuda.synchronize()
+    finally:
+        _lib.call("qcf_set_attention_kernel", 0)
+    n_sel = plans[0].n_sel
+    for r, (logits, sel) in enumerate(singles):
+        bsel = b.rc_pos[r * b.Mr:r * b.Mr + n_sel].cpu().numpy()
+        blog = b.logits[r].cpu().numpy()
+        assert len(set(bsel.tolist()) & set(sel.tolist())) >= 0.9 * n_sel, r
+        assert np.abs(blog - logits).max() < 5e-2 * np.abs(logits).max(), r
+
+
 # ---------------------------------------------------------------- GQA extension (BASELINE configs[3] shape family)
 def _gqa_case(tmp_path, dtype, H, Hkv, D, d_ff, lens, q, ratio, seed=5):
     import paper_2604_08585_b200 as Q
