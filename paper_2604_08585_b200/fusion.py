@@ -537,7 +537,7 @@ class FusionEngine:
         # True: the whole assembly may also overlap the probe (both HBM-bound); QCF_ASM_CONCURRENT=1
         self.concurrent = os.environ.get("QCF_ASM_CONCURRENT", "0") == "1"
         self.asm_skip = os.environ.get("QCF_ASM_SKIP", "1") != "0"
-        self.asm_group = 4        # layers per side-stream assembly launch
+        self.asm_group = int(os.environ.get("QCF_ASM_GROUP", "4"))   # layers per side-stream assembly launch
         # False: assembly on the main stream, in order (instrumented passes; QCF_PIPELINE_ASM=0)
         self.pipeline_asm = os.environ.get("QCF_PIPELINE_ASM", "1") != "0"
         self.decode_graph = True  # greedy decode as a replayed CUDA graph (False: eager loop)
